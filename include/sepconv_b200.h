@@ -1,0 +1,124 @@
+/*
+ * sepconv_b200.h -- C ABI of libsepconv_b200.so, the B200 (sm_100a) implementation
+ * of the separable (2r+1)-tap convolution hot path of sepconv_lab
+ * (S/ = /root/reference/pkg/src/sepconv_lab/, the reference being arXiv 1711.09791's
+ * lab). Plain pointers and sizes only; no torch types.
+ *
+ * Layout: a stack of `nplanes` float32 planes; element (p, y, x) lives at
+ *   base + p*plane_stride + y*row_stride + x        (strides in ELEMENTS)
+ * The reference's Image is a list of C-contiguous (rows, cols) planes
+ * (S/image.py:26-75); a (P, R, C) buffer is plane_stride = R*C, row_stride = C.
+ *
+ * All device entry points take DEVICE pointers and a cudaStream_t (as void*),
+ * are stream-ordered and asynchronous, validate everything before launching and
+ * never allocate or free caller buffers. `sc_two_pass_host_f32` takes HOST
+ * pointers and blocks, like the reference's launches (S/executors.py:142-151).
+ *
+ * Arithmetic is bit-identical to the reference: float32 multiply and add, never
+ * fused, folded in the reference order (S/conv.py:1-15).
+ */
+#ifndef SEPCONV_B200_H
+#define SEPCONV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the Python layer maps them onto the reference's exceptions
+ * (S/errors.py:4-42). Validation happens before any launch. */
+#define SC_OK 0
+#define SC_INVALID_ARGUMENT 1  /* InvalidArgumentError: shapes, ranges, aliasing (S/conv.py:68-75) */
+#define SC_INVALID_DIMENSION 2 /* InvalidDimensionError: plane smaller than the kernel (S/conv.py:76-79) */
+#define SC_UNSUPPORTED_WIDTH 3 /* UnsupportedWidthError: width outside 1..9 (odd) */
+#define SC_CUDA_ERROR 4        /* ExecutionError: a launch or copy failed (S/errors.py:36-42) */
+
+/* Flags */
+#define SC_EXTENDED 0x1  /* row pass over every row: conv_two_pass(extended=True), S/conv.py:417-418 */
+#define SC_NO_RING 0x2   /* fused two-pass: leave dst outside the valid region untouched */
+#define SC_ZERO_FILL 0x4 /* row pass: dst outside the computed region := 0 (zeroed scratch, S/conv.py:414) */
+#define SC_COPY_BACK 0x8 /* single pass: also copy the valid region back into src (S/conv.py:424-449) */
+
+int sc_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char *sc_last_error(void);
+/* Number of kernels this library has launched in this process. */
+uint64_t sc_launch_count(void);
+
+/* Fused single-read / single-write two-pass, out of place (src and dst must not overlap).
+ * dst = the image the reference leaves in `image` after conv_two_pass
+ * (S/conv.py:392-421) / convolve_image(TWO_PASS) (S/executors.py:308-326):
+ * ring (outside [r,R-r)x[r,C-r)) = src, valid region = V(H0) with H0 zero on rows
+ * outside [r,R-r) unless SC_EXTENDED. With SC_NO_RING the dst ring is untouched. */
+int sc_two_pass_fused_f32(const float *src, float *dst, int nplanes, int rows, int cols,
+                          int64_t src_plane_stride, int64_t dst_plane_stride,
+                          int64_t src_row_stride, int64_t dst_row_stride,
+                          const float *taps, int width, int flags, void *stream);
+
+/* Row-band form of the fused two-pass for the multi-GPU partitioner: the image is
+ * global_rows tall; src holds global rows [src_row0, src_row0+src_rows) (the band
+ * plus its r-row halo), dst row 0 is global row dst_row0; output rows
+ * [out_lo, out_hi) are produced with the faithful rule and ring in GLOBAL rows. */
+int sc_two_pass_band_f32(const float *src, float *dst, int nplanes, int global_rows, int cols,
+                         int64_t src_plane_stride, int64_t dst_plane_stride,
+                         int64_t src_row_stride, int64_t dst_row_stride,
+                         int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
+                         const float *taps, int width, int flags, void *stream);
+
+/* horizontal_rows_vec over rows [row_lo,row_hi) (S/conv.py:215-240; public
+ * horizontal_pass uses [r, R-r), S/conv.py:362-375). SC_ZERO_FILL also zeroes
+ * every other dst element (the two-pass scratch convention). */
+int sc_hpass_f32(const float *src, float *dst, int nplanes, int rows, int cols,
+                 int64_t src_plane_stride, int64_t dst_plane_stride,
+                 int64_t src_row_stride, int64_t dst_row_stride,
+                 int row_lo, int row_hi, const float *taps, int width, int flags, void *stream);
+
+/* vertical_rows_vec over rows [row_lo,row_hi) within [r, R-r) (S/conv.py:269-293). */
+int sc_vpass_f32(const float *src, float *dst, int nplanes, int rows, int cols,
+                 int64_t src_plane_stride, int64_t dst_plane_stride,
+                 int64_t src_row_stride, int64_t dst_row_stride,
+                 int row_lo, int row_hi, const float *taps, int width, int flags, void *stream);
+
+/* The reference two-pass with its exact buffer semantics, two launches:
+ * scratch := H0 (zero outside the row-pass region), then image[valid] := V(scratch).
+ * image ring untouched. conv_two_pass(plane, kernel, scratch, extended), S/conv.py:392-421. */
+int sc_two_pass_split_f32(float *image, float *scratch, int nplanes, int rows, int cols,
+                          int64_t image_plane_stride, int64_t scratch_plane_stride,
+                          int64_t image_row_stride, int64_t scratch_row_stride,
+                          const float *taps, int width, int flags, void *stream);
+
+/* Single pass with the dense width x width matrix (row-major, pass the reference's
+ * outer_product(k).matrix, S/kernels.py:66-72): dst[valid] := D, dst ring untouched
+ * (single_pass_rows_vec S/conv.py:86-114 == unrolled5 :146-175). SC_COPY_BACK then
+ * copies dst[valid] into src[valid] (S/executors.py:330-331). */
+int sc_single_pass_f32(float *src, float *dst, int nplanes, int rows, int cols,
+                       int64_t src_plane_stride, int64_t dst_plane_stride,
+                       int64_t src_row_stride, int64_t dst_row_stride,
+                       const float *dense, int width, int flags, void *stream);
+
+/* copy_back (S/conv.py:424-440): dst[rows lo..hi, cols lo..hi] := src[...]. */
+int sc_copy_region_f32(const float *src, float *dst, int nplanes, int rows, int cols,
+                       int64_t src_plane_stride, int64_t dst_plane_stride,
+                       int64_t src_row_stride, int64_t dst_row_stride,
+                       int row_lo, int row_hi, int col_lo, int col_hi, void *stream);
+
+/* Deterministic inputs: splitmix64 draw (offset+i) of `seed` (S/image.py:131-141)
+ * mapped by kind: 0 -> [0,256) as make_synthetic (S/image.py:158-160),
+ * 1 -> U[0,1), 2 -> U[0,255). */
+int sc_fill_synthetic_f32(float *dst, int64_t count, uint64_t seed, uint64_t offset, int kind,
+                          void *stream);
+
+/* End-to-end two-pass on HOST planes (the reference's Image: one pointer per
+ * C-contiguous plane): streams row chunks H2D -> fused kernel -> D2H on three
+ * CUDA streams with double/triple buffering, on `device`. In-place
+ * (dst_planes == src_planes) is allowed, as in conv_two_pass. Pinned host memory
+ * gives full PCIe rate; pageable memory works at lower rate. Blocks until done. */
+int sc_two_pass_host_f32(const float *const *src_planes, float *const *dst_planes, int nplanes,
+                         int rows, int cols, const float *taps, int width, int flags, int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEPCONV_B200_H */

@@ -1,0 +1,468 @@
+// capi.cu -- C ABI of libsepconv_b200.so (declared in include/sepconv_b200.h).
+//
+// Validation mirrors the reference's checks before any launch:
+//   shape/stride/range errors and aliasing -> SC_INVALID_ARGUMENT (S/conv.py:68-75)
+//   plane smaller than the kernel          -> SC_INVALID_DIMENSION (S/conv.py:76-79)
+//   width not odd in 1..9                  -> SC_UNSUPPORTED_WIDTH
+// then plans the launch (strip width, row-band height, persistent grid) for the
+// device that owns the buffers.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "../../include/sepconv_b200.h"
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace sc {
+
+static thread_local std::string t_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_err = msg; }
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static int fail(int code, const std::string& msg) {
+    set_error(msg);
+    return code;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+    return fail(SC_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    return std::atoi(v);
+}
+
+// --------------------------------------------------------------------------
+// Device of a pointer (the caller's buffers decide where we launch)
+
+static int select_device(const void* ptr) {
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged) return -1;
+    cudaSetDevice(attr.device);
+    return attr.device;
+}
+
+struct DevInfo {
+    int sms = 0;
+};
+
+static DevInfo dev_info(int dev) {
+    static std::mutex mu;
+    static std::map<int, DevInfo> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    DevInfo d;
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = d;
+    return d;
+}
+
+static int occupancy(const void* kern, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(kern, threads, smem, dev);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 1;
+    }
+    if (occ < 1) occ = 1;
+    cache[key] = occ;
+    return occ;
+}
+
+// --------------------------------------------------------------------------
+// Planner
+
+// Consumer threads per CTA: strip width TW = 4*nt; minimise padding columns.
+static int choose_nt(int C) {
+    int forced = env_int("SC_NT", 0);
+    if (forced >= 32 && forced <= 256 && forced % 32 == 0) return forced;
+    static const int cand[] = {128, 96, 160, 64, 192, 256, 32};
+    int best = 128;
+    long long best_waste = -1;
+    for (int nt : cand) {
+        const long long tw = 4LL * nt;
+        const long long strips = (C + tw - 1) / tw;
+        const long long waste = strips * tw - C;
+        if (best_waste < 0 || waste < best_waste) {
+            best_waste = waste;
+            best = nt;
+        }
+    }
+    return best;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int launch_rows(const RowsJob& j, cudaStream_t s) {
+    const int rad = j.width / 2;
+    const void* kern = nullptr;
+    const bool aligned = (j.C % 4 == 0) && aligned16(j.src) && aligned16(j.dst) && (j.sps % 4 == 0) &&
+                         (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) &&
+                         env_int("SC_FORCE_GENERIC", 0) == 0;
+    switch (j.mode) {
+        case MODE_FUSED: kern = kernel_fused(rad, aligned); break;
+        case MODE_HPASS: kern = kernel_hpass(rad, aligned); break;
+        case MODE_VPASS: kern = kernel_vpass(rad, aligned); break;
+        case MODE_SINGLE: kern = kernel_single(rad, aligned); break;
+    }
+    if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(j.width));
+    if (j.out_hi <= j.out_lo || j.nplanes <= 0) return SC_OK;
+
+    Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.src = j.src;
+    p.dst = j.dst;
+    p.src_plane_stride = j.sps;
+    p.dst_plane_stride = j.dps;
+    p.src_row_stride = j.srs;
+    p.dst_row_stride = j.drs;
+    p.nplanes = j.nplanes;
+    p.R = j.R;
+    p.C = j.C;
+    p.src_row0 = j.src_row0;
+    p.src_rows = j.src_rows;
+    p.dst_row0 = j.dst_row0;
+    p.out_lo = j.out_lo;
+    p.out_hi = j.out_hi;
+    p.hrow_lo = j.hrow_lo;
+    p.hrow_hi = j.hrow_hi;
+    p.flags = j.flags;
+    for (int i = 0; i < j.width; ++i) p.w[i] = j.taps ? j.taps[i] : 0.0f;
+    if (j.dense)
+        for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];
+
+    const int nt = choose_nt(j.C);
+    p.tw = 4 * nt;
+    p.nstrips = (j.C + p.tw - 1) / p.tw;
+    int nr = env_int("SC_NR", 16);
+    if (nr < 2 * rad + 4) nr = 2 * rad + 4;
+    if (nr > 64) nr = 64;
+    p.nr = nr;
+    const int threads = 32 + nt;
+    const size_t smem = (size_t)((2 * nr * 8 + 127) / 128) * 128 + (size_t)nr * (p.tw + 2 * HALO) * 4;
+
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const DevInfo di = dev_info(dev);
+    int occ = occupancy(kern, threads, smem);
+    const int occ_cap = env_int("SC_OCC", 0);
+    if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;
+    const long long G = (long long)di.sms * occ;
+
+    // Row-band height: minimise (waves x rows per item), each item re-reading a
+    // 2r-row halo plus a fixed pipeline ramp worth ~8 rows.
+    const int rows_out = j.out_hi - j.out_lo;
+    const long long units = (long long)j.nplanes * p.nstrips;
+    int band_h = env_int("SC_BAND_H", 0);
+    if (band_h <= 0) {
+        const int min_bh = 8;
+        const int max_nb = rows_out / min_bh > 1 ? rows_out / min_bh : 1;
+        long long best_cost = -1;
+        int best_bh = rows_out;
+        for (int nb = 1; nb <= max_nb; ++nb) {
+            const int bh = (rows_out + nb - 1) / nb;
+            const long long nb_eff = (rows_out + bh - 1) / bh;
+            const long long items = units * nb_eff;
+            const long long waves = (items + G - 1) / G;
+            const long long cost = waves * (bh + 2 * rad + 8);
+            if (best_cost < 0 || cost < best_cost) {
+                best_cost = cost;
+                best_bh = bh;
+            }
+        }
+        band_h = best_bh;
+    }
+    p.band_h = band_h;
+    const long long nbands = (rows_out + band_h - 1) / band_h;
+    const long long nitems = units * nbands;
+    if (nitems > 0x7fffffffLL) return fail(SC_INVALID_ARGUMENT, "too many work items");
+    p.nitems = (int)nitems;
+    const int grid = (int)(nitems < G ? nitems : G);
+
+    void* args[] = {&p};
+    cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    count_launch();
+    if (env_int("SC_DEBUG_PLAN", 0))
+        std::fprintf(stderr, "[sc] mode=%d rad=%d aligned=%d nt=%d tw=%d strips=%d band_h=%d items=%d grid=%d occ=%d smem=%zu\n",
+                     j.mode, rad, (int)aligned, nt, p.tw, p.nstrips, band_h, p.nitems, grid, occ, smem);
+    return SC_OK;
+}
+
+// --------------------------------------------------------------------------
+// Validation helpers
+
+static int check_width(int width) {
+    if (width < 1 || width % 2 == 0)
+        return fail(SC_INVALID_ARGUMENT, "kernel width must be odd and >= 1, got " + std::to_string(width));
+    if (width > MAX_W)
+        return fail(SC_UNSUPPORTED_WIDTH, "kernel width " + std::to_string(width) + " > 9 not supported");
+    return SC_OK;
+}
+
+static int check_dims(int nplanes, int rows, int cols, int width) {
+    if (nplanes < 1 || rows < 1 || cols < 1)
+        return fail(SC_INVALID_ARGUMENT, "plane count and dimensions must be positive");
+    if (rows < width || cols < width)
+        return fail(SC_INVALID_DIMENSION, "plane " + std::to_string(rows) + "x" + std::to_string(cols) +
+                                              " smaller than kernel width " + std::to_string(width));
+    return SC_OK;
+}
+
+static int check_strides(int nplanes, int rows, int cols, long long ps, long long rs, const char* what) {
+    if (rs < cols || (nplanes > 1 && ps < (long long)rows * rs))
+        return fail(SC_INVALID_ARGUMENT, std::string(what) + ": strides overlap rows or planes");
+    return SC_OK;
+}
+
+static long long extent_bytes(int nplanes, int rows, int cols, long long ps, long long rs) {
+    return ((long long)(nplanes - 1) * ps + (long long)(rows - 1) * rs + cols) * 4LL;
+}
+
+static bool overlaps(const void* a, long long na, const void* b, long long nb) {
+    const char* pa = static_cast<const char*>(a);
+    const char* pb = static_cast<const char*>(b);
+    return pa < pb + nb && pb < pa + na;
+}
+
+static int prepare(const void* ptr) {
+    if (!ptr) return fail(SC_INVALID_ARGUMENT, "null buffer");
+    if (select_device(ptr) < 0) return fail(SC_INVALID_ARGUMENT, "buffer is not device memory");
+    return SC_OK;
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+#define SC_TRY(x)                \
+    do {                         \
+        int _rc = (x);           \
+        if (_rc != SC_OK) return _rc; \
+    } while (0)
+
+extern "C" {
+
+int sc_abi_version(void) { return 1; }
+
+const char* sc_last_error(void) { return t_err.c_str(); }
+
+uint64_t sc_launch_count(void) { return g_launches.load(); }
+
+int sc_two_pass_band_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
+                         int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                         int64_t dst_row_stride, int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
+                         const float* taps, int width, int flags, void* stream) {
+    set_error("");
+    SC_TRY(check_width(width));
+    SC_TRY(check_dims(nplanes, global_rows, cols, width));
+    if (!taps) return fail(SC_INVALID_ARGUMENT, "null taps");
+    const int r = width / 2;
+    if (out_lo < 0 || out_hi > global_rows || out_lo > out_hi)
+        return fail(SC_INVALID_ARGUMENT, "output rows out of range");
+    const int need_lo = out_lo - r > 0 ? out_lo - r : 0;
+    const int need_hi = out_hi + r < global_rows ? out_hi + r : global_rows;
+    if (out_hi > out_lo && (src_row0 > need_lo || src_row0 + src_rows < need_hi || src_row0 < 0 ||
+                            src_row0 + src_rows > global_rows))
+        return fail(SC_INVALID_ARGUMENT, "source band does not cover the output rows plus halo");
+    if (dst_row0 > out_lo) return fail(SC_INVALID_ARGUMENT, "destination band starts after the output rows");
+    SC_TRY(check_strides(nplanes, src_rows, cols, src_plane_stride, src_row_stride, "src"));
+    SC_TRY(check_strides(nplanes, out_hi - dst_row0, cols, dst_plane_stride, dst_row_stride, "dst"));
+    SC_TRY(prepare(src));
+    SC_TRY(prepare(dst));
+    if (overlaps(src, extent_bytes(nplanes, src_rows, cols, src_plane_stride, src_row_stride), dst,
+                 extent_bytes(nplanes, out_hi - dst_row0, cols, dst_plane_stride, dst_row_stride)))
+        return fail(SC_INVALID_ARGUMENT, "source and destination must be distinct buffers");
+    RowsJob j{};
+    j.mode = MODE_FUSED;
+    j.src = src;
+    j.dst = dst;
+    j.sps = src_plane_stride;
+    j.dps = dst_plane_stride;
+    j.srs = src_row_stride;
+    j.drs = dst_row_stride;
+    j.nplanes = nplanes;
+    j.R = global_rows;
+    j.C = cols;
+    j.src_row0 = src_row0;
+    j.src_rows = src_rows;
+    j.dst_row0 = dst_row0;
+    j.out_lo = out_lo;
+    j.out_hi = out_hi;
+    j.hrow_lo = (flags & SC_EXTENDED) ? 0 : r;
+    j.hrow_hi = (flags & SC_EXTENDED) ? global_rows : global_rows - r;
+    j.flags = flags;
+    j.width = width;
+    j.taps = taps;
+    return launch_rows(j, static_cast<cudaStream_t>(stream));
+}
+
+int sc_two_pass_fused_f32(const float* src, float* dst, int nplanes, int rows, int cols, int64_t src_plane_stride,
+                          int64_t dst_plane_stride, int64_t src_row_stride, int64_t dst_row_stride,
+                          const float* taps, int width, int flags, void* stream) {
+    return sc_two_pass_band_f32(src, dst, nplanes, rows, cols, src_plane_stride, dst_plane_stride, src_row_stride,
+                                dst_row_stride, 0, rows, 0, 0, rows, taps, width, flags, stream);
+}
+
+static int pass_common(int mode, const float* src, float* dst, int nplanes, int rows, int cols, int64_t sps,
+                       int64_t dps, int64_t srs, int64_t drs, int row_lo, int row_hi, const float* taps,
+                       const float* dense, int width, int flags, void* stream) {
+    SC_TRY(check_width(width));
+    SC_TRY(check_dims(nplanes, rows, cols, width));
+    if (mode == MODE_SINGLE ? !dense : !taps) return fail(SC_INVALID_ARGUMENT, "null taps");
+    SC_TRY(check_strides(nplanes, rows, cols, sps, srs, "src"));
+    SC_TRY(check_strides(nplanes, rows, cols, dps, drs, "dst"));
+    const int r = width / 2;
+    if (mode == MODE_HPASS) {
+        if (row_lo < 0 || row_hi > rows || row_lo > row_hi)
+            return fail(SC_INVALID_ARGUMENT, "row range out of bounds");
+    } else {
+        if (row_lo > row_hi || (row_hi > row_lo && (row_lo < r || row_hi > rows - r)))
+            return fail(SC_INVALID_ARGUMENT, "row range must lie inside the valid rows");
+    }
+    SC_TRY(prepare(src));
+    SC_TRY(prepare(dst));
+    if (overlaps(src, extent_bytes(nplanes, rows, cols, sps, srs), dst, extent_bytes(nplanes, rows, cols, dps, drs)))
+        return fail(SC_INVALID_ARGUMENT, "source and destination must be distinct buffers");
+    RowsJob j{};
+    j.mode = mode;
+    j.src = src;
+    j.dst = dst;
+    j.sps = sps;
+    j.dps = dps;
+    j.srs = srs;
+    j.drs = drs;
+    j.nplanes = nplanes;
+    j.R = rows;
+    j.C = cols;
+    j.src_row0 = 0;
+    j.src_rows = rows;
+    j.dst_row0 = 0;
+    j.hrow_lo = row_lo;
+    j.hrow_hi = row_hi;
+    if (mode == MODE_HPASS && (flags & SC_ZERO_FILL)) {
+        j.out_lo = 0;
+        j.out_hi = rows;
+    } else {
+        j.out_lo = row_lo;
+        j.out_hi = row_hi;
+    }
+    j.flags = flags;
+    j.width = width;
+    j.taps = taps;
+    j.dense = dense;
+    if (mode == MODE_SINGLE) {
+        static float zeros[MAX_W] = {0};
+        j.taps = zeros;
+    }
+    return launch_rows(j, static_cast<cudaStream_t>(stream));
+}
+
+int sc_hpass_f32(const float* src, float* dst, int nplanes, int rows, int cols, int64_t src_plane_stride,
+                 int64_t dst_plane_stride, int64_t src_row_stride, int64_t dst_row_stride, int row_lo, int row_hi,
+                 const float* taps, int width, int flags, void* stream) {
+    set_error("");
+    return pass_common(MODE_HPASS, src, dst, nplanes, rows, cols, src_plane_stride, dst_plane_stride,
+                       src_row_stride, dst_row_stride, row_lo, row_hi, taps, nullptr, width, flags, stream);
+}
+
+int sc_vpass_f32(const float* src, float* dst, int nplanes, int rows, int cols, int64_t src_plane_stride,
+                 int64_t dst_plane_stride, int64_t src_row_stride, int64_t dst_row_stride, int row_lo, int row_hi,
+                 const float* taps, int width, int flags, void* stream) {
+    set_error("");
+    return pass_common(MODE_VPASS, src, dst, nplanes, rows, cols, src_plane_stride, dst_plane_stride,
+                       src_row_stride, dst_row_stride, row_lo, row_hi, taps, nullptr, width, flags, stream);
+}
+
+int sc_two_pass_split_f32(float* image, float* scratch, int nplanes, int rows, int cols, int64_t image_plane_stride,
+                          int64_t scratch_plane_stride, int64_t image_row_stride, int64_t scratch_row_stride,
+                          const float* taps, int width, int flags, void* stream) {
+    set_error("");
+    SC_TRY(check_width(width));
+    SC_TRY(check_dims(nplanes, rows, cols, width));
+    const int r = width / 2;
+    const int h_lo = (flags & SC_EXTENDED) ? 0 : r;
+    const int h_hi = (flags & SC_EXTENDED) ? rows : rows - r;
+    SC_TRY(pass_common(MODE_HPASS, image, scratch, nplanes, rows, cols, image_plane_stride, scratch_plane_stride,
+                       image_row_stride, scratch_row_stride, h_lo, h_hi, taps, nullptr, width, SC_ZERO_FILL,
+                       stream));
+    return pass_common(MODE_VPASS, scratch, image, nplanes, rows, cols, scratch_plane_stride, image_plane_stride,
+                       scratch_row_stride, image_row_stride, r, rows - r, taps, nullptr, width, 0, stream);
+}
+
+int sc_single_pass_f32(float* src, float* dst, int nplanes, int rows, int cols, int64_t src_plane_stride,
+                       int64_t dst_plane_stride, int64_t src_row_stride, int64_t dst_row_stride, const float* dense,
+                       int width, int flags, void* stream) {
+    set_error("");
+    SC_TRY(check_width(width));
+    SC_TRY(check_dims(nplanes, rows, cols, width));
+    const int r = width / 2;
+    SC_TRY(pass_common(MODE_SINGLE, src, dst, nplanes, rows, cols, src_plane_stride, dst_plane_stride,
+                       src_row_stride, dst_row_stride, r, rows - r, nullptr, dense, width, flags, stream));
+    if (flags & SC_COPY_BACK) {
+        cudaError_t e = launch_copy_region(dst, src, dst_plane_stride, src_plane_stride, dst_row_stride,
+                                           src_row_stride, nplanes, r, rows - 2 * r, r, cols - 2 * r,
+                                           static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return cuda_fail(e, "copy-back launch");
+    }
+    return SC_OK;
+}
+
+int sc_copy_region_f32(const float* src, float* dst, int nplanes, int rows, int cols, int64_t src_plane_stride,
+                       int64_t dst_plane_stride, int64_t src_row_stride, int64_t dst_row_stride, int row_lo,
+                       int row_hi, int col_lo, int col_hi, void* stream) {
+    set_error("");
+    if (nplanes < 1 || rows < 1 || cols < 1) return fail(SC_INVALID_ARGUMENT, "dimensions must be positive");
+    if (!(0 <= row_lo && row_lo <= row_hi && row_hi <= rows && 0 <= col_lo && col_lo <= col_hi && col_hi <= cols))
+        return fail(SC_INVALID_ARGUMENT, "region out of bounds");
+    SC_TRY(check_strides(nplanes, rows, cols, src_plane_stride, src_row_stride, "src"));
+    SC_TRY(check_strides(nplanes, rows, cols, dst_plane_stride, dst_row_stride, "dst"));
+    SC_TRY(prepare(src));
+    SC_TRY(prepare(dst));
+    if (overlaps(src, extent_bytes(nplanes, rows, cols, src_plane_stride, src_row_stride), dst,
+                 extent_bytes(nplanes, rows, cols, dst_plane_stride, dst_row_stride)))
+        return fail(SC_INVALID_ARGUMENT, "source and destination must be distinct buffers");
+    cudaError_t e = launch_copy_region(src, dst, src_plane_stride, dst_plane_stride, src_row_stride, dst_row_stride,
+                                       nplanes, row_lo, row_hi - row_lo, col_lo, col_hi - col_lo,
+                                       static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "copy launch");
+    return SC_OK;
+}
+
+int sc_fill_synthetic_f32(float* dst, int64_t count, uint64_t seed, uint64_t offset, int kind, void* stream) {
+    set_error("");
+    if (count < 0 || kind < 0 || kind > 2) return fail(SC_INVALID_ARGUMENT, "bad count or kind");
+    if (count == 0) return SC_OK;
+    SC_TRY(prepare(dst));
+    cudaError_t e = launch_fill_synthetic(dst, count, seed, offset, kind, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "fill launch");
+    return SC_OK;
+}
+
+}  // extern "C"

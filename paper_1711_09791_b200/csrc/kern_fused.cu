@@ -1,0 +1,25 @@
+// Instantiates the row-streaming kernel for MODE_FUSED (one TU per mode keeps
+// nvcc builds parallel). See kernels.cuh.
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace sc {
+
+const void* kernel_fused(int rad, bool aligned) {
+#define SC_K(R)                                                                                   \
+    case R:                                                                                       \
+        return aligned ? (const void*)sepconv_rows_kernel<MODE_FUSED, R, true>                       \
+                       : (const void*)sepconv_rows_kernel<MODE_FUSED, R, false>;
+    switch (rad) {
+        SC_K(0)
+        SC_K(1)
+        SC_K(2)
+        SC_K(3)
+        SC_K(4)
+        default:
+            return nullptr;
+    }
+#undef SC_K
+}
+
+}  // namespace sc

@@ -1,0 +1,47 @@
+// launch.h -- internal (C++) interface between the C ABI layer and the kernel TUs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace sc {
+
+struct Params;
+
+// Kernel entry for (mode, radius, aligned); nullptr if unsupported.
+const void* kernel_fused(int rad, bool aligned);
+const void* kernel_hpass(int rad, bool aligned);
+const void* kernel_vpass(int rad, bool aligned);
+const void* kernel_single(int rad, bool aligned);
+
+cudaError_t launch_copy_region(const float* src, float* dst, long long sps, long long dps, long long srs,
+                               long long drs, int nplanes, int row_lo, int nrows, int col_lo, int ncols,
+                               cudaStream_t s);
+cudaError_t launch_fill_synthetic(float* dst, long long count, uint64_t seed, uint64_t offset, int kind,
+                                  cudaStream_t s);
+
+// Geometry of one row-streaming launch (global row indices).
+struct RowsJob {
+    int mode;
+    const float* src;
+    float* dst;
+    long long sps, dps, srs, drs;
+    int nplanes, R, C;
+    int src_row0, src_rows, dst_row0;
+    int out_lo, out_hi, hrow_lo, hrow_hi;
+    int flags;
+    int width;
+    const float* taps;   // width floats (host)
+    const float* dense;  // width*width floats (host), SINGLE only
+};
+
+// Plans and launches one row-streaming kernel; returns an SC_* status and sets
+// the thread's last error on failure.
+int launch_rows(const RowsJob& job, cudaStream_t s);
+
+void set_error(const std::string& msg);
+void count_launch(uint64_t n = 1);
+
+}  // namespace sc

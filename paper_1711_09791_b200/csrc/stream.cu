@@ -1,0 +1,229 @@
+// stream.cu -- end-to-end two-pass on HOST planes (sc_two_pass_host_f32).
+//
+// The reference convolves numpy planes in host memory and blocks until done
+// (convolve_image, S/executors.py:269-405). This entry point keeps that contract
+// for host buffers: each plane is cut into row chunks; chunk k's input rows
+// [lo-r, hi+r) go H2D on one stream, the fused kernel runs on a second, and the
+// output rows [lo, hi) go D2H on a third, with NSLOT device slots so copy-in,
+// compute and copy-out of consecutive chunks overlap (PCIe is full duplex).
+// D2H of chunk k is ordered after H2D of chunk k+1, so in-place use
+// (dst_planes == src_planes, as conv_two_pass mutates `plane`) never reads a row
+// that was already overwritten.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sepconv_b200.h"
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace sc {
+
+static constexpr int NSLOT = 3;
+
+struct HostCtx {
+    int device = -1;
+    cudaStream_t h2d = nullptr, cmp = nullptr, d2h = nullptr;
+    float* in_buf[NSLOT] = {};
+    float* out_buf[NSLOT] = {};
+    size_t in_cap = 0, out_cap = 0;  // floats per slot
+    cudaEvent_t ev_h2d[NSLOT] = {}, ev_cmp[NSLOT] = {}, ev_d2h[NSLOT] = {};
+    std::mutex mu;
+};
+
+static HostCtx* host_ctx(int device) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<HostCtx>> ctxs;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& c = ctxs[device];
+    if (!c) {
+        c.reset(new HostCtx());
+        c->device = device;
+    }
+    return c.get();
+}
+
+static int ensure(HostCtx* c, size_t in_floats, size_t out_floats, std::string& err) {
+    cudaError_t e;
+    if (!c->h2d) {
+        if ((e = cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->cmp, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking)) != cudaSuccess) {
+            err = cudaGetErrorString(e);
+            return SC_CUDA_ERROR;
+        }
+        for (int i = 0; i < NSLOT; ++i) {
+            cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&c->ev_cmp[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming);
+        }
+    }
+    if (in_floats > c->in_cap || out_floats > c->out_cap) {
+        for (int i = 0; i < NSLOT; ++i) {
+            if (c->in_buf[i]) cudaFree(c->in_buf[i]);
+            if (c->out_buf[i]) cudaFree(c->out_buf[i]);
+            c->in_buf[i] = c->out_buf[i] = nullptr;
+        }
+        c->in_cap = c->out_cap = 0;
+        for (int i = 0; i < NSLOT; ++i) {
+            if ((e = cudaMalloc(&c->in_buf[i], in_floats * sizeof(float))) != cudaSuccess ||
+                (e = cudaMalloc(&c->out_buf[i], out_floats * sizeof(float))) != cudaSuccess) {
+                err = std::string("staging allocation: ") + cudaGetErrorString(e);
+                return SC_CUDA_ERROR;
+            }
+        }
+        c->in_cap = in_floats;
+        c->out_cap = out_floats;
+    }
+    return SC_OK;
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+extern "C" int sc_two_pass_host_f32(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows,
+                                    int cols, const float* taps, int width, int flags, int device) {
+    set_error("");
+    if (!src_planes || !dst_planes || !taps || nplanes < 1 || rows < 1 || cols < 1) {
+        set_error("null pointer or non-positive dimension");
+        return SC_INVALID_ARGUMENT;
+    }
+    if (width < 1 || width % 2 == 0) {
+        set_error("kernel width must be odd and >= 1");
+        return SC_INVALID_ARGUMENT;
+    }
+    if (width > MAX_W) {
+        set_error("kernel width > 9 not supported");
+        return SC_UNSUPPORTED_WIDTH;
+    }
+    if (rows < width || cols < width) {
+        set_error("plane smaller than kernel width");
+        return SC_INVALID_DIMENSION;
+    }
+    for (int p = 0; p < nplanes; ++p)
+        if (!src_planes[p] || !dst_planes[p]) {
+            set_error("null plane pointer");
+            return SC_INVALID_ARGUMENT;
+        }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+        return SC_CUDA_ERROR;
+    }
+    const int r = width / 2;
+    HostCtx* c = host_ctx(device);
+    std::lock_guard<std::mutex> lk(c->mu);
+
+    // chunk rows: ~32 MiB of output per chunk (env SC_HOST_CHUNK_MB overrides)
+    const char* mbs = std::getenv("SC_HOST_CHUNK_MB");
+    const long long chunk_bytes = (long long)(mbs && *mbs ? std::atoi(mbs) : 32) << 20;
+    long long ch = chunk_bytes / ((long long)cols * 4);
+    if (ch < 16) ch = 16;
+    if (ch > rows) ch = rows;
+    const int chunk = (int)ch;
+    std::string err;
+    int rc = ensure(c, (size_t)(chunk + 2 * r) * cols, (size_t)chunk * cols, err);
+    if (rc != SC_OK) {
+        set_error(err);
+        return rc;
+    }
+
+    struct Chunk {
+        int plane, lo, hi, in_lo, in_hi;
+    };
+    std::vector<Chunk> chunks;
+    for (int p = 0; p < nplanes; ++p)
+        for (int lo = 0; lo < rows; lo += chunk) {
+            Chunk k;
+            k.plane = p;
+            k.lo = lo;
+            k.hi = lo + chunk < rows ? lo + chunk : rows;
+            k.in_lo = k.lo - r > 0 ? k.lo - r : 0;
+            k.in_hi = k.hi + r < rows ? k.hi + r : rows;
+            chunks.push_back(k);
+        }
+    const size_t n = chunks.size();
+    const size_t row_bytes = (size_t)cols * sizeof(float);
+
+    auto issue_h2d = [&](size_t k) -> cudaError_t {
+        const Chunk& q = chunks[k];
+        const int s = (int)(k % NSLOT);
+        if (k >= NSLOT) cudaStreamWaitEvent(c->h2d, c->ev_cmp[s], 0);  // slot's previous kernel done
+        cudaError_t e2 = cudaMemcpyAsync(c->in_buf[s], src_planes[q.plane] + (size_t)q.in_lo * cols,
+                                         (size_t)(q.in_hi - q.in_lo) * row_bytes, cudaMemcpyHostToDevice, c->h2d);
+        cudaEventRecord(c->ev_h2d[s], c->h2d);
+        return e2;
+    };
+
+    if (n > 0 && (e = issue_h2d(0)) != cudaSuccess) {
+        set_error(std::string("H2D: ") + cudaGetErrorString(e));
+        return SC_CUDA_ERROR;
+    }
+    for (size_t k = 0; k < n; ++k) {
+        const Chunk& q = chunks[k];
+        const int s = (int)(k % NSLOT);
+        if (k + 1 < n && (e = issue_h2d(k + 1)) != cudaSuccess) {
+            set_error(std::string("H2D: ") + cudaGetErrorString(e));
+            return SC_CUDA_ERROR;
+        }
+        cudaStreamWaitEvent(c->cmp, c->ev_h2d[s], 0);
+        if (k >= NSLOT) cudaStreamWaitEvent(c->cmp, c->ev_d2h[s], 0);  // out slot drained
+        RowsJob j{};
+        j.mode = MODE_FUSED;
+        j.src = c->in_buf[s];
+        j.dst = c->out_buf[s];
+        j.sps = (long long)(q.in_hi - q.in_lo) * cols;
+        j.dps = (long long)(q.hi - q.lo) * cols;
+        j.srs = cols;
+        j.drs = cols;
+        j.nplanes = 1;
+        j.R = rows;
+        j.C = cols;
+        j.src_row0 = q.in_lo;
+        j.src_rows = q.in_hi - q.in_lo;
+        j.dst_row0 = q.lo;
+        j.out_lo = q.lo;
+        j.out_hi = q.hi;
+        j.hrow_lo = (flags & SC_EXTENDED) ? 0 : r;
+        j.hrow_hi = (flags & SC_EXTENDED) ? rows : rows - r;
+        j.flags = flags & (SC_EXTENDED | SC_NO_RING);
+        j.width = width;
+        j.taps = taps;
+        rc = launch_rows(j, c->cmp);
+        if (rc != SC_OK) return rc;
+        cudaEventRecord(c->ev_cmp[s], c->cmp);
+        cudaStreamWaitEvent(c->d2h, c->ev_cmp[s], 0);
+        if (k + 1 < n) cudaStreamWaitEvent(c->d2h, c->ev_h2d[(k + 1) % NSLOT], 0);  // in-place safety
+        if (flags & SC_NO_RING) {
+            // only valid rows/cols leave the device: the host ring keeps its values
+            const int vlo = q.lo > r ? q.lo : r;
+            const int vhi = q.hi < rows - r ? q.hi : rows - r;
+            if (vhi > vlo)
+                e = cudaMemcpy2DAsync(dst_planes[q.plane] + (size_t)vlo * cols + r, row_bytes,
+                                      c->out_buf[s] + (size_t)(vlo - q.lo) * cols + r, row_bytes,
+                                      (size_t)(cols - 2 * r) * sizeof(float), (size_t)(vhi - vlo),
+                                      cudaMemcpyDeviceToHost, c->d2h);
+        } else {
+            e = cudaMemcpyAsync(dst_planes[q.plane] + (size_t)q.lo * cols, c->out_buf[s],
+                                (size_t)(q.hi - q.lo) * row_bytes, cudaMemcpyDeviceToHost, c->d2h);
+        }
+        if (e != cudaSuccess) {
+            set_error(std::string("D2H: ") + cudaGetErrorString(e));
+            return SC_CUDA_ERROR;
+        }
+        cudaEventRecord(c->ev_d2h[s], c->d2h);
+    }
+    e = cudaStreamSynchronize(c->d2h);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->cmp);
+    if (e != cudaSuccess) {
+        set_error(std::string("stream sync: ") + cudaGetErrorString(e));
+        return SC_CUDA_ERROR;
+    }
+    return SC_OK;
+}

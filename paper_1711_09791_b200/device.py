@@ -1,0 +1,230 @@
+"""Device API: the hot path on torch CUDA tensors (PyTorch is plumbing here --
+device memory and streams; every sample is computed by libsepconv_b200.so).
+
+Tensors are float32 stacks of planes, shape (P, R, C) or (N, P, R, C) (any
+leading dims that collapse to a uniform plane stride), unit column stride.
+Launches go on the current torch stream of the tensor's device and are
+asynchronous, like any CUDA op.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidArgumentError
+
+
+def _taps(taps) -> np.ndarray:
+    w = getattr(taps, "weights", taps)  # SeparableKernel or array-like
+    if isinstance(w, torch.Tensor):
+        w = w.detach().cpu().numpy()
+    w = np.ascontiguousarray(w, dtype=np.float32).reshape(-1)
+    return w
+
+
+def _dense(dense) -> np.ndarray:
+    m = getattr(dense, "matrix", dense)
+    if isinstance(m, torch.Tensor):
+        m = m.detach().cpu().numpy()
+    m = np.ascontiguousarray(m, dtype=np.float32)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise InvalidArgumentError(f"dense kernel must be square, got shape {m.shape}")
+    return m
+
+
+def _fp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def _planes(t: torch.Tensor, what: str):
+    """(nplanes, R, C, plane_stride, row_stride) of a CUDA float32 plane stack."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidArgumentError(f"{what} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise InvalidArgumentError(f"{what} must be float32, got {t.dtype}")
+    if t.dim() < 2:
+        raise InvalidArgumentError(f"{what} must have at least 2 dims (rows, cols)")
+    R, C = t.shape[-2], t.shape[-1]
+    if t.stride(-1) != 1 and C > 1:
+        raise InvalidArgumentError(f"{what} needs unit column stride")
+    try:
+        v = t.view(-1, R, C)
+    except RuntimeError as exc:
+        raise InvalidArgumentError(f"{what}: leading dims do not collapse to one plane stride") from exc
+    ps = v.stride(0) if v.shape[0] > 1 else R * max(v.stride(1), C)
+    return v.shape[0], R, C, ps, v.stride(1)
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _same_geometry(a: torch.Tensor, b: torch.Tensor):
+    if a.shape != b.shape:
+        raise InvalidArgumentError(
+            f"source and destination dimensions differ: {tuple(a.shape)} vs {tuple(b.shape)}"
+        )
+    if a.device != b.device:
+        raise InvalidArgumentError("source and destination live on different devices")
+
+
+def two_pass(src: torch.Tensor, taps, out: torch.Tensor | None = None, *, extended: bool = False,
+             ring: bool = True) -> torch.Tensor:
+    """Fused single-read/single-write two-pass, out of place (K1).
+
+    Returns the image the reference leaves in `image` after conv_two_pass
+    (S/conv.py:392-421): ring = src, valid region = V(H0). ring=False leaves
+    out's ring untouched.
+    """
+    w = _taps(taps)
+    if out is None:
+        out = torch.empty_like(src)
+    _same_geometry(src, out)
+    n, R, C, sps, srs = _planes(src, "src")
+    _, _, _, dps, drs = _planes(out, "out")
+    flags = (_lib.SC_EXTENDED if extended else 0) | (0 if ring else _lib.SC_NO_RING)
+    L = _lib.load()
+    _lib.check(L.sc_two_pass_fused_f32(src.data_ptr(), out.data_ptr(), n, R, C, sps, dps, srs, drs,
+                                       _fp(w), w.size, flags, _stream(src)))
+    return out
+
+
+def two_pass_band(src: torch.Tensor, taps, out: torch.Tensor, *, global_rows: int, src_row0: int,
+                  dst_row0: int, out_lo: int, out_hi: int, extended: bool = False) -> torch.Tensor:
+    """Row band of the fused two-pass (multi-GPU partitioner): src holds global rows
+    [src_row0, src_row0 + src.shape[-2]), out row 0 is global row dst_row0."""
+    w = _taps(taps)
+    n, Rs, C, sps, srs = _planes(src, "src")
+    n2, Rd, C2, dps, drs = _planes(out, "out")
+    if n2 != n or C2 != C:
+        raise InvalidArgumentError("band source and destination plane counts / widths differ")
+    if out_hi - dst_row0 > Rd:
+        raise InvalidArgumentError("destination band too short for the output rows")
+    flags = _lib.SC_EXTENDED if extended else 0
+    L = _lib.load()
+    _lib.check(L.sc_two_pass_band_f32(src.data_ptr(), out.data_ptr(), n, global_rows, C, sps, dps, srs, drs,
+                                      src_row0, Rs, dst_row0, out_lo, out_hi, _fp(w), w.size, flags,
+                                      _stream(src)))
+    return out
+
+
+def hpass(src: torch.Tensor, taps, out: torch.Tensor, row_lo: int | None = None, row_hi: int | None = None,
+          *, zero_fill: bool = False) -> torch.Tensor:
+    """horizontal_rows_vec (S/conv.py:215-240) over rows [row_lo, row_hi) (default: valid rows)."""
+    w = _taps(taps)
+    _same_geometry(src, out)
+    n, R, C, sps, srs = _planes(src, "src")
+    _, _, _, dps, drs = _planes(out, "out")
+    r = w.size // 2
+    lo = r if row_lo is None else row_lo
+    hi = R - r if row_hi is None else row_hi
+    L = _lib.load()
+    _lib.check(L.sc_hpass_f32(src.data_ptr(), out.data_ptr(), n, R, C, sps, dps, srs, drs, lo, hi, _fp(w),
+                              w.size, _lib.SC_ZERO_FILL if zero_fill else 0, _stream(src)))
+    return out
+
+
+def vpass(src: torch.Tensor, taps, out: torch.Tensor, row_lo: int | None = None,
+          row_hi: int | None = None) -> torch.Tensor:
+    """vertical_rows_vec (S/conv.py:269-293) over rows [row_lo, row_hi) inside [r, R-r)."""
+    w = _taps(taps)
+    _same_geometry(src, out)
+    n, R, C, sps, srs = _planes(src, "src")
+    _, _, _, dps, drs = _planes(out, "out")
+    r = w.size // 2
+    lo = r if row_lo is None else row_lo
+    hi = R - r if row_hi is None else row_hi
+    L = _lib.load()
+    _lib.check(L.sc_vpass_f32(src.data_ptr(), out.data_ptr(), n, R, C, sps, dps, srs, drs, lo, hi, _fp(w),
+                              w.size, 0, _stream(src)))
+    return out
+
+
+def two_pass_split(image: torch.Tensor, scratch: torch.Tensor, taps, *, extended: bool = False) -> torch.Tensor:
+    """The reference two-pass with its buffer semantics (K2 + K3): scratch := H0,
+    image[valid] := V(scratch); image ring untouched. Returns image."""
+    w = _taps(taps)
+    _same_geometry(image, scratch)
+    n, R, C, ips, irs = _planes(image, "image")
+    _, _, _, sps, srs = _planes(scratch, "scratch")
+    L = _lib.load()
+    _lib.check(L.sc_two_pass_split_f32(image.data_ptr(), scratch.data_ptr(), n, R, C, ips, sps, irs, srs,
+                                       _fp(w), w.size, _lib.SC_EXTENDED if extended else 0, _stream(image)))
+    return image
+
+
+def single_pass(src: torch.Tensor, dense, out: torch.Tensor, *, copy_back: bool = False) -> torch.Tensor:
+    """single_pass_rows_vec (S/conv.py:86-114) with the dense matrix; out's ring untouched.
+    copy_back additionally writes the valid region into src (S/executors.py:330-331)."""
+    m = _dense(dense)
+    _same_geometry(src, out)
+    n, R, C, sps, srs = _planes(src, "src")
+    _, _, _, dps, drs = _planes(out, "out")
+    L = _lib.load()
+    _lib.check(L.sc_single_pass_f32(src.data_ptr(), out.data_ptr(), n, R, C, sps, dps, srs, drs, _fp(m),
+                                    m.shape[0], _lib.SC_COPY_BACK if copy_back else 0, _stream(src)))
+    return out
+
+
+def copy_region(src: torch.Tensor, dst: torch.Tensor, row_lo: int, row_hi: int, col_lo: int,
+                col_hi: int) -> torch.Tensor:
+    """copy_back (S/conv.py:424-440) on device planes."""
+    _same_geometry(src, dst)
+    n, R, C, sps, srs = _planes(src, "src")
+    _, _, _, dps, drs = _planes(dst, "dst")
+    L = _lib.load()
+    _lib.check(L.sc_copy_region_f32(src.data_ptr(), dst.data_ptr(), n, R, C, sps, dps, srs, drs, row_lo, row_hi,
+                                    col_lo, col_hi, _stream(src)))
+    return dst
+
+
+def fill_synthetic(t: torch.Tensor, seed: int, kind: int, offset: int = 0) -> torch.Tensor:
+    """Fill a contiguous CUDA float32 tensor with splitmix64 draws offset.. (S/image.py:131-162)."""
+    if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+        raise InvalidArgumentError("fill_synthetic needs a contiguous CUDA float32 tensor")
+    L = _lib.load()
+    _lib.check(L.sc_fill_synthetic_f32(t.data_ptr(), t.numel(), seed & (2**64 - 1), offset, kind, _stream(t)))
+    return t
+
+
+def synthetic(shape, seed: int, kind: int, device="cuda", offset: int = 0) -> torch.Tensor:
+    t = torch.empty(tuple(shape), dtype=torch.float32, device=device)
+    return fill_synthetic(t, seed, kind, offset)
+
+
+def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring: bool = True,
+                  device: int = 0) -> None:
+    """End-to-end two-pass on HOST planes (numpy arrays or CPU tensors, ideally pinned):
+    streamed H2D -> fused kernel -> D2H inside the library; blocks until done.
+    dst_planes may be src_planes (in place, as conv_two_pass)."""
+    w = _taps(taps)
+    ptrs_in, ptrs_out = [], []
+    shape = None
+    for a, b in zip(src_planes, dst_planes):
+        for arr in (a, b):
+            if isinstance(arr, torch.Tensor):
+                if arr.is_cuda or arr.dtype != torch.float32 or not arr.is_contiguous():
+                    raise InvalidArgumentError("host planes must be contiguous CPU float32")
+                shp = tuple(arr.shape)
+            else:
+                if arr.dtype != np.float32 or not arr.flags.c_contiguous:
+                    raise InvalidArgumentError("host planes must be C-contiguous float32")
+                shp = arr.shape
+            if len(shp) != 2 or (shape is not None and shp != shape):
+                raise InvalidArgumentError("host planes must be 2-D and share one shape")
+            shape = shp
+        ptrs_in.append(a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data)
+        ptrs_out.append(b.data_ptr() if isinstance(b, torch.Tensor) else b.ctypes.data)
+    if not ptrs_in or len(ptrs_in) != len(list(dst_planes)):
+        raise InvalidArgumentError("need matching, non-empty source and destination plane lists")
+    n = len(ptrs_in)
+    arr_in = (ctypes.c_void_p * n)(*ptrs_in)
+    arr_out = (ctypes.c_void_p * n)(*ptrs_out)
+    flags = (_lib.SC_EXTENDED if extended else 0) | (0 if ring else _lib.SC_NO_RING)
+    L = _lib.load()
+    _lib.check(L.sc_two_pass_host_f32(ctypes.cast(arr_in, ctypes.c_void_p), ctypes.cast(arr_out, ctypes.c_void_p),
+                                      n, shape[0], shape[1], _fp(w), w.size, flags, int(device)))
