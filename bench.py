@@ -1,0 +1,413 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 separable-convolution hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg5]
+
+Workload (BASELINE.json configs[4], the largest single-image config and the one
+north_star scores at 1/2/4/8 GPUs): one image of 3 float32 planes x 16384 x 16384,
+values U[0,1) from a seed, taps [1,4,6,4,1]/16, faithful two-pass. A "step" is
+one fused two-pass over the whole image; N>1 splits it into row bands with a
+2-row NCCL halo exchange per step (strong scaling: total work fixed).
+
+metric: Gpixels/s (1 pixel = one (row, col) location across the 3 planes);
+value = whole-job pixels / max-over-ranks step time, inputs resident in HBM.
+e2e: the same metric through the C-ABI host entry point (sc_two_pass_host_f32):
+pinned host planes in, H2D + kernel + D2H inside the timed region.
+
+Inputs are 3.2 GB, far larger than the 126 MB L2, so no flush is needed between
+timed steps. --impl reference times the reference algorithm on the host CPU
+(the oracle's numpy port of sepconv_lab's StaticChunked two-pass).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1711_09791_b200.configs import CONFIGS  # noqa: E402
+
+METRIC = "Gpixels/s (3-plane fp32) and effective HBM GB/s as % of B200 peak, 1/2/4/8 GPU"
+NOMINAL_HBM_GBPS = 8000.0
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def traffic_from_profiles(cfg: str):
+    """dram read+write bytes per launch of the fused kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(cfg)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:  # noqa: BLE001 - clocks are best-effort evidence
+                return
+            self._stop.wait(0.05)
+
+    def start(self):
+        self._t = threading.Thread(target=self._poll, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"], "samples": 0}
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        busy = [s for s in self.samples if num(s[7]) and num(s[7]) > 0] or self.samples
+        sm = [num(s[0]) for s in busy if num(s[0])]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in busy:
+            for name, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(busy[0][1]), "reasons": sorted(reasons), "samples": len(busy)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_arm(args, wl):
+    """The reference algorithm on host cores (numpy port of the reference's
+    vectorised StaticChunked two-pass; oracle/oracle.py) -- rank 0 only."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+
+    cores = os.cpu_count() or 1
+    rows = max(64, min(wl.rows, args.ref_rows))
+    sample_px = rows * wl.cols
+    w = wl.tap_vector()
+    planes = [orc.synthetic(rows * wl.cols, wl.seed, wl.kind, offset=p * wl.rows * wl.cols).reshape(rows, wl.cols)
+              for p in range(wl.planes)]
+    scratch = [np.zeros_like(p) for p in planes]
+    run = orc.NumpyTwoPass(cores)
+    try:
+        for _ in range(args.warmup):
+            run(planes, scratch, w)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            run(planes, scratch, w)
+        dt = (time.perf_counter() - t0) / args.steps
+    finally:
+        run.close()
+    value = sample_px / dt / 1e9
+    sample = (f"{wl.planes}x{rows}x{wl.cols} slice of {wl.name} per step (numpy port of the reference's "
+              f"vectorised two-pass, StaticChunked({cores}) threads, S/executors.py:366-380)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gpix/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {wl.note}", "sample_rows": rows},
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gpix/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 6), "unit": "Gpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(wl):
+    """Bounded CPU sample of the same workload (reported baseline, not the target)."""
+    from oracle import oracle as orc
+
+    cores = os.cpu_count() or 1
+    rows = min(wl.rows, 2048)
+    w = wl.tap_vector()
+    planes = [orc.synthetic(rows * wl.cols, wl.seed, wl.kind, offset=p * wl.rows * wl.cols).reshape(rows, wl.cols)
+              for p in range(wl.planes)]
+    scratch = [np.zeros_like(p) for p in planes]
+    run = orc.NumpyTwoPass(cores)
+    try:
+        run(planes, scratch, w)  # warm-up (S/bench.py:158-159)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            run(planes, scratch, w)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el > 10.0 or reps >= 8:
+                break
+    finally:
+        run.close()
+    return {"value": round(rows * wl.cols * reps / el / 1e9, 6), "unit": "Gpix/s", "cores": cores,
+            "kind": "port",
+            "sample": f"{wl.planes}x{rows}x{wl.cols} slice of {wl.name}, {reps} reps after 1 warm-up, numpy port "
+                      f"of the reference two-pass with StaticChunked({cores}) threads"}
+
+
+def host_chunk_bytes(rows, cols, planes, r, band_lo, band_hi, in_lo, in_hi):
+    """Bytes the host path moves per step (mirrors csrc/stream.cu chunking: 32 MiB chunks)."""
+    ch = max(16, min(rows, (32 << 20) // (cols * 4)))
+    h2d = d2h = 0
+    for lo in range(band_lo, band_hi, ch):
+        hi = min(lo + ch, band_hi)
+        a, b = max(lo - r, in_lo), min(hi + r, in_hi)
+        h2d += (b - a) * cols * 4
+        d2h += (hi - lo) * cols * 4
+    return h2d * planes, d2h * planes
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return reference_arm(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_09791_b200 import _lib
+    from paper_1711_09791_b200 import device as dev
+    from paper_1711_09791_b200.multi import band_plan, band_two_pass, frame_shard
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    w = wl.tap_vector()
+    r = len(w) // 2
+    P, R, C = wl.planes, wl.rows, wl.cols
+    per_frame = P * R * C
+
+    # ---- inputs resident in HBM (generated in place: counter-based, no scatter)
+    if wl.frames > 1:
+        f0, f1 = frame_shard(wl.frames, rank, world)
+        src = torch.empty((f1 - f0, P, R, C), dtype=torch.float32, device=device)
+        dev.fill_synthetic(src, wl.seed, wl.kind, offset=f0 * per_frame)
+        dst = torch.empty_like(src)
+        band = None
+        units_px = (f1 - f0) * R * C
+
+        def step():
+            dev.two_pass(src, w, dst)
+    else:
+        band = band_plan(R, rank, world, r)
+        src = torch.empty((P, band.local_rows, C), dtype=torch.float32, device=device)
+        for p in range(P):
+            # owned rows plus the halo rows (the halo is refreshed by the exchange each step)
+            dev.fill_synthetic(src[p], wl.seed, wl.kind, offset=p * R * C + band.in_lo * C)
+        dst = torch.empty((P, band.hi - band.lo, C), dtype=torch.float32, device=device)
+        units_px = (band.hi - band.lo) * C
+
+        def step():
+            if world == 1:
+                dev.two_pass(src, w, dst)
+            else:
+                band_two_pass(src, dst, band, w)
+
+    total_px = wl.frames * R * C
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    stream = torch.cuda.current_stream()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step()
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = _lib.launch_count() - launches0
+    sampler.stop()
+    ms = t_start.elapsed_time(t_end) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = total_px / (ms / 1e3) / 1e9
+
+    # ---- dominant-kernel roofline: the fused kernel's own launch time (events on its stream)
+    kev = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if band is not None and world > 1:
+            dev.two_pass_band(src, w, dst, global_rows=R, src_row0=band.in_lo, dst_row0=band.lo,
+                              out_lo=band.lo, out_hi=band.hi)
+        else:
+            dev.two_pass(src, w, dst)
+        b.record(stream)
+        b.synchronize()
+        kev.append(a.elapsed_time(b))
+    kms = statistics.median(kev)
+    kernel_bytes = 2 * 4 * P * units_px  # algorithmic: one read + one write of this rank's samples
+    peaks, peak_kind = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = kernel_bytes / (kms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(args.config),
+                "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                "kernel": "sepconv_rows_kernel<MODE_FUSED, r=2, TMA>", "kernel_ms": round(kms, 4),
+                "alg_bytes_per_launch": kernel_bytes}
+
+    # ---- end to end through the C-ABI host entry point (pinned host planes)
+    e2e = None
+    if args.e2e_steps > 0:
+        if band is not None:
+            lo, hi, in_lo, in_hi = band.lo, band.hi, band.in_lo, band.in_hi
+            host = [torch.empty((R, C), dtype=torch.float32, pin_memory=True) for _ in range(P)] if world == 1 else None
+            if host is None:
+                host = None
+        # host planes hold this rank's rows (N=1: the whole image); in place like conv_two_pass
+        if band is not None and world == 1:
+            for p in range(P):
+                host[p].copy_(src[p].cpu())
+            h2d, d2h = host_chunk_bytes(R, C, P, r, 0, R, 0, R)
+            planes = [h for h in host]
+
+            def e2e_step():
+                dev.two_pass_host(planes, planes, w, device=local)
+        elif band is not None:
+            # N>1: each rank streams its band (+halo rows) from its own pinned buffer
+            hb = torch.empty((P, band.local_rows, C), dtype=torch.float32, pin_memory=True)
+            hb.copy_(src.cpu())
+            ho = torch.empty((P, band.hi - band.lo, C), dtype=torch.float32, pin_memory=True)
+            h2d = P * band.local_rows * C * 4
+            d2h = P * (band.hi - band.lo) * C * 4
+            ds = torch.empty_like(src)
+            do = torch.empty_like(dst)
+
+            def e2e_step():
+                ds.copy_(hb, non_blocking=True)
+                band_two_pass(ds, do, band, w)
+                ho.copy_(do, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+        else:
+            hb = src.cpu().pin_memory()
+            ho = torch.empty_like(hb).pin_memory()
+            h2d = d2h = hb.numel() * 4
+            ds = torch.empty_like(src)
+            do = torch.empty_like(dst)
+
+            def e2e_step():
+                ds.copy_(hb, non_blocking=True)
+                dev.two_pass(ds, w, do)
+                ho.copy_(do, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": round(total_px / (e_ms / 1e3) / 1e9, 4), "unit": "Gpix/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3),
+               "path": "sc_two_pass_host_f32 (pinned host planes, chunked H2D/kernel/D2H on 3 streams)"
+               if world == 1 and band is not None else "pinned H2D + device API + D2H per rank"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl)
+
+    if rank == 0:
+        eff = 2 * 4 * P * total_px / (ms / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Gpix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak" if wl.frames > 1 else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.note}", "frames": wl.frames, "planes": P, "rows": R, "cols": C,
+                       "taps": [float(v) for v in w], "parallelism": f"rowband{world}" if wl.frames == 1
+                       else f"frames{world}", "l2": "inputs 3.2 GB >> 126 MB L2; no flush needed"},
+            "effective_GBps": round(eff, 1), "pct_of_8TBps": round(100 * eff / NOMINAL_HBM_GBPS, 2),
+            "pct_of_measured_copy": round(100 * eff / peak, 2),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -21,6 +21,7 @@
  * intact.
  */
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #define ORC_API __attribute__((visibility("default")))
@@ -169,3 +170,39 @@ ORC_API void orc_fill_synthetic(float *dst, uint64_t count, uint64_t seed, uint6
 }
 
 ORC_API int orc_abi_version(void) { return 1; }
+
+/* Row band of the faithful/extended two-pass (the multi-GPU partitioner's unit,
+ * SURVEY.md section 8e) restated directly from the reference's rules with
+ * GLOBAL row indices: src holds global rows [src_row0, src_row0+src_rows), dst
+ * row 0 is global row dst_row0; output rows [out_lo, out_hi) are produced.
+ * Ring rows/cols (outside [r,R-r)x[r,C-r)) copy the input, as the in-place
+ * reference leaves them (S/conv.py:392-421); valid samples are V(H0). */
+ORC_API int orc_two_pass_band(const float *src, float *dst, int global_rows, int cols,
+                              int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
+                              const float *w, int width, int extended)
+{
+    const int r = width / 2;
+    float *scr = (float *)calloc((size_t)src_rows * (size_t)cols, sizeof(float));
+    if (!scr) return -1;
+    for (int i = 0; i < src_rows; ++i) {
+        const int g = src_row0 + i;
+        if (extended || (g >= r && g < global_rows - r))
+            orc_horizontal_rows(src + (int64_t)i * cols - 0, scr + (int64_t)i * cols, 1, cols, w, width, 0, 1);
+    }
+    for (int y = out_lo; y < out_hi; ++y) {
+        const float *a = src + (int64_t)(y - src_row0) * cols;
+        float *d = dst + (int64_t)(y - dst_row0) * cols;
+        memcpy(d, a, sizeof(float) * (size_t)cols);
+        if (y < r || y >= global_rows - r) continue;
+        for (int x = r; x < cols - r; ++x) d[x] = scr[(int64_t)(y - r - src_row0) * cols + x] * w[0];
+        for (int m = 1; m < width; ++m) {
+            const float *s = scr + (int64_t)(y - r + m - src_row0) * cols;
+            for (int x = r; x < cols - r; ++x) {
+                float term = s[x] * w[m];
+                d[x] = d[x] + term;
+            }
+        }
+    }
+    free(scr);
+    return 0;
+}

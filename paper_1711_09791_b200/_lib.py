@@ -19,7 +19,8 @@ from .errors import (
     UnsupportedWidthError,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsepconv_b200.so")
+LIB_PATH = os.environ.get("SEPCONV_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libsepconv_b200.so")
 
 SC_OK = 0
 SC_INVALID_ARGUMENT = 1

@@ -95,18 +95,44 @@ static int occupancy(const void* kern, int threads, size_t smem) {
     return occ;
 }
 
+// Ring of zeroed [next, finished] ticket pairs per device for the kernels'
+// dynamic item scheduling; the last CTA of a launch re-zeroes its pair, so a
+// slot is reusable once its launch retired (1024 launches in flight at most).
+static constexpr int kWorkSlots = 1024;
+
+static int* work_slot(int dev) {
+    static std::mutex mu;
+    static std::map<int, int*> bufs;
+    static std::map<int, unsigned> next;
+    std::lock_guard<std::mutex> lk(mu);
+    int*& b = bufs[dev];
+    if (!b) {
+        if (cudaMalloc(&b, sizeof(int) * 2 * kWorkSlots) != cudaSuccess) {
+            cudaGetLastError();
+            b = nullptr;
+            return nullptr;
+        }
+        cudaMemset(b, 0, sizeof(int) * 2 * kWorkSlots);
+        cudaDeviceSynchronize();
+    }
+    const unsigned k = next[dev]++ % kWorkSlots;
+    return b + 2 * k;
+}
+
 // --------------------------------------------------------------------------
 // Planner
 
 // Consumer threads per CTA: strip width TW = 4*nt; minimise padding columns.
+static constexpr int COLS_PER_THREAD = 4 * GROUPS;
+
 static int choose_nt(int C) {
     int forced = env_int("SC_NT", 0);
     if (forced >= 32 && forced <= 256 && forced % 32 == 0) return forced;
-    static const int cand[] = {128, 96, 160, 64, 192, 256, 32};
+    static const int cand[] = {128, 96, 64, 160, 192, 256, 32};
     int best = 128;
     long long best_waste = -1;
     for (int nt : cand) {
-        const long long tw = 4LL * nt;
+        const long long tw = (long long)COLS_PER_THREAD * nt;
         const long long strips = (C + tw - 1) / tw;
         const long long waste = strips * tw - C;
         if (best_waste < 0 || waste < best_waste) {
@@ -153,19 +179,22 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.hrow_lo = j.hrow_lo;
     p.hrow_hi = j.hrow_hi;
     p.flags = j.flags;
+    p.one = 1.0f;
+    if (env_int("SC_L2_NORMAL", 0)) p.flags |= F_L2_NORMAL;
+    if (env_int("SC_ST_CS", 0)) p.flags |= F_ST_CS;
     for (int i = 0; i < j.width; ++i) p.w[i] = j.taps ? j.taps[i] : 0.0f;
     if (j.dense)
         for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];
 
     const int nt = choose_nt(j.C);
-    p.tw = 4 * nt;
+    p.tw = COLS_PER_THREAD * nt;
     p.nstrips = (j.C + p.tw - 1) / p.tw;
-    int nr = env_int("SC_NR", 16);
-    if (nr < 2 * rad + 4) nr = 2 * rad + 4;
-    if (nr > 64) nr = 64;
-    p.nr = nr;
+    int ns = env_int("SC_NS", 4);
+    if (ns < 3) ns = 3;
+    if (ns > 16) ns = 16;
+    p.ns = ns;
     const int threads = 32 + nt;
-    const size_t smem = (size_t)((2 * nr * 8 + 127) / 128) * 128 + (size_t)nr * (p.tw + 2 * HALO) * 4;
+    const size_t smem = (size_t)((2 * ns * 8 + ns * 4 + 127) / 128) * 128 + (size_t)ns * SROWS * (p.tw + 2 * HALO) * 4;
 
     int dev = 0;
     cudaGetDevice(&dev);
@@ -175,28 +204,18 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;
     const long long G = (long long)di.sms * occ;
 
-    // Row-band height: minimise (waves x rows per item), each item re-reading a
-    // 2r-row halo plus a fixed pipeline ramp worth ~8 rows.
+    // Row-band height. Items are claimed dynamically (atomic ticket), so short
+    // bands cost nothing in balance; they only re-read a 2r-row halo (mostly
+    // from L2, since neighbouring bands run concurrently). ~64 rows measured
+    // best on B200 at 16384^2 (tools/sweep.py); keep >= ~8 items per CTA slot.
     const int rows_out = j.out_hi - j.out_lo;
     const long long units = (long long)j.nplanes * p.nstrips;
     int band_h = env_int("SC_BAND_H", 0);
     if (band_h <= 0) {
-        const int min_bh = 8;
-        const int max_nb = rows_out / min_bh > 1 ? rows_out / min_bh : 1;
-        long long best_cost = -1;
-        int best_bh = rows_out;
-        for (int nb = 1; nb <= max_nb; ++nb) {
-            const int bh = (rows_out + nb - 1) / nb;
-            const long long nb_eff = (rows_out + bh - 1) / bh;
-            const long long items = units * nb_eff;
-            const long long waves = (items + G - 1) / G;
-            const long long cost = waves * (bh + 2 * rad + 8);
-            if (best_cost < 0 || cost < best_cost) {
-                best_cost = cost;
-                best_bh = bh;
-            }
-        }
-        band_h = best_bh;
+        band_h = 64;
+        // small images: shrink bands until every CTA slot has work
+        while (band_h > 8 && units * ((rows_out + band_h - 1) / band_h) < 2 * G) band_h /= 2;
+        if (band_h > rows_out) band_h = rows_out;
     }
     p.band_h = band_h;
     const long long nbands = (rows_out + band_h - 1) / band_h;
@@ -204,14 +223,16 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     if (nitems > 0x7fffffffLL) return fail(SC_INVALID_ARGUMENT, "too many work items");
     p.nitems = (int)nitems;
     const int grid = (int)(nitems < G ? nitems : G);
+    p.work = work_slot(dev);
+    if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
 
     void* args[] = {&p};
     cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     count_launch();
     if (env_int("SC_DEBUG_PLAN", 0))
-        std::fprintf(stderr, "[sc] mode=%d rad=%d aligned=%d nt=%d tw=%d strips=%d band_h=%d items=%d grid=%d occ=%d smem=%zu\n",
-                     j.mode, rad, (int)aligned, nt, p.tw, p.nstrips, band_h, p.nitems, grid, occ, smem);
+        std::fprintf(stderr, "[sc] mode=%d rad=%d aligned=%d nt=%d tw=%d strips=%d ns=%d band_h=%d items=%d grid=%d occ=%d smem=%zu\n",
+                     j.mode, rad, (int)aligned, nt, p.tw, p.nstrips, ns, band_h, p.nitems, grid, occ, smem);
     return SC_OK;
 }
 

@@ -40,11 +40,14 @@ enum Mode : int { MODE_FUSED = 0, MODE_HPASS = 1, MODE_VPASS = 2, MODE_SINGLE = 
 constexpr int F_EXTENDED = 0x1;
 constexpr int F_NO_RING = 0x2;
 constexpr int F_ZERO_FILL = 0x4;
+// tuning flags (set by the planner from SC_* environment variables)
+constexpr int F_L2_NORMAL = 0x100;  // no evict_first hint on the row loads
+constexpr int F_ST_CS = 0x200;      // streaming (.cs) stores
 
 constexpr int HALO = 4;       // smem columns kept either side of a strip (supports r <= 4)
 constexpr int MAX_RAD = 4;
 constexpr int MAX_W = 2 * MAX_RAD + 1;
-constexpr int MAX_THREADS = 32 + 256;
+constexpr int MAX_THREADS = 32 + 256;  // producer warp + up to 8 consumer warps
 
 struct Params {
     const float* src;
@@ -60,7 +63,9 @@ struct Params {
     int flags;
     int tw;                  // strip width = 4 * consumer threads
     int nstrips, band_h, nitems;
-    int nr;                  // ring slots (rows)
+    int ns;                  // smem stages (SROWS rows each)
+    float one;               // 1.0f, passed at run time (see mad2)
+    int* work;               // [next item, finished CTAs]: dynamic scheduling ticket pair (zero at launch)
     float w[MAX_W];
     float k[MAX_W * MAX_W];
 };
@@ -108,6 +113,12 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
         : "memory");
 }
 
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -120,6 +131,15 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 __device__ __forceinline__ float fm(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float fa(float a, float b) { return __fadd_rn(a, b); }
 
+// acc + x*w as two IEEE roundings (mul, then add), packed two columns wide.
+// ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 with a
+// single rounding -- which would break parity -- so the add is issued as an
+// FFMA2 by a RUN-TIME 1.0: prod*1 is exact and the FFMA2 rounds once, i.e. the
+// same bits as add.rn, and ptxas cannot fold what it cannot prove is 1.
+__device__ __forceinline__ float2 mad2(float2 acc, float2 x, float2 w, float2 one) {
+    return __ffma2_rn(__fmul2_rn(x, w), one, acc);
+}
+
 struct F4 {
     float v[4];
 };
@@ -131,12 +151,29 @@ __device__ __forceinline__ F4 ld4(const float* p) {
     return r;
 }
 
-__device__ __forceinline__ void st4(float* p, const F4& a) {
-    *reinterpret_cast<float4*>(p) = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
+__device__ __forceinline__ void st4(float* p, const F4& a, bool streaming = false) {
+    const float4 t = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
+    if (streaming)
+        __stcs(reinterpret_cast<float4*>(p), t);
+    else
+        *reinterpret_cast<float4*>(p) = t;
 }
 
 // ---------------------------------------------------------------------------
-// Item geometry
+// Geometry
+//
+// Strip = TW = 8*NT output columns; consumer thread t owns two 4-column groups
+// at strip offsets 4t and 4t + TW/2, so each warp-wide STG.128 writes 512
+// contiguous bytes. Rows travel in stages of SROWS rows per mbarrier pair.
+
+#ifndef SC_GROUPS
+#define SC_GROUPS 2
+#endif
+#ifndef SC_F2
+#define SC_F2 1
+#endif
+constexpr int SROWS = 4;
+constexpr int GROUPS = SC_GROUPS;
 
 struct Item {
     int plane, x0, ylo, yhi, in_lo, in_hi;
@@ -163,50 +200,110 @@ __device__ __forceinline__ Item decode_item(const Params& p, int item) {
     return it;
 }
 
+// Rows needing per-row special cases: ring rows (FUSED copies them), rows where
+// the row pass is dead (FUSED's zero H0 rows, HPASS's zero fill).
+template <int MODE, int RAD>
+__device__ __forceinline__ bool item_rows_edge(const Params& p, const Item& it) {
+    if (MODE == MODE_HPASS) return it.ylo < p.hrow_lo || it.yhi > p.hrow_hi;
+    if (MODE == MODE_FUSED)
+        return it.in_lo < p.hrow_lo || it.in_hi > p.hrow_hi || it.ylo < RAD || it.yhi > p.R - RAD;
+    return false;
+}
+
 // ---------------------------------------------------------------------------
-// Producer: one warp streams rows of the strip into the smem ring.
+// Producer: one warp streams the strip's rows into the smem stage ring.
 
 template <int MODE, int RAD, bool ALIGNED>
-__device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t* full, uint64_t* empty) {
+__device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t* full, uint64_t* empty,
+                                         int* sitem) {
+    // Items are claimed dynamically (atomic ticket), so CTAs that get more
+    // bandwidth do more items and no SM idles in a tail. The claimed item id
+    // rides in sitem[slot] of its first stage; id -1 tells consumers to stop.
     const int lane = threadIdx.x & 31;
     if (ALIGNED && lane != 0) return;
     const int SW = p.tw + 2 * HALO;
-    const int NR = p.nr;
+    const int NS = p.ns;
     uint64_t pol = 0;
-    if (ALIGNED) pol = policy_evict_first();
+    if (ALIGNED) pol = (p.flags & F_L2_NORMAL) ? policy_evict_normal() : policy_evict_first();
     int slot = 0;
     uint32_t phase = 0;
-    long long g = 0;
-    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
+    int gs = 0;
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(&p.work[0], 1);
+        if (!ALIGNED) item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= p.nitems) {
+            if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
+            if (lane == 0) sitem[slot] = -1;
+            if (ALIGNED) {
+                mbar_arrive_expect_tx(&full[slot], 0u);
+            } else {
+                __syncwarp();
+                mbar_arrive(&full[slot]);
+            }
+            if (lane == 0) {
+                // the last CTA out re-arms the ticket pair for the next launch
+                __threadfence();
+                if (atomicAdd(&p.work[1], 1) == (int)gridDim.x - 1) {
+                    atomicExch(&p.work[0], 0);
+                    atomicExch(&p.work[1], 0);
+                }
+            }
+            return;
+        }
         const Item it = decode_item<MODE, RAD>(p, item);
         const int cx0 = max(it.x0 - HALO, 0);
         const int cx1 = min(it.x0 + p.tw + HALO, p.C);
         const int n = cx1 - cx0;
         const float* gbase = p.src + (long long)it.plane * p.src_plane_stride + cx0;
-        for (int yi = it.in_lo; yi < it.in_hi; ++yi, ++g) {
-            if (g >= NR) mbar_wait(&empty[slot], phase ^ 1u);
-            const float* gsrc = gbase + (long long)(yi - p.src_row0) * p.src_row_stride;
-            float* sdst = ring + slot * SW + (cx0 - (it.x0 - HALO));
+        const int soff = cx0 - (it.x0 - HALO);
+        for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
+            if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
+            const int nrows = min(SROWS, it.in_hi - r0);
+            float* sbase = ring + slot * SROWS * SW + soff;
+            const float* g0 = gbase + (long long)(r0 - p.src_row0) * p.src_row_stride;
+            if (lane == 0) sitem[slot] = item;
             if (ALIGNED) {
                 const uint32_t bytes = (uint32_t)n * 4u;
-                mbar_arrive_expect_tx(&full[slot], bytes);
-                bulk_g2s(sdst, gsrc, bytes, &full[slot], pol);
+                mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
+                for (int k = 0; k < nrows; ++k)
+                    bulk_g2s(sbase + k * SW, g0 + (long long)k * p.src_row_stride, bytes, &full[slot], pol);
             } else {
-                for (int c = lane; c < n; c += 32) sdst[c] = __ldg(gsrc + c);
+                for (int k = 0; k < nrows; ++k) {
+                    const float* gr = g0 + (long long)k * p.src_row_stride;
+                    float* sr = sbase + k * SW;
+                    for (int c = lane; c < n; c += 32) sr[c] = __ldg(gr + c);
+                }
+                __syncwarp();
                 mbar_arrive(&full[slot]);
             }
-            if (++slot == NR) { slot = 0; phase ^= 1u; }
+            if (++slot == NS) { slot = 0; phase ^= 1u; }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Consumer helpers
+// Per-row arithmetic for one 4-column group. win holds columns x4-4 .. x4+7.
 
-// Row pass for 4 adjacent output columns: win holds columns x4-4 .. x4+7.
 template <int RAD>
-__device__ __forceinline__ F4 row_pass(const float (&win)[12], const float* w) {
+__device__ __forceinline__ F4 row_pass(const float (&win)[12], const float* w, float one) {
     F4 h;
+#if SC_F2
+    const float2 one2 = make_float2(one, one);
+    // packed f32x2: two adjacent output columns per FMUL2/FADD2, each lane an
+    // IEEE fp32 mul/add (same bits as __fmul_rn/__fadd_rn, never fused)
+#pragma unroll
+    for (int c = 0; c < 4; c += 2) {
+        const int o = HALO - RAD + c;
+        float2 acc = __fmul2_rn(make_float2(win[o], win[o + 1]), make_float2(w[0], w[0]));
+#pragma unroll
+        for (int m = 1; m <= 2 * RAD; ++m)
+            acc = mad2(acc, make_float2(win[o + m], win[o + m + 1]), make_float2(w[m], w[m]), one2);
+        h.v[c] = acc.x;
+        h.v[c + 1] = acc.y;
+    }
+#else
+    (void)one;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         float acc = fm(win[HALO - RAD + c], w[0]);
@@ -214,27 +311,136 @@ __device__ __forceinline__ F4 row_pass(const float (&win)[12], const float* w) {
         for (int m = 1; m <= 2 * RAD; ++m) acc = fa(acc, fm(win[HALO - RAD + c + m], w[m]));
         h.v[c] = acc;
     }
+#endif
     return h;
 }
 
-// Store one output row segment of 4 columns with the column-ring policy.
-//   ring_mode 0: keep   -- only columns in [RAD, C-RAD) are written
-//   ring_mode 1: copy   -- ring columns take `ringv` (input samples)
-//   ring_mode 2: zero   -- ring columns take 0
-template <bool ALIGNED>
-__device__ __forceinline__ void store_row(float* drow, int x4, int C, int RAD_, const F4& val, const F4& ringv,
-                                          int ring_mode) {
-    const bool interior = (x4 >= RAD_) && (x4 + 4 <= C - RAD_);
-    if (ALIGNED && interior) {
-        st4(drow + x4, val);
-        return;
+// Column fold: push row value v into the shift register, return the finished
+// output (row y-RAD). acc[j] holds the partial sum of output y-RAD+... started
+// j+1 rows ago; every update is acc + v*w[j], exactly the reference's order.
+template <int RAD, int NACC>
+__device__ __forceinline__ F4 col_fold(F4 (&acc)[NACC], const F4& v, const float* w, float one) {
+    F4 out;
+    (void)one;
+    if (RAD == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out.v[c] = fm(v.v[c], w[0]);
+        return out;
     }
+#if SC_F2
+#pragma unroll
+    for (int c = 0; c < 4; c += 2) {
+        const float2 one2 = make_float2(one, one);
+        const float2 vv = make_float2(v.v[c], v.v[c + 1]);
+        float2 t = mad2(make_float2(acc[NACC - 1].v[c], acc[NACC - 1].v[c + 1]), vv,
+                        make_float2(w[2 * RAD], w[2 * RAD]), one2);
+        out.v[c] = t.x;
+        out.v[c + 1] = t.y;
+#pragma unroll
+        for (int j = NACC - 1; j >= 1; --j) {
+            t = mad2(make_float2(acc[j - 1].v[c], acc[j - 1].v[c + 1]), vv, make_float2(w[j], w[j]), one2);
+            acc[j].v[c] = t.x;
+            acc[j].v[c + 1] = t.y;
+        }
+        t = __fmul2_rn(vv, make_float2(w[0], w[0]));
+        acc[0].v[c] = t.x;
+        acc[0].v[c + 1] = t.y;
+    }
+#else
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out.v[c] = fa(acc[NACC - 1].v[c], fm(v.v[c], w[2 * RAD]));
+#pragma unroll
+    for (int j = NACC - 1; j >= 1; --j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[j].v[c] = fa(acc[j - 1].v[c], fm(v.v[c], w[j]));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[0].v[c] = fm(v.v[c], w[0]);
+#endif
+    return out;
+}
+
+// Dense fold (single pass): input row yi carries kernel row i of output yi+RAD-i.
+template <int RAD, int NACC>
+__device__ __forceinline__ F4 dense_fold(F4 (&acc)[NACC], const float (&win)[12], const float* k, float one) {
+    constexpr int W = 2 * RAD + 1;
+    F4 out;
+    (void)one;
+    if (RAD == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out.v[c] = fm(win[HALO + c], k[0]);
+        return out;
+    }
+#if SC_F2
+    const float2 one2 = make_float2(one, one);
+#pragma unroll
+    for (int c = 0; c < 4; c += 2) {
+        const int o = HALO - RAD + c;
+        float2 t = make_float2(acc[NACC - 1].v[c], acc[NACC - 1].v[c + 1]);
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            t = mad2(t, make_float2(win[o + j], win[o + j + 1]),
+                     make_float2(k[(W - 1) * W + j], k[(W - 1) * W + j]), one2);
+        out.v[c] = t.x;
+        out.v[c + 1] = t.y;
+#pragma unroll
+        for (int i = NACC - 1; i >= 1; --i) {
+            t = make_float2(acc[i - 1].v[c], acc[i - 1].v[c + 1]);
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                t = mad2(t, make_float2(win[o + j], win[o + j + 1]), make_float2(k[i * W + j], k[i * W + j]),
+                         one2);
+            acc[i].v[c] = t.x;
+            acc[i].v[c + 1] = t.y;
+        }
+        t = __fmul2_rn(make_float2(win[o], win[o + 1]), make_float2(k[0], k[0]));
+#pragma unroll
+        for (int j = 1; j < W; ++j)
+            t = mad2(t, make_float2(win[o + j], win[o + j + 1]), make_float2(k[j], k[j]), one2);
+        acc[0].v[c] = t.x;
+        acc[0].v[c + 1] = t.y;
+    }
+#else
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        float t = acc[NACC - 1].v[c];
+#pragma unroll
+        for (int j = 0; j < W; ++j) t = fa(t, fm(win[HALO - RAD + c + j], k[(W - 1) * W + j]));
+        out.v[c] = t;
+    }
+#pragma unroll
+    for (int i = NACC - 1; i >= 1; --i) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float t = acc[i - 1].v[c];
+#pragma unroll
+            for (int j = 0; j < W; ++j) t = fa(t, fm(win[HALO - RAD + c + j], k[i * W + j]));
+            acc[i].v[c] = t;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        float t = fm(win[HALO - RAD + c], k[0]);
+#pragma unroll
+        for (int j = 1; j < W; ++j) t = fa(t, fm(win[HALO - RAD + c + j], k[j]));
+        acc[0].v[c] = t;
+    }
+#endif
+    return out;
+}
+
+// Store 4 columns of an output row with the column-ring policy (edge threads).
+//   ring_mode 0: keep -- only columns in [rad, C-rad) are written
+//   ring_mode 1: copy -- ring columns take `ringv` (the input samples)
+//   ring_mode 2: zero -- ring columns take 0
+template <bool ALIGNED>
+__device__ __noinline__ void store_edge(float* drow, int x4, int C, int rad, const F4& val, const F4& ringv,
+                                        int ring_mode) {
     if (x4 >= C) return;
     F4 o;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const int col = x4 + c;
-        const bool valid = col >= RAD_ && col < C - RAD_;
+        const bool valid = col >= rad && col < C - rad;
         o.v[c] = valid ? val.v[c] : (ring_mode == 1 ? ringv.v[c] : 0.0f);
     }
     if (ALIGNED && ring_mode != 0) {  // x4 + 4 <= C when C % 4 == 0
@@ -245,8 +451,148 @@ __device__ __forceinline__ void store_row(float* drow, int x4, int C, int RAD_, 
     for (int c = 0; c < 4; ++c) {
         const int col = x4 + c;
         if (col >= C) break;
-        const bool valid = col >= RAD_ && col < C - RAD_;
+        const bool valid = col >= rad && col < C - rad;
         if (valid || ring_mode != 0) drow[col] = o.v[c];
+    }
+}
+
+__device__ __forceinline__ void load_win(float (&win)[12], const float* s) {
+    const F4 a = ld4(s), b = ld4(s + 4), c = ld4(s + 8);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        win[i] = a.v[i];
+        win[4 + i] = b.v[i];
+        win[8 + i] = c.v[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Consumer: one item (plane, strip, band). ROW_EDGE items contain ring rows or
+// rows with a dead row pass; all others run the lean loop.
+
+template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE>
+__device__ __forceinline__ void consume_item(const Params& p, const Item& it, const float* ring, uint64_t* full,
+                                             uint64_t* empty, int& slot, uint32_t& phase, int& gs) {
+    constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
+    const int SW = p.tw + 2 * HALO;
+    const int NS = p.ns;
+    const int ct = threadIdx.x - 32;
+    const int lane = threadIdx.x & 31;
+    const int tw2 = p.tw / GROUPS;  // column offset between a thread's groups
+    const int R = p.R, C = p.C;
+    const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);
+    const bool zero_fill = (MODE == MODE_HPASS) && (p.flags & F_ZERO_FILL);
+
+    int x4[GROUPS];
+    bool fast[GROUPS];
+#pragma unroll
+    for (int g = 0; g < GROUPS; ++g) {
+        x4[g] = it.x0 + 4 * ct + g * tw2;
+        fast[g] = ALIGNED && x4[g] >= RAD && x4[g] + 4 <= C - RAD;
+    }
+    float* dplane = p.dst + (long long)it.plane * p.dst_plane_stride;
+
+    // rows whose output is emitted: HPASS emits row yi, the vertical modes row yi-RAD
+    int emit_lo, emit_hi;
+    if (MODE == MODE_HPASS) {
+        emit_lo = it.ylo;
+        emit_hi = it.yhi;
+    } else {
+        emit_lo = max(max(it.ylo, RAD), it.in_lo + RAD);
+        emit_hi = min(it.yhi, R - RAD);
+    }
+    float* dcur = dplane + (long long)(emit_lo - p.dst_row0) * p.dst_row_stride;
+
+    F4 acc[GROUPS][NACC];
+#pragma unroll
+    for (int g = 0; g < GROUPS; ++g)
+#pragma unroll
+        for (int j = 0; j < NACC; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[g][j].v[c] = 0.0f;
+
+    for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
+        if (r0 != it.in_lo) mbar_wait(&full[slot], phase);  // the item's first stage was waited by the caller
+        const int prev = (slot == 0) ? NS - 1 : slot - 1;
+        const float* sstage = ring + slot * SROWS * SW + 4 * ct;
+        const float* sprev = ring + prev * SROWS * SW + 4 * ct;
+#pragma unroll
+        for (int k = 0; k < SROWS; ++k) {
+            const int yi = r0 + k;
+            if (yi < it.in_hi) {
+                const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
+                const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
+                const bool emit = yo >= emit_lo && yo < emit_hi;
+#pragma unroll
+                for (int g = 0; g < GROUPS; ++g) {
+                    const float* srow = sstage + k * SW + g * tw2;
+                    float win[12];
+                    load_win(win, srow);
+                    F4 own;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) own.v[i] = win[4 + i];
+                    F4 outv;
+                    if (MODE == MODE_HPASS) {
+                        if (live) {
+                            outv = row_pass<RAD>(win, p.w, p.one);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) outv.v[i] = 0.0f;
+                        }
+                    } else if (MODE == MODE_SINGLE) {
+                        outv = dense_fold<RAD, NACC>(acc[g], win, p.k, p.one);
+                    } else {
+                        F4 v;
+                        if (MODE == MODE_FUSED) {
+                            if (live) {
+                                v = row_pass<RAD>(win, p.w, p.one);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) v.v[i] = 0.0f;  // faithful: scratch row stays 0
+                            }
+                        } else {
+                            v = own;  // VPASS: src already holds the row-pass result
+                        }
+                        outv = col_fold<RAD, NACC>(acc[g], v, p.w, p.one);
+                    }
+                    if (MODE == MODE_HPASS) {
+                        // dead rows are written only under zero fill
+                        if (emit && (live || zero_fill)) {
+                            if (fast[g] && live)
+                                st4(dcur + 4 * ct + g * tw2 + (it.x0), outv);
+                            else
+                                store_edge<ALIGNED>(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
+                        }
+                    } else if (emit) {
+                        if (fast[g]) {
+                            st4(dcur + x4[g], outv);
+                        } else {
+                            F4 ringv;
+                            if (ring_copy) {
+                                const float* rrow =
+                                    (k >= RAD) ? sstage + (k - RAD) * SW : sprev + (k - RAD + SROWS) * SW;
+                                ringv = ld4(rrow + g * tw2 + 4);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) ringv.v[i] = 0.0f;
+                            }
+                            store_edge<ALIGNED>(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                        }
+                    }
+                    if (ROW_EDGE && ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD)) {
+                        float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
+                        store_edge<ALIGNED>(drow, x4[g], C, 0, own, own, 1);
+                    }
+                }
+                if (emit) dcur += p.dst_row_stride;
+            }
+        }
+        // this stage is done; release the previous one (kept for the RAD-row lag)
+        if (gs >= 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[prev]);
+        }
+        if (++slot == NS) { slot = 0; phase ^= 1u; }
     }
 }
 
@@ -256,16 +602,16 @@ __device__ __forceinline__ void store_row(float* drow, int x4, int C, int RAD_, 
 template <int MODE, int RAD, bool ALIGNED>
 __global__ void __launch_bounds__(MAX_THREADS, 1) sepconv_rows_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int NR = p.nr;
+    const int NS = p.ns;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-    uint64_t* empty = full + NR;
-    float* ring = reinterpret_cast<float*>(smem_raw + ((2 * NR * 8 + 127) / 128) * 128);
+    uint64_t* empty = full + NS;
+    int* sitem = reinterpret_cast<int*>(empty + NS);
+    float* ring = reinterpret_cast<float*>(smem_raw + ((2 * NS * 8 + NS * 4 + 127) / 128) * 128);
     const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
     const int ncw = (blockDim.x >> 5) - 1;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NR; ++i) {
+        for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], ALIGNED ? 1u : 32u);
             mbar_init(&empty[i], (uint32_t)ncw);
         }
@@ -274,150 +620,22 @@ __global__ void __launch_bounds__(MAX_THREADS, 1) sepconv_rows_kernel(const __gr
     __syncthreads();
 
     if (warp == 0) {
-        producer<MODE, RAD, ALIGNED>(p, ring, full, empty);
+        producer<MODE, RAD, ALIGNED>(p, ring, full, empty, sitem);
         return;
     }
 
-    constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
-    constexpr int LAG = RAD;  // rows kept after use (FUSED reads row y-r for ring columns)
-    const int SW = p.tw + 2 * HALO;
-    const int ct = threadIdx.x - 32;
-    const int R = p.R, C = p.C;
-    const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);
-    const bool zero_fill = (MODE == MODE_HPASS) && (p.flags & F_ZERO_FILL);
-
     int slot = 0;
     uint32_t phase = 0;
-    long long g = 0;
-
-    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
+    int gs = 0;
+    for (;;) {
+        mbar_wait(&full[slot], phase);
+        const int item = sitem[slot];
+        if (item < 0) break;
         const Item it = decode_item<MODE, RAD>(p, item);
-        const int x4 = it.x0 + 4 * ct;
-        float* dplane = p.dst + (long long)it.plane * p.dst_plane_stride;
-        const int v_lo = max(it.ylo, RAD);
-        const int v_hi = min(it.yhi, R - RAD);
-
-        F4 acc[NACC];
-#pragma unroll
-        for (int j = 0; j < NACC; ++j)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[j].v[c] = 0.0f;
-
-        for (int yi = it.in_lo; yi < it.in_hi; ++yi, ++g) {
-            mbar_wait(&full[slot], phase);
-            const float* srow = ring + slot * SW + 4 * ct;  // smem col 0 of this thread = x4 - 4
-            float win[12];
-            {
-                const F4 a = ld4(srow), b = ld4(srow + 4), c = ld4(srow + 8);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) { win[i] = a.v[i]; win[4 + i] = b.v[i]; win[8 + i] = c.v[i]; }
-            }
-            F4 own;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) own.v[i] = win[4 + i];
-
-            if (MODE == MODE_HPASS) {
-                float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
-                if (yi >= p.hrow_lo && yi < p.hrow_hi) {
-                    const F4 h = row_pass<RAD>(win, p.w);
-                    store_row<ALIGNED>(drow, x4, C, RAD, h, own, zero_fill ? 2 : 0);
-                } else if (zero_fill) {
-                    F4 z;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) z.v[i] = 0.0f;
-                    store_row<ALIGNED>(drow, x4, C, 0, z, z, 2);
-                }
-            } else {
-                // value entering the vertical fold for this input row
-                F4 v;
-                F4 outv;
-                if (MODE == MODE_SINGLE) {
-                    // dense fold, row-major: kernel row i of output (yi + RAD - i)
-                    if (RAD == 0) {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) outv.v[c] = fm(win[HALO + c], p.k[0]);
-                    } else {
-                        constexpr int W = 2 * RAD + 1;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            float t = acc[NACC - 1].v[c];
-#pragma unroll
-                            for (int j = 0; j < W; ++j) t = fa(t, fm(win[HALO - RAD + c + j], p.k[(W - 1) * W + j]));
-                            outv.v[c] = t;
-                        }
-#pragma unroll
-                        for (int i = NACC - 1; i >= 1; --i) {
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                float t = acc[i - 1].v[c];
-#pragma unroll
-                                for (int j = 0; j < W; ++j) t = fa(t, fm(win[HALO - RAD + c + j], p.k[i * W + j]));
-                                acc[i].v[c] = t;
-                            }
-                        }
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            float t = fm(win[HALO - RAD + c], p.k[0]);
-#pragma unroll
-                            for (int j = 1; j < W; ++j) t = fa(t, fm(win[HALO - RAD + c + j], p.k[j]));
-                            acc[0].v[c] = t;
-                        }
-                    }
-                } else {
-                    if (MODE == MODE_FUSED) {
-                        if (yi >= p.hrow_lo && yi < p.hrow_hi) {
-                            v = row_pass<RAD>(win, p.w);
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) v.v[c] = 0.0f;  // faithful: scratch row stays 0
-                        }
-                    } else {
-                        v = own;  // VPASS: src already holds the row-pass result
-                    }
-                    if (RAD == 0) {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) outv.v[c] = fm(v.v[c], p.w[0]);
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) outv.v[c] = fa(acc[NACC - 1].v[c], fm(v.v[c], p.w[2 * RAD]));
-#pragma unroll
-                        for (int j = NACC - 1; j >= 1; --j)
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) acc[j].v[c] = fa(acc[j - 1].v[c], fm(v.v[c], p.w[j]));
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) acc[0].v[c] = fm(v.v[c], p.w[0]);
-                    }
-                }
-
-                const int yo = yi - RAD;
-                if (yo >= v_lo && yo < v_hi && yo >= it.in_lo + RAD) {
-                    float* drow = dplane + (long long)(yo - p.dst_row0) * p.dst_row_stride;
-                    F4 ringv;
-                    if (ring_copy) {
-                        int s2 = slot - LAG;
-                        if (s2 < 0) s2 += NR;
-                        ringv = ld4(ring + s2 * SW + 4 * ct + 4);
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) ringv.v[c] = 0.0f;
-                    }
-                    store_row<ALIGNED>(drow, x4, C, RAD, outv, ringv, ring_copy ? 1 : 0);
-                }
-                if (ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD)) {
-                    float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
-                    if (x4 < C) store_row<ALIGNED>(drow, x4, C, 0, own, own, 1);
-                }
-            }
-
-            // release the row LAG rows back (it is no longer read by anyone)
-            if (g >= LAG) {
-                int s2 = slot - LAG;
-                if (s2 < 0) s2 += NR;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s2]);
-            }
-            if (++slot == NR) { slot = 0; phase ^= 1u; }
-        }
+        if (item_rows_edge<MODE, RAD>(p, it))
+            consume_item<MODE, RAD, ALIGNED, true>(p, it, ring, full, empty, slot, phase, gs);
+        else
+            consume_item<MODE, RAD, ALIGNED, false>(p, it, ring, full, empty, slot, phase, gs);
     }
 }
 

@@ -1,0 +1,194 @@
+"""`convolve_image` with a CUDA execution plan (S/executors.py:269-412).
+
+The reference's plans schedule row blocks on CPU threads (Sequential,
+StaticChunked, TaskPool); here one plan type, `Cuda`, replaces all three: every
+plane of the image is covered by ONE grid launch per pass (the reference's
+plane agglomeration, S/executors.py:334-356, taken to its limit), and the
+results are bit-identical to every reference plan (T/test_executors.py:188-231).
+
+Two-pass end states, per buffer residency:
+  * device image, or host image with Cuda(fused=False): the split pair K2+K3
+    reproduces the reference exactly -- workspace = H0 scratch, image = V(H0).
+  * host image with Cuda(fused=True) (default): the streamed fused path
+    (H2D -> K1 -> D2H, in place on the host planes). image is bit-identical;
+    the workspace is not used as scratch and keeps its previous contents.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+from . import _lib
+from .conv import Algorithm, ConvVariant, OpCounter
+from .errors import InvalidArgumentError, UnsupportedCombinationError, UnsupportedWidthError
+from .image import Image, valid_region
+from .kernels import SeparableKernel, outer_product
+from .multi import partition_block  # noqa: F401  (re-exported like the reference)
+
+
+@dataclass(frozen=True)
+class Cuda:
+    """Run on one CUDA device. device=None: the image's device (or the current one
+    for host images). fused: stream host images through the fused kernel."""
+
+    device: int | None = None
+    fused: bool = True
+
+    def __post_init__(self):
+        if self.device is not None and self.device < 0:
+            raise InvalidArgumentError(f"device must be >= 0, got {self.device}")
+
+
+ExecPlan = Cuda
+
+
+def make_plan(mode: str, workers: int | None = None, cutoff: int = 100, agglomerate: bool = False,
+              *, device: int | None = None, fused: bool = True) -> ExecPlan:
+    """Plan from loose configuration (CLI flags, request bodies), S/executors.py:88-109.
+
+    mode "cuda" is the B200 plan. The reference's CPU thread modes are not part of
+    this build and raise UnsupportedCombinationError naming the replacement.
+    """
+    if mode == "cuda":
+        if agglomerate:
+            # every launch already covers all planes; accepted for compatibility
+            pass
+        return Cuda(device=device, fused=fused)
+    if mode in ("sequential", "static", "taskpool"):
+        raise UnsupportedCombinationError(
+            f"plan mode {mode!r} schedules CPU threads; the B200 build runs mode 'cuda'"
+        )
+    raise InvalidArgumentError(f"unknown plan mode {mode!r}")
+
+
+@dataclass
+class LaunchStats:
+    """Kernel launches issued and wall time (S/executors.py:112-118)."""
+
+    parallel_region_launches: int = 0
+    tasks_spawned: int = 0
+    wall_time_ns: int = 0
+
+
+def _stacked(image: Image):
+    """A (P, R, C) strided view when the planes are evenly spaced in one CUDA
+    allocation (one grid for all planes), else None."""
+    import torch
+
+    ts = [p.data for p in image.planes]
+    t0 = ts[0]
+    if len(ts) == 1:
+        return t0.unsqueeze(0)
+    step = ts[1].data_ptr() - t0.data_ptr()
+    if step <= 0 or step % 4:
+        return None
+    for i, t in enumerate(ts):
+        if (t.data_ptr() - t0.data_ptr() != i * step or t.stride() != t0.stride()
+                or t.device != t0.device or t.untyped_storage().data_ptr() != t0.untyped_storage().data_ptr()):
+            return None
+    ps = step // 4
+    rs = t0.stride(0)
+    if ps < image.rows * rs:
+        return None
+    return torch.as_strided(t0, (len(ts), image.rows, image.cols), (ps, rs, 1))
+
+
+def _device_groups(image: Image):
+    st = _stacked(image)
+    if st is not None:
+        return [st]
+    return [p.data.unsqueeze(0) for p in image.planes]
+
+
+def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, plan: ExecPlan, *,
+                   vectorized: bool = True, workspace: Image | None = None, pool=None,
+                   counter: OpCounter | None = None) -> LaunchStats:
+    """Convolve every plane of `image` (S/executors.py:269-405), on the GPU.
+
+    Single-pass variants write `workspace` (allocated if not given) and optionally
+    copy the valid region back into `image`; two-pass finishes with the result in
+    `image`. Returns launch statistics; samples are bit-identical to the reference.
+    """
+    import torch
+
+    from . import device as dev
+
+    if variant.algorithm is Algorithm.SINGLE_PASS_UNROLLED5 and kernel.width != 5:
+        raise UnsupportedWidthError(f"unrolled variant needs width 5, got {kernel.width}")
+    if not isinstance(plan, Cuda):
+        raise UnsupportedCombinationError(
+            f"plan {plan!r} is a CPU thread plan; pass Cuda() (make_plan('cuda'))"
+        )
+    if counter is not None:
+        raise InvalidArgumentError("operation counters are supported for sequential runs only")
+    if pool is not None:
+        raise UnsupportedCombinationError("worker pools belong to the CPU plans; Cuda() takes none")
+
+    rows, cols = image.rows, image.cols
+    r = kernel.radius
+    region = valid_region(rows, cols, r)
+    nplanes = image.plane_count
+    on_dev = image.on_device
+    if not on_dev and any(p.on_device for p in image.planes):
+        raise InvalidArgumentError("image planes must all be host arrays or all CUDA tensors")
+    if workspace is None:
+        workspace = Image.zeros_like(image)
+    if workspace.rows != rows or workspace.cols != cols or workspace.plane_count != nplanes:
+        raise InvalidArgumentError("workspace must match the image's dimensions")
+    if workspace.on_device != on_dev:
+        raise InvalidArgumentError("workspace must live where the image lives")
+
+    stats = LaunchStats()
+    before = _lib.launch_count()
+    t0 = time.perf_counter_ns()
+    two_pass = variant.algorithm is Algorithm.TWO_PASS
+
+    if on_dev:
+        device_index = image.planes[0].data.device
+        with torch.cuda.device(device_index):
+            img_groups = _device_groups(image)
+            ws_groups = _device_groups(workspace)
+            if len(img_groups) != len(ws_groups):
+                img_groups = [p.data.unsqueeze(0) for p in image.planes]
+                ws_groups = [p.data.unsqueeze(0) for p in workspace.planes]
+            for ig, wg in zip(img_groups, ws_groups):
+                if two_pass:
+                    dev.two_pass_split(ig, wg, kernel.weights)
+                else:
+                    dev.single_pass(ig, outer_product(kernel).matrix, wg, copy_back=variant.copy_back)
+            torch.cuda.current_stream().synchronize()
+    else:
+        device_index = plan.device if plan.device is not None else torch.cuda.current_device()
+        if two_pass and plan.fused:
+            planes = [p.data for p in image.planes]
+            dev.two_pass_host(planes, planes, kernel.weights, device=device_index)
+        else:
+            with torch.cuda.device(device_index):
+                src = torch.stack([torch.from_numpy(p.data) for p in image.planes]).cuda()
+                wsd = torch.stack([torch.from_numpy(p.data) for p in workspace.planes]).cuda()
+                if two_pass:
+                    dev.two_pass_split(src, wsd, kernel.weights)
+                else:
+                    dev.single_pass(src, outer_product(kernel).matrix, wsd, copy_back=variant.copy_back)
+                src_h, wsd_h = src.cpu().numpy(), wsd.cpu().numpy()
+            rl, rh, cl, ch = region.row_lo, region.row_hi, region.col_lo, region.col_hi
+            for p in range(nplanes):
+                if two_pass:
+                    image.planes[p].data[rl:rh, cl:ch] = src_h[p, rl:rh, cl:ch]
+                    workspace.planes[p].data[...] = wsd_h[p]
+                else:
+                    workspace.planes[p].data[rl:rh, cl:ch] = wsd_h[p, rl:rh, cl:ch]
+                    if variant.copy_back:
+                        image.planes[p].data[rl:rh, cl:ch] = src_h[p, rl:rh, cl:ch]
+
+    stats.wall_time_ns = time.perf_counter_ns() - t0
+    stats.parallel_region_launches = _lib.launch_count() - before
+    return stats
+
+
+def result_image(image: Image, workspace: Image, variant: ConvVariant) -> Image:
+    """Where the convolved samples live after convolve_image (S/executors.py:408-412)."""
+    if variant.algorithm is Algorithm.TWO_PASS or variant.copy_back:
+        return image
+    return workspace

@@ -1,0 +1,204 @@
+"""Host-side logic on CPU: the C ABI library loads and exports what the header
+declares, validates before launching, and the Python mirror of the reference
+interface keeps the reference's names, argument meaning and errors."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden
+
+HEADER = os.path.join(ROOT, "include", "sepconv_b200.h")
+
+
+def header_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(sc_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1711_09791_b200 import _lib
+
+    L = _lib.load()
+    declared = header_symbols()
+    assert declared, "no declarations parsed from the header"
+    assert set(declared) == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.sc_abi_version() == 1
+    assert L.sc_launch_count() == 0
+
+
+def _fused(L, src, dst, nplanes, rows, cols, width, flags=0):
+    taps = (ctypes.c_float * max(width, 1))(*([0.2] * max(width, 1)))
+    return L.sc_two_pass_fused_f32(src, dst, nplanes, rows, cols, rows * cols, rows * cols, cols, cols,
+                                   taps, width, flags, None)
+
+
+def test_abi_validates_before_launch():
+    """Status codes for the reference's error classes; nothing reaches the GPU."""
+    from paper_1711_09791_b200 import _lib
+
+    L = _lib.load()
+    buf = (ctypes.c_float * 64)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    assert _fused(L, p, p, 1, 8, 8, 4) == _lib.SC_INVALID_ARGUMENT          # even width
+    assert _fused(L, p, p, 1, 8, 8, 11) == _lib.SC_UNSUPPORTED_WIDTH        # > 9
+    assert _fused(L, p, p, 1, 4, 8, 5) == _lib.SC_INVALID_DIMENSION         # rows < width
+    assert b"smaller than kernel width" in L.sc_last_error()
+    assert _fused(L, p, p, 0, 8, 8, 5) == _lib.SC_INVALID_ARGUMENT          # no planes
+    # host memory is refused (no CPU fallback): the pointer is not device memory
+    other = (ctypes.c_float * 64)()
+    q = ctypes.cast(other, ctypes.c_void_p)
+    assert _fused(L, p, q, 1, 8, 8, 5) == _lib.SC_INVALID_ARGUMENT
+    # band geometry: source band must cover output rows plus halo
+    taps = (ctypes.c_float * 5)(*([0.2] * 5))
+    rc = L.sc_two_pass_band_f32(p, q, 1, 100, 8, 800, 800, 8, 8, 10, 20, 10, 10, 30, taps, 5, 0, None)
+    assert rc == _lib.SC_INVALID_ARGUMENT and b"halo" in L.sc_last_error()
+    assert L.sc_fill_synthetic_f32(p, 10, 1, 0, 7, None) == _lib.SC_INVALID_ARGUMENT
+    assert L.sc_launch_count() == 0
+
+
+def test_status_maps_to_reference_exceptions():
+    from paper_1711_09791_b200 import _lib
+    from paper_1711_09791_b200.errors import (
+        ExecutionError,
+        InvalidArgumentError,
+        InvalidDimensionError,
+        SepconvError,
+        UnsupportedWidthError,
+    )
+
+    _lib.load()
+    for code, exc in ((1, InvalidArgumentError), (2, InvalidDimensionError), (3, UnsupportedWidthError),
+                      (4, ExecutionError)):
+        with pytest.raises(exc):
+            _lib.check(code)
+        assert issubclass(exc, SepconvError)
+    _lib.check(0)
+
+
+def test_missing_extension_fails_loudly(tmp_path, monkeypatch):
+    from paper_1711_09791_b200 import _lib
+
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "absent.so"))
+    with pytest.raises(_lib.ExtensionMissingError):
+        _lib.load()
+
+
+def test_kernels_mirror_reference(oracle):
+    from paper_1711_09791_b200.errors import InvalidArgumentError
+    from paper_1711_09791_b200.kernels import DenseKernel, SeparableKernel, delta, gaussian5, outer_product
+
+    k = gaussian5()
+    assert k.weights.tolist() == [0.0625, 0.25, 0.375, 0.25, 0.0625] and k.radius == 2
+    assert outer_product(k).matrix[0, 0] == np.float32(1 / 256)
+    for w in ([0.1, 0.7, 0.3], [-1, -2, 7, -2, -1], np.random.default_rng(3).standard_normal(9)):
+        sk = SeparableKernel(w)
+        assert np.array_equal(outer_product(sk).matrix, oracle.outer_product(sk.weights))
+    assert np.array_equal(outer_product(delta(5)).matrix, np.diag([0, 0, 1, 0, 0]).astype(np.float32))
+    with pytest.raises(InvalidArgumentError):
+        SeparableKernel([1.0, 2.0])
+    with pytest.raises(InvalidArgumentError):
+        DenseKernel(np.ones((2, 3)))
+
+
+def test_image_model_mirrors_reference():
+    from paper_1711_09791_b200.errors import InvalidArgumentError, InvalidDimensionError
+    from paper_1711_09791_b200.image import Image, Plane, ValidRegion, make_synthetic, max_abs_diff, valid_region
+
+    z = load_golden("synthetic")
+    img = make_synthetic(8, 8, 3, seed=42)
+    assert np.array_equal(np.stack([p.data for p in img.planes]), z["make_synthetic_8x8x3_s42"])
+    assert valid_region(1152, 1152, 2) == ValidRegion(2, 1150, 2, 1150)
+    with pytest.raises(InvalidDimensionError):
+        valid_region(4, 9, 2)
+    with pytest.raises(InvalidDimensionError):
+        make_synthetic(4, 5, 1, seed=0)
+    with pytest.raises(InvalidArgumentError):
+        Image([Plane.zeros(5, 5), Plane.zeros(5, 6)])
+    with pytest.raises(InvalidArgumentError):
+        Plane(np.zeros(5))
+    a, b = Plane.full(6, 6, 1.0), Plane.full(6, 6, 1.5)
+    assert max_abs_diff(a, b, valid_region(6, 6, 2)) == 0.5
+    p = Plane(np.arange(12, dtype=np.float64).reshape(3, 4))
+    assert p.data.dtype == np.float32 and p.data.flags.c_contiguous
+
+
+def test_conv_api_checks_and_counts():
+    from paper_1711_09791_b200.conv import (
+        Algorithm,
+        ConvVariant,
+        _check_pair,
+        arith_count,
+        doubly_interior_region,
+    )
+    from paper_1711_09791_b200.errors import InvalidArgumentError, InvalidDimensionError
+    from paper_1711_09791_b200.image import Plane
+
+    # T/test_conv.py:325-357 and SPEC.md:492 numbers
+    single = ConvVariant(Algorithm.SINGLE_PASS_GENERIC, copy_back=True)
+    two = ConvVariant(Algorithm.TWO_PASS, copy_back=True)
+    assert two.copy_back is False
+    assert arith_count(single, 1152, 1152, 5).multiplications == 25 * 1148 * 1148
+    assert arith_count(two, 64, 64, 5).multiplications == 10 * 60 * 60
+    assert arith_count(ConvVariant(Algorithm.SINGLE_PASS_GENERIC), 6, 7, 1).additions == 0
+    assert doubly_interior_region(12, 12, 2).row_lo == 4
+    src = Plane.zeros(8, 8)
+    with pytest.raises(InvalidArgumentError):
+        _check_pair(src, Plane.zeros(8, 9), 5)
+    with pytest.raises(InvalidArgumentError):
+        _check_pair(src, Plane(src.data[:, :]), 5)
+    with pytest.raises(InvalidDimensionError):
+        _check_pair(Plane.zeros(4, 8), Plane.zeros(4, 8), 5)
+
+
+def test_plans_and_dispatch_errors():
+    from paper_1711_09791_b200.conv import Algorithm, ConvVariant
+    from paper_1711_09791_b200.errors import (
+        InvalidArgumentError,
+        UnsupportedCombinationError,
+        UnsupportedWidthError,
+    )
+    from paper_1711_09791_b200.executors import Cuda, LaunchStats, convolve_image, make_plan, result_image
+    from paper_1711_09791_b200.image import Image
+    from paper_1711_09791_b200.kernels import SeparableKernel, gaussian5
+
+    assert make_plan("cuda") == Cuda()
+    with pytest.raises(UnsupportedCombinationError):
+        make_plan("static", workers=4)
+    with pytest.raises(InvalidArgumentError):
+        make_plan("bogus")
+    img = Image.zeros(8, 8, 3)
+    with pytest.raises(UnsupportedWidthError):
+        convolve_image(img, SeparableKernel([0.2, 0.6, 0.2]), ConvVariant(Algorithm.SINGLE_PASS_UNROLLED5), Cuda())
+    with pytest.raises(UnsupportedCombinationError):
+        convolve_image(img, gaussian5(), ConvVariant(Algorithm.TWO_PASS), object())
+    with pytest.raises(InvalidArgumentError):
+        convolve_image(img, gaussian5(), ConvVariant(Algorithm.TWO_PASS), Cuda(), counter=object())
+    with pytest.raises(InvalidArgumentError):
+        convolve_image(img, gaussian5(), ConvVariant(Algorithm.TWO_PASS), Cuda(), workspace=Image.zeros(8, 9, 3))
+    assert LaunchStats() == LaunchStats(0, 0, 0)
+    ws = Image.zeros(8, 8, 3)
+    assert result_image(img, ws, ConvVariant(Algorithm.TWO_PASS)) is img
+    assert result_image(img, ws, ConvVariant(Algorithm.SINGLE_PASS_GENERIC)) is ws
+    assert result_image(img, ws, ConvVariant(Algorithm.SINGLE_PASS_GENERIC, copy_back=True)) is img
+
+
+def test_partition_block_matches_reference_rule():
+    from paper_1711_09791_b200.errors import InvalidArgumentError
+    from paper_1711_09791_b200.multi import partition_block
+
+    # S/executors.py:121-139: first n mod k chunks one longer; empty trailing chunks
+    assert [partition_block(0, 10, i, 4) for i in range(4)] == [(0, 3), (3, 6), (6, 8), (8, 10)]
+    assert [partition_block(2, 4, i, 3) for i in range(3)] == [(2, 3), (3, 4), (4, 4)]
+    with pytest.raises(InvalidArgumentError):
+        partition_block(0, 10, 4, 4)
+    with pytest.raises(InvalidArgumentError):
+        partition_block(5, 4, 0, 1)
