@@ -22,7 +22,7 @@ LIB = os.path.join(PKG, "libsepconv_b200.so")
 OBJ = os.path.join(PKG, "csrc", "_obj")
 
 SOURCES = ["capi.cu", "stream.cu", "kern_aux.cu", "kern_fused.cu", "kern_hpass.cu", "kern_vpass.cu", "kern_single.cu"]
-HEADERS = ["kernels.cuh", "launch.h"]
+HEADERS = ["kernels.cuh", "direct.cuh", "launch.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -18,6 +18,7 @@
 #include <tuple>
 
 #include "../../include/sepconv_b200.h"
+#include "direct.cuh"
 #include "kernels.cuh"
 #include "launch.h"
 
@@ -186,15 +187,32 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     if (j.dense)
         for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];
 
-    const int nt = choose_nt(j.C);
-    p.tw = COLS_PER_THREAD * nt;
+    // Kernel family: the TMA stage pipeline (default) or the register-streaming
+    // direct kernel (SC_DIRECT=1), both bit-identical.
+    const bool direct = aligned && env_int("SC_DIRECT", 0) != 0;
+    int nt, threads, ns = 0;
+    size_t smem = 0;
+    if (direct) {
+        switch (j.mode) {
+            case MODE_FUSED: kern = kernel_fused_direct(rad); break;
+            case MODE_HPASS: kern = kernel_hpass_direct(rad); break;
+            case MODE_VPASS: kern = kernel_vpass_direct(rad); break;
+            case MODE_SINGLE: kern = kernel_single_direct(rad); break;
+        }
+        nt = 32;
+        p.tw = 128;
+        threads = 32 * DWARPS;
+    } else {
+        nt = choose_nt(j.C);
+        p.tw = COLS_PER_THREAD * nt;
+        ns = env_int("SC_NS", 4);
+        if (ns < 3) ns = 3;
+        if (ns > 16) ns = 16;
+        threads = 32 + nt;
+        smem = (size_t)((2 * ns * 8 + ns * 4 + 127) / 128) * 128 + (size_t)ns * SROWS * (p.tw + 2 * HALO) * 4;
+    }
     p.nstrips = (j.C + p.tw - 1) / p.tw;
-    int ns = env_int("SC_NS", 4);
-    if (ns < 3) ns = 3;
-    if (ns > 16) ns = 16;
     p.ns = ns;
-    const int threads = 32 + nt;
-    const size_t smem = (size_t)((2 * ns * 8 + ns * 4 + 127) / 128) * 128 + (size_t)ns * SROWS * (p.tw + 2 * HALO) * 4;
 
     int dev = 0;
     cudaGetDevice(&dev);
@@ -202,18 +220,17 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     int occ = occupancy(kern, threads, smem);
     const int occ_cap = env_int("SC_OCC", 0);
     if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;
-    const long long G = (long long)di.sms * occ;
+    const long long G = (long long)di.sms * occ * (direct ? DWARPS : 1);  // concurrent workers
 
     // Row-band height. Items are claimed dynamically (atomic ticket), so short
     // bands cost nothing in balance; they only re-read a 2r-row halo (mostly
     // from L2, since neighbouring bands run concurrently). ~64 rows measured
-    // best on B200 at 16384^2 (tools/sweep.py); keep >= ~8 items per CTA slot.
+    // best on B200 at 16384^2 (tools/sweep.py); keep >= ~2 items per worker.
     const int rows_out = j.out_hi - j.out_lo;
     const long long units = (long long)j.nplanes * p.nstrips;
     int band_h = env_int("SC_BAND_H", 0);
     if (band_h <= 0) {
         band_h = 64;
-        // small images: shrink bands until every CTA slot has work
         while (band_h > 8 && units * ((rows_out + band_h - 1) / band_h) < 2 * G) band_h /= 2;
         if (band_h > rows_out) band_h = rows_out;
     }
@@ -222,7 +239,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     const long long nitems = units * nbands;
     if (nitems > 0x7fffffffLL) return fail(SC_INVALID_ARGUMENT, "too many work items");
     p.nitems = (int)nitems;
-    const int grid = (int)(nitems < G ? nitems : G);
+    const long long ctas = direct ? (nitems + DWARPS - 1) / DWARPS : nitems;
+    const int grid = (int)(ctas < (long long)di.sms * occ ? ctas : (long long)di.sms * occ);
     p.work = work_slot(dev);
     if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
 

@@ -1,6 +1,7 @@
 // Instantiates the row-streaming kernel for MODE_FUSED (one TU per mode keeps
 // nvcc builds parallel). See kernels.cuh.
 #include "kernels.cuh"
+#include "direct.cuh"
 #include "launch.h"
 
 namespace sc {
@@ -20,6 +21,17 @@ const void* kernel_fused(int rad, bool aligned) {
             return nullptr;
     }
 #undef SC_K
+}
+
+const void* kernel_fused_direct(int rad) {
+    switch (rad) {
+        case 0: return (const void*)sepconv_direct_kernel<MODE_FUSED, 0>;
+        case 1: return (const void*)sepconv_direct_kernel<MODE_FUSED, 1>;
+        case 2: return (const void*)sepconv_direct_kernel<MODE_FUSED, 2>;
+        case 3: return (const void*)sepconv_direct_kernel<MODE_FUSED, 3>;
+        case 4: return (const void*)sepconv_direct_kernel<MODE_FUSED, 4>;
+        default: return nullptr;
+    }
 }
 
 }  // namespace sc

@@ -1,6 +1,7 @@
 // Instantiates the row-streaming kernel for MODE_HPASS (one TU per mode keeps
 // nvcc builds parallel). See kernels.cuh.
 #include "kernels.cuh"
+#include "direct.cuh"
 #include "launch.h"
 
 namespace sc {
@@ -20,6 +21,17 @@ const void* kernel_hpass(int rad, bool aligned) {
             return nullptr;
     }
 #undef SC_K
+}
+
+const void* kernel_hpass_direct(int rad) {
+    switch (rad) {
+        case 0: return (const void*)sepconv_direct_kernel<MODE_HPASS, 0>;
+        case 1: return (const void*)sepconv_direct_kernel<MODE_HPASS, 1>;
+        case 2: return (const void*)sepconv_direct_kernel<MODE_HPASS, 2>;
+        case 3: return (const void*)sepconv_direct_kernel<MODE_HPASS, 3>;
+        case 4: return (const void*)sepconv_direct_kernel<MODE_HPASS, 4>;
+        default: return nullptr;
+    }
 }
 
 }  // namespace sc

@@ -433,7 +433,7 @@ __device__ __forceinline__ F4 dense_fold(F4 (&acc)[NACC], const float (&win)[12]
 //   ring_mode 1: copy -- ring columns take `ringv` (the input samples)
 //   ring_mode 2: zero -- ring columns take 0
 template <bool ALIGNED>
-__device__ __noinline__ void store_edge(float* drow, int x4, int C, int rad, const F4& val, const F4& ringv,
+__device__ __forceinline__ void store_edge(float* drow, int x4, int C, int rad, const F4& val, const F4& ringv,
                                         int ring_mode) {
     if (x4 >= C) return;
     F4 o;

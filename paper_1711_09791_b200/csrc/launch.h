@@ -15,6 +15,10 @@ const void* kernel_fused(int rad, bool aligned);
 const void* kernel_hpass(int rad, bool aligned);
 const void* kernel_vpass(int rad, bool aligned);
 const void* kernel_single(int rad, bool aligned);
+const void* kernel_fused_direct(int rad);
+const void* kernel_hpass_direct(int rad);
+const void* kernel_vpass_direct(int rad);
+const void* kernel_single_direct(int rad);
 
 cudaError_t launch_copy_region(const float* src, float* dst, long long sps, long long dps, long long srs,
                                long long drs, int nplanes, int row_lo, int nrows, int col_lo, int ncols,

@@ -202,3 +202,62 @@ def test_partition_block_matches_reference_rule():
         partition_block(0, 10, 4, 4)
     with pytest.raises(InvalidArgumentError):
         partition_block(5, 4, 0, 1)
+
+
+def test_hot_kernels_use_no_local_memory():
+    """Regression guard: a stack frame in the row kernels turned every output row
+    into local-memory stores that doubled L1->L2 write traffic.
+    Every hot kernel must compile without STL/LDL."""
+    import shutil
+    import subprocess
+
+    from paper_1711_09791_b200 import _lib
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    current, bad = None, []
+    for line in sass.splitlines():
+        if "Function :" in line:
+            current = line.split("Function :")[1].strip()
+        elif current and "sepconv_" in current and re.search(r"\b(STL|LDL)\b", line):
+            bad.append(current)
+    # known exception: the 9x9 dense single pass (MODE 3, r = 4) holds 8 partial
+    # rows of 8 columns and spills; it is outside the five BASELINE workloads.
+    bad = [b for b in bad if "ILi3ELi4E" not in b]
+    assert not bad, sorted(set(bad))
+
+
+def test_packed_math_keeps_two_roundings():
+    """ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 (single rounding).
+    The kernels issue the add as FFMA2(product, run-time 1.0, acc); every FFMA2 in
+    the row kernels must therefore multiply by a uniform/constant operand that is
+    the run-time `one`, never by a tap product. Check: FFMA2 count never exceeds
+    the FMUL2 count (each mad2 is one FMUL2 + one FFMA2; first terms are FMUL2 only)."""
+    import shutil
+    import subprocess
+
+    from paper_1711_09791_b200 import _lib
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    counts, current = {}, None
+    for line in sass.splitlines():
+        if "Function :" in line:
+            current = line.split("Function :")[1].strip()
+            counts[current] = [0, 0, 0]
+        elif current:
+            if re.search(r"\bFMUL2\b", line):
+                counts[current][0] += 1
+            elif re.search(r"\bFFMA2\b", line):
+                counts[current][1] += 1
+            elif re.search(r"\bFFMA\b", line):
+                counts[current][2] += 1
+    for fn, (fmul2, ffma2, ffma) in counts.items():
+        if "sepconv_" not in fn:
+            continue
+        assert ffma == 0, f"scalar FFMA (contracted mul+add) in {fn}"
+        assert ffma2 <= fmul2, f"{fn}: {ffma2} FFMA2 vs {fmul2} FMUL2 -- contraction suspected"
