@@ -41,7 +41,8 @@ constexpr int F_EXTENDED = 0x1;
 constexpr int F_NO_RING = 0x2;
 constexpr int F_ZERO_FILL = 0x4;
 // tuning flags (set by the planner from SC_* environment variables)
-constexpr int F_L2_NORMAL = 0x100;  // no evict_first hint on the row loads
+constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (default: evict_normal,
+                                         // which lets neighbouring bands' halo rows hit in L2)
 constexpr int F_ST_CS = 0x200;      // streaming (.cs) stores
 
 constexpr int HALO = 4;       // smem columns kept either side of a strip (supports r <= 4)
@@ -224,7 +225,7 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
     const int SW = p.tw + 2 * HALO;
     const int NS = p.ns;
     uint64_t pol = 0;
-    if (ALIGNED) pol = (p.flags & F_L2_NORMAL) ? policy_evict_normal() : policy_evict_first();
+    if (ALIGNED) pol = (p.flags & F_L2_EVICT_FIRST) ? policy_evict_first() : policy_evict_normal();
     int slot = 0;
     uint32_t phase = 0;
     int gs = 0;

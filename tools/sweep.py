@@ -19,7 +19,7 @@ y = torch.empty_like(x)
 dense = np.outer(w, w).astype(np.float32)
 op = {"fused": lambda: dev.two_pass(x, w, y), "single": lambda: dev.single_pass(x, dense, y),
       "hpass": lambda: dev.hpass(x, w, y), "vpass": lambda: dev.vpass(x, w, y)}[a.op]
-KEYS = ["SC_NS", "SC_OCC", "SC_NT", "SC_BAND_H", "SC_L2_NORMAL", "SC_ST_CS"]
+KEYS = ["SC_NS", "SC_OCC", "SC_NT", "SC_BAND_H", "SC_L2_EVICT_FIRST", "SC_ST_CS"]
 def run(env):
     for k in KEYS: os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
@@ -36,7 +36,7 @@ grid += [{"SC_NS": n} for n in (3, 5, 6, 8)]
 grid += [{"SC_OCC": o} for o in (1, 2, 3)]
 grid += [{"SC_NT": t} for t in (32, 64, 96, 192, 256)]
 grid += [{"SC_BAND_H": b} for b in (64, 128, 256, 512, 1024, 2048)]
-grid += [{"SC_L2_NORMAL": 1}]
+grid += [{"SC_L2_EVICT_FIRST": 1}]
 grid += [{"SC_NT": 64, "SC_NS": 6}, {"SC_NT": 64, "SC_NS": 8}, {"SC_NT": 256, "SC_NS": 3}]
 if a.grid:
     grid = [json.loads(g) for g in a.grid.split(";")]
