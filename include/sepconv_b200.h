@@ -66,6 +66,15 @@ int sc_two_pass_band_f32(const float *src, float *dst, int nplanes, int global_r
                          int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
                          const float *taps, int width, int flags, void *stream);
 
+/* Same with two disjoint output segments in ONE launch (the band's top and
+ * bottom boundary rows after the halo exchange): [out_lo,out_hi) and
+ * [out_lo2,out_hi2); either may be empty. */
+int sc_two_pass_band2_f32(const float *src, float *dst, int nplanes, int global_rows, int cols,
+                          int64_t src_plane_stride, int64_t dst_plane_stride,
+                          int64_t src_row_stride, int64_t dst_row_stride,
+                          int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
+                          int out_lo2, int out_hi2, const float *taps, int width, int flags, void *stream);
+
 /* horizontal_rows_vec over rows [row_lo,row_hi) (S/conv.py:215-240; public
  * horizontal_pass uses [r, R-r), S/conv.py:362-375). SC_ZERO_FILL also zeroes
  * every other dst element (the two-pass scratch convention). */

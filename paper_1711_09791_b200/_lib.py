@@ -40,6 +40,7 @@ EXPORTS = (
     "sc_launch_count",
     "sc_two_pass_fused_f32",
     "sc_two_pass_band_f32",
+    "sc_two_pass_band2_f32",
     "sc_hpass_f32",
     "sc_vpass_f32",
     "sc_two_pass_split_f32",
@@ -71,6 +72,7 @@ _SIGNATURES = {
     "sc_launch_count": ([], _u64),
     "sc_two_pass_fused_f32": (_STRIDED + [_fp, _i32, _i32, _vp], _i32),
     "sc_two_pass_band_f32": (_STRIDED + [_i32, _i32, _i32, _i32, _i32, _fp, _i32, _i32, _vp], _i32),
+    "sc_two_pass_band2_f32": (_STRIDED + [_i32] * 7 + [_fp, _i32, _i32, _vp], _i32),
     "sc_hpass_f32": (_STRIDED + [_i32, _i32, _fp, _i32, _i32, _vp], _i32),
     "sc_vpass_f32": (_STRIDED + [_i32, _i32, _fp, _i32, _i32, _vp], _i32),
     "sc_two_pass_split_f32": (_STRIDED + [_fp, _i32, _i32, _vp], _i32),

@@ -159,7 +159,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         case MODE_SINGLE: kern = kernel_single(rad, aligned); break;
     }
     if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(j.width));
-    if (j.out_hi <= j.out_lo || j.nplanes <= 0) return SC_OK;
+    const bool seg2 = j.out_hi2 > j.out_lo2;
+    if ((j.out_hi <= j.out_lo && !seg2) || j.nplanes <= 0) return SC_OK;
 
     Params p;
     std::memset(&p, 0, sizeof(p));
@@ -177,6 +178,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.dst_row0 = j.dst_row0;
     p.out_lo = j.out_lo;
     p.out_hi = j.out_hi;
+    p.out_lo2 = seg2 ? j.out_lo2 : 0;
+    p.out_hi2 = seg2 ? j.out_hi2 : 0;
     p.hrow_lo = j.hrow_lo;
     p.hrow_hi = j.hrow_hi;
     p.flags = j.flags;
@@ -226,7 +229,9 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     // bands cost nothing in balance; they only re-read a 2r-row halo (mostly
     // from L2, since neighbouring bands run concurrently). ~64 rows measured
     // best on B200 at 16384^2 (tools/sweep.py); keep >= ~2 items per worker.
-    const int rows_out = j.out_hi - j.out_lo;
+    const int rows0 = j.out_hi > j.out_lo ? j.out_hi - j.out_lo : 0;
+    const int rows1 = seg2 ? j.out_hi2 - j.out_lo2 : 0;
+    const int rows_out = rows0 + rows1;
     const long long units = (long long)j.nplanes * p.nstrips;
     int band_h = env_int("SC_BAND_H", 0);
     if (band_h <= 0) {
@@ -235,10 +240,11 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         if (band_h > rows_out) band_h = rows_out;
     }
     p.band_h = band_h;
-    const long long nbands = (rows_out + band_h - 1) / band_h;
-    const long long nitems = units * nbands;
+    const long long nitems0 = units * ((rows0 + band_h - 1) / band_h);
+    const long long nitems = nitems0 + units * ((rows1 + band_h - 1) / band_h);
     if (nitems > 0x7fffffffLL) return fail(SC_INVALID_ARGUMENT, "too many work items");
     p.nitems = (int)nitems;
+    p.nitems0 = (int)nitems0;
     const long long ctas = direct ? (nitems + DWARPS - 1) / DWARPS : nitems;
     const int grid = (int)(ctas < (long long)di.sms * occ ? ctas : (long long)di.sms * occ);
     p.work = work_slot(dev);
@@ -314,29 +320,35 @@ const char* sc_last_error(void) { return t_err.c_str(); }
 
 uint64_t sc_launch_count(void) { return g_launches.load(); }
 
-int sc_two_pass_band_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
-                         int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
-                         int64_t dst_row_stride, int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
-                         const float* taps, int width, int flags, void* stream) {
+int sc_two_pass_band2_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
+                          int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                          int64_t dst_row_stride, int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
+                          int out_lo2, int out_hi2, const float* taps, int width, int flags, void* stream) {
     set_error("");
     SC_TRY(check_width(width));
     SC_TRY(check_dims(nplanes, global_rows, cols, width));
     if (!taps) return fail(SC_INVALID_ARGUMENT, "null taps");
     const int r = width / 2;
-    if (out_lo < 0 || out_hi > global_rows || out_lo > out_hi)
+    if (out_lo < 0 || out_hi > global_rows || out_lo > out_hi || out_lo2 < 0 || out_hi2 > global_rows ||
+        out_lo2 > out_hi2)
         return fail(SC_INVALID_ARGUMENT, "output rows out of range");
-    const int need_lo = out_lo - r > 0 ? out_lo - r : 0;
-    const int need_hi = out_hi + r < global_rows ? out_hi + r : global_rows;
-    if (out_hi > out_lo && (src_row0 > need_lo || src_row0 + src_rows < need_hi || src_row0 < 0 ||
-                            src_row0 + src_rows > global_rows))
+    const bool has1 = out_hi > out_lo, has2 = out_hi2 > out_lo2;
+    if (has1 && has2 && out_lo < out_hi2 && out_lo2 < out_hi)
+        return fail(SC_INVALID_ARGUMENT, "output segments overlap");
+    if (!has1 && !has2) return SC_OK;
+    const int lo_all = has1 && has2 ? (out_lo < out_lo2 ? out_lo : out_lo2) : (has1 ? out_lo : out_lo2);
+    const int hi_all = has1 && has2 ? (out_hi > out_hi2 ? out_hi : out_hi2) : (has1 ? out_hi : out_hi2);
+    const int need_lo = lo_all - r > 0 ? lo_all - r : 0;
+    const int need_hi = hi_all + r < global_rows ? hi_all + r : global_rows;
+    if (src_row0 > need_lo || src_row0 + src_rows < need_hi || src_row0 < 0 || src_row0 + src_rows > global_rows)
         return fail(SC_INVALID_ARGUMENT, "source band does not cover the output rows plus halo");
-    if (dst_row0 > out_lo) return fail(SC_INVALID_ARGUMENT, "destination band starts after the output rows");
+    if (dst_row0 > lo_all) return fail(SC_INVALID_ARGUMENT, "destination band starts after the output rows");
     SC_TRY(check_strides(nplanes, src_rows, cols, src_plane_stride, src_row_stride, "src"));
-    SC_TRY(check_strides(nplanes, out_hi - dst_row0, cols, dst_plane_stride, dst_row_stride, "dst"));
+    SC_TRY(check_strides(nplanes, hi_all - dst_row0, cols, dst_plane_stride, dst_row_stride, "dst"));
     SC_TRY(prepare(src));
     SC_TRY(prepare(dst));
     if (overlaps(src, extent_bytes(nplanes, src_rows, cols, src_plane_stride, src_row_stride), dst,
-                 extent_bytes(nplanes, out_hi - dst_row0, cols, dst_plane_stride, dst_row_stride)))
+                 extent_bytes(nplanes, hi_all - dst_row0, cols, dst_plane_stride, dst_row_stride)))
         return fail(SC_INVALID_ARGUMENT, "source and destination must be distinct buffers");
     RowsJob j{};
     j.mode = MODE_FUSED;
@@ -352,14 +364,25 @@ int sc_two_pass_band_f32(const float* src, float* dst, int nplanes, int global_r
     j.src_row0 = src_row0;
     j.src_rows = src_rows;
     j.dst_row0 = dst_row0;
-    j.out_lo = out_lo;
-    j.out_hi = out_hi;
+    j.out_lo = has1 ? out_lo : out_lo2;
+    j.out_hi = has1 ? out_hi : out_hi2;
+    j.out_lo2 = has1 ? out_lo2 : 0;
+    j.out_hi2 = has1 ? out_hi2 : 0;
     j.hrow_lo = (flags & SC_EXTENDED) ? 0 : r;
     j.hrow_hi = (flags & SC_EXTENDED) ? global_rows : global_rows - r;
     j.flags = flags;
     j.width = width;
     j.taps = taps;
     return launch_rows(j, static_cast<cudaStream_t>(stream));
+}
+
+int sc_two_pass_band_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
+                         int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                         int64_t dst_row_stride, int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
+                         const float* taps, int width, int flags, void* stream) {
+    return sc_two_pass_band2_f32(src, dst, nplanes, global_rows, cols, src_plane_stride, dst_plane_stride,
+                                 src_row_stride, dst_row_stride, src_row0, src_rows, dst_row0, out_lo, out_hi, 0, 0,
+                                 taps, width, flags, stream);
 }
 
 int sc_two_pass_fused_f32(const float* src, float* dst, int nplanes, int rows, int cols, int64_t src_plane_stride,

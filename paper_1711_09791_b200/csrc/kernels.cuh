@@ -60,6 +60,8 @@ struct Params {
     int src_row0, src_rows;  // src holds global rows [src_row0, src_row0 + src_rows)
     int dst_row0;            // dst row 0 is global row dst_row0
     int out_lo, out_hi;      // output rows produced (global)
+    int out_lo2, out_hi2;    // optional second output segment (empty if lo2 >= hi2)
+    int nitems0;             // items of the first segment; the rest belong to the second
     int hrow_lo, hrow_hi;    // rows where the row pass is live (else H0 = 0 / zero fill)
     int flags;
     int tw;                  // strip width = 4 * consumer threads
@@ -183,14 +185,20 @@ struct Item {
 template <int MODE, int RAD>
 __device__ __forceinline__ Item decode_item(const Params& p, int item) {
     const int units = p.nplanes * p.nstrips;
+    int seg_lo = p.out_lo, seg_hi = p.out_hi;
+    if (item >= p.nitems0) {
+        item -= p.nitems0;
+        seg_lo = p.out_lo2;
+        seg_hi = p.out_hi2;
+    }
     const int band = item / units;
     const int rem = item - band * units;
     Item it;
     it.plane = rem / p.nstrips;
     const int strip = rem - it.plane * p.nstrips;
     it.x0 = strip * p.tw;
-    it.ylo = p.out_lo + band * p.band_h;
-    it.yhi = min(it.ylo + p.band_h, p.out_hi);
+    it.ylo = seg_lo + band * p.band_h;
+    it.yhi = min(it.ylo + p.band_h, seg_hi);
     if (MODE == MODE_HPASS) {
         it.in_lo = it.ylo;
         it.in_hi = it.yhi;

@@ -35,6 +35,7 @@ struct RowsJob {
     int nplanes, R, C;
     int src_row0, src_rows, dst_row0;
     int out_lo, out_hi, hrow_lo, hrow_hi;
+    int out_lo2 = 0, out_hi2 = 0;  // optional second output segment
     int flags;
     int width;
     const float* taps;   // width floats (host)

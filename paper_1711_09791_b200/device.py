@@ -94,21 +94,23 @@ def two_pass(src: torch.Tensor, taps, out: torch.Tensor | None = None, *, extend
 
 
 def two_pass_band(src: torch.Tensor, taps, out: torch.Tensor, *, global_rows: int, src_row0: int,
-                  dst_row0: int, out_lo: int, out_hi: int, extended: bool = False) -> torch.Tensor:
+                  dst_row0: int, out_lo: int, out_hi: int, extended: bool = False, out_lo2: int = 0,
+                  out_hi2: int = 0) -> torch.Tensor:
     """Row band of the fused two-pass (multi-GPU partitioner): src holds global rows
-    [src_row0, src_row0 + src.shape[-2]), out row 0 is global row dst_row0."""
+    [src_row0, src_row0 + src.shape[-2]), out row 0 is global row dst_row0. An
+    optional second segment [out_lo2, out_hi2) runs in the same launch."""
     w = _taps(taps)
     n, Rs, C, sps, srs = _planes(src, "src")
     n2, Rd, C2, dps, drs = _planes(out, "out")
     if n2 != n or C2 != C:
         raise InvalidArgumentError("band source and destination plane counts / widths differ")
-    if out_hi - dst_row0 > Rd:
+    if max(out_hi, out_hi2) - dst_row0 > Rd:
         raise InvalidArgumentError("destination band too short for the output rows")
     flags = _lib.SC_EXTENDED if extended else 0
     L = _lib.load()
-    _lib.check(L.sc_two_pass_band_f32(src.data_ptr(), out.data_ptr(), n, global_rows, C, sps, dps, srs, drs,
-                                      src_row0, Rs, dst_row0, out_lo, out_hi, _fp(w), w.size, flags,
-                                      _stream(src)))
+    _lib.check(L.sc_two_pass_band2_f32(src.data_ptr(), out.data_ptr(), n, global_rows, C, sps, dps, srs, drs,
+                                       src_row0, Rs, dst_row0, out_lo, out_hi, out_lo2, out_hi2, _fp(w), w.size,
+                                       flags, _stream(src)))
     return out
 
 

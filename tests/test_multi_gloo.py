@@ -40,6 +40,17 @@ def _worker(rank, world, port, R, C, P, taps, extended, overlap, q):
         band_two_pass(local, out, band, w, extended=extended, band_fn=orc.two_pass_band, overlap=overlap)
         want = orc.two_pass(full, w, extended=extended)[:, band.lo:band.hi]
         ok = np.array_equal(out.numpy().view(np.uint32), want.view(np.uint32))
+        # a prepared op list is reused every step (BandStepper): exchange twice more
+        from paper_1711_09791_b200.multi import halo_ops
+
+        ops = halo_ops(local, band)
+        for _ in range(2):
+            local[:, : band.owned.start] = float("nan")
+            local[:, band.owned.stop :] = float("nan")
+            if ops:
+                for wk in dist.batch_isend_irecv(ops):
+                    wk.wait()
+            ok = ok and np.array_equal(local.numpy(), full[:, band.in_lo : band.in_hi])
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
