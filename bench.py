@@ -211,7 +211,7 @@ def host_chunk_bytes(rows, cols, planes, r, band_lo, band_hi, in_lo, in_hi):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))

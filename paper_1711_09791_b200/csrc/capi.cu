@@ -176,10 +176,6 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.src_row0 = j.src_row0;
     p.src_rows = j.src_rows;
     p.dst_row0 = j.dst_row0;
-    p.out_lo = j.out_lo;
-    p.out_hi = j.out_hi;
-    p.out_lo2 = seg2 ? j.out_lo2 : 0;
-    p.out_hi2 = seg2 ? j.out_hi2 : 0;
     p.hrow_lo = j.hrow_lo;
     p.hrow_hi = j.hrow_hi;
     p.flags = j.flags;
@@ -208,9 +204,10 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     } else {
         nt = choose_nt(j.C);
         p.tw = COLS_PER_THREAD * nt;
-        ns = env_int("SC_NS", 4);
-        if (ns < 3) ns = 3;
-        if (ns > 16) ns = 16;
+        ns = env_int("SC_NS", 16 / SROWS);
+        const int lags = (rad + SROWS - 1) / SROWS > 0 ? (rad + SROWS - 1) / SROWS : 1;
+        if (ns < lags + 2) ns = lags + 2;
+        if (ns > 32) ns = 32;
         threads = 32 + nt;
         smem = (size_t)((2 * ns * 8 + ns * 4 + 127) / 128) * 128 + (size_t)ns * SROWS * (p.tw + 2 * HALO) * 4;
     }
@@ -229,22 +226,58 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     // bands cost nothing in balance; they only re-read a 2r-row halo (mostly
     // from L2, since neighbouring bands run concurrently). ~64 rows measured
     // best on B200 at 16384^2 (tools/sweep.py); keep >= ~2 items per worker.
-    const int rows0 = j.out_hi > j.out_lo ? j.out_hi - j.out_lo : 0;
-    const int rows1 = seg2 ? j.out_hi2 - j.out_lo2 : 0;
-    const int rows_out = rows0 + rows1;
+    // Work split ("guided" schedule). Items are claimed from an atomic ticket in
+    // order, so the tail of a launch is what load balance depends on, while every
+    // item re-reads a 2r-row halo (from DRAM: an item runs ~100 us, long enough
+    // for the neighbouring band's rows to leave L2). A single output range is
+    // therefore cut into a head of tall bands (halo overhead 4/128) and a tail of
+    // short bands sized to ~2 waves of workers; explicit two-segment jobs (the
+    // band boundary strips) use short bands throughout.
+    int lo1 = j.out_lo, hi1 = j.out_hi, lo2 = seg2 ? j.out_lo2 : 0, hi2 = seg2 ? j.out_hi2 : 0;
+    if (hi1 <= lo1) { lo1 = lo2; hi1 = hi2; lo2 = hi2 = 0; }
     const long long units = (long long)j.nplanes * p.nstrips;
-    int band_h = env_int("SC_BAND_H", 0);
-    if (band_h <= 0) {
-        band_h = 64;
-        while (band_h > 8 && units * ((rows_out + band_h - 1) / band_h) < 2 * G) band_h /= 2;
-        if (band_h > rows_out) band_h = rows_out;
+    int bh_tall = env_int("SC_BAND_H", 128);
+    int bh_short = env_int("SC_BAND_H2", 32);
+    if (bh_tall < 1) bh_tall = 1;
+    if (bh_short < 1) bh_short = 1;
+    int h1, h2;
+    if (hi2 > lo2) {
+        h1 = h2 = bh_short;
+    } else {
+        const int rows = hi1 - lo1;
+        long long tail_rows = ((2 * G + units - 1) / units) * (long long)bh_short;
+        if (tail_rows >= rows || bh_tall <= bh_short) {
+            // small job: short bands only, shrunk until every worker has work
+            h1 = bh_short;
+            while (h1 > 4 && units * ((rows + h1 - 1) / h1) < 2 * G) h1 /= 2;
+            h2 = h1;
+        } else {
+            const int head = (int)(((rows - tail_rows) / bh_tall) * bh_tall);
+            if (head <= 0) {
+                h1 = h2 = bh_short;
+            } else {
+                lo2 = lo1 + head;
+                hi2 = hi1;
+                hi1 = lo2;
+                h1 = bh_tall;
+                h2 = bh_short;
+            }
+        }
     }
-    p.band_h = band_h;
-    const long long nitems0 = units * ((rows0 + band_h - 1) / band_h);
-    const long long nitems = nitems0 + units * ((rows1 + band_h - 1) / band_h);
+    if (h1 > hi1 - lo1 && hi1 > lo1) h1 = hi1 - lo1;
+    if (hi2 > lo2 && h2 > hi2 - lo2) h2 = hi2 - lo2;
+    p.out_lo = lo1;
+    p.out_hi = hi1;
+    p.out_lo2 = lo2;
+    p.out_hi2 = hi2;
+    p.band_h = h1 > 0 ? h1 : 1;
+    p.band_h2 = h2 > 0 ? h2 : 1;
+    const long long nitems0 = hi1 > lo1 ? units * ((hi1 - lo1 + p.band_h - 1) / p.band_h) : 0;
+    const long long nitems = nitems0 + (hi2 > lo2 ? units * ((hi2 - lo2 + p.band_h2 - 1) / p.band_h2) : 0);
     if (nitems > 0x7fffffffLL) return fail(SC_INVALID_ARGUMENT, "too many work items");
     p.nitems = (int)nitems;
     p.nitems0 = (int)nitems0;
+    const int band_h = p.band_h;
     const long long ctas = direct ? (nitems + DWARPS - 1) / DWARPS : nitems;
     const int grid = (int)(ctas < (long long)di.sms * occ ? ctas : (long long)di.sms * occ);
     p.work = work_slot(dev);
@@ -255,8 +288,9 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     count_launch();
     if (env_int("SC_DEBUG_PLAN", 0))
-        std::fprintf(stderr, "[sc] mode=%d rad=%d aligned=%d nt=%d tw=%d strips=%d ns=%d band_h=%d items=%d grid=%d occ=%d smem=%zu\n",
-                     j.mode, rad, (int)aligned, nt, p.tw, p.nstrips, ns, band_h, p.nitems, grid, occ, smem);
+        std::fprintf(stderr, "[sc] mode=%d rad=%d aligned=%d nt=%d tw=%d strips=%d ns=%d seg1=[%d,%d)/%d seg2=[%d,%d)/%d items=%d grid=%d occ=%d smem=%zu\n",
+                     j.mode, rad, (int)aligned, nt, p.tw, p.nstrips, ns, p.out_lo, p.out_hi, band_h, p.out_lo2, p.out_hi2,
+                     p.band_h2, p.nitems, grid, occ, smem);
     return SC_OK;
 }
 

@@ -66,6 +66,7 @@ struct Params {
     int flags;
     int tw;                  // strip width = 4 * consumer threads
     int nstrips, band_h, nitems;
+    int band_h2;             // band height of the second segment
     int ns;                  // smem stages (SROWS rows each)
     float one;               // 1.0f, passed at run time (see mad2)
     int* work;               // [next item, finished CTAs]: dynamic scheduling ticket pair (zero at launch)
@@ -175,7 +176,10 @@ __device__ __forceinline__ void st4(float* p, const F4& a, bool streaming = fals
 #ifndef SC_F2
 #define SC_F2 1
 #endif
-constexpr int SROWS = 4;
+#ifndef SC_SROWS
+#define SC_SROWS 4
+#endif
+constexpr int SROWS = SC_SROWS;
 constexpr int GROUPS = SC_GROUPS;
 
 struct Item {
@@ -185,11 +189,12 @@ struct Item {
 template <int MODE, int RAD>
 __device__ __forceinline__ Item decode_item(const Params& p, int item) {
     const int units = p.nplanes * p.nstrips;
-    int seg_lo = p.out_lo, seg_hi = p.out_hi;
+    int seg_lo = p.out_lo, seg_hi = p.out_hi, bh = p.band_h;
     if (item >= p.nitems0) {
         item -= p.nitems0;
         seg_lo = p.out_lo2;
         seg_hi = p.out_hi2;
+        bh = p.band_h2;
     }
     const int band = item / units;
     const int rem = item - band * units;
@@ -197,8 +202,8 @@ __device__ __forceinline__ Item decode_item(const Params& p, int item) {
     it.plane = rem / p.nstrips;
     const int strip = rem - it.plane * p.nstrips;
     it.x0 = strip * p.tw;
-    it.ylo = seg_lo + band * p.band_h;
-    it.yhi = min(it.ylo + p.band_h, seg_hi);
+    it.ylo = seg_lo + band * bh;
+    it.yhi = min(it.ylo + bh, seg_hi);
     if (MODE == MODE_HPASS) {
         it.in_lo = it.ylo;
         it.in_hi = it.yhi;
@@ -522,9 +527,8 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 
     for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
         if (r0 != it.in_lo) mbar_wait(&full[slot], phase);  // the item's first stage was waited by the caller
-        const int prev = (slot == 0) ? NS - 1 : slot - 1;
+        // stages are contiguous in smem: the ring is one circular buffer of NS*SROWS rows
         const float* sstage = ring + slot * SROWS * SW + 4 * ct;
-        const float* sprev = ring + prev * SROWS * SW + 4 * ct;
 #pragma unroll
         for (int k = 0; k < SROWS; ++k) {
             const int yi = r0 + k;
@@ -578,8 +582,9 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                         } else {
                             F4 ringv;
                             if (ring_copy) {
-                                const float* rrow =
-                                    (k >= RAD) ? sstage + (k - RAD) * SW : sprev + (k - RAD + SROWS) * SW;
+                                int rr = slot * SROWS + k - RAD;  // ring row of input row yo
+                                if (rr < 0) rr += NS * SROWS;
+                                const float* rrow = ring + rr * SW + 4 * ct;
                                 ringv = ld4(rrow + g * tw2 + 4);
                             } else {
 #pragma unroll
@@ -596,10 +601,14 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                 if (emit) dcur += p.dst_row_stride;
             }
         }
-        // this stage is done; release the previous one (kept for the RAD-row lag)
-        if (gs >= 1) {
+        // this stage is done; release the one LAGS stages back (rows up to RAD back
+        // are still read for the ring columns)
+        constexpr int LAGS = (RAD + SROWS - 1) / SROWS > 0 ? (RAD + SROWS - 1) / SROWS : 1;
+        if (gs >= LAGS) {
+            int rel = slot - LAGS;
+            if (rel < 0) rel += NS;
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[prev]);
+            if (lane == 0) mbar_arrive(&empty[rel]);
         }
         if (++slot == NS) { slot = 0; phase ^= 1u; }
     }
