@@ -118,6 +118,21 @@ int sc_copy_region_f32(const float *src, float *dst, int nplanes, int rows, int 
 int sc_fill_synthetic_f32(float *dst, int64_t count, uint64_t seed, uint64_t offset, int kind,
                           void *stream);
 
+/* The PPM payload either side of the path (S/ppm.py): interleaved u8 HWC rows
+ * (3 bytes per pixel, R,G,B = planes 0,1,2; row strides in BYTES).
+ * sc_two_pass_u8hwc: read_ppm -> two-pass -> write_ppm fused, i.e. the bytes the
+ * reference writes after convolve_image(TWO_PASS) on read_ppm(src)
+ * (S/ppm.py:72-73, S/executors.py:308-326, S/ppm.py:87-89: rint half-even,
+ * clip 0..255). Needs cols % 16 == 0 and 16-B aligned src rows, 4-B aligned dst. */
+int sc_two_pass_u8hwc(const uint8_t *src, uint8_t *dst, int rows, int cols, int64_t src_row_stride,
+                      int64_t dst_row_stride, const float *taps, int width, int flags, void *stream);
+/* u8 HWC -> 3 float32 planes (read_ppm_bytes, S/ppm.py:72-73). */
+int sc_hwc_u8_to_planes_f32(const uint8_t *src, float *dst, int rows, int cols, int64_t src_row_stride,
+                            int64_t dst_plane_stride, int64_t dst_row_stride, void *stream);
+/* 3 float32 planes -> u8 HWC with clip(rint(x), 0, 255) (write_ppm_bytes, S/ppm.py:87-89). */
+int sc_planes_f32_to_hwc_u8(const float *src, uint8_t *dst, int rows, int cols, int64_t src_plane_stride,
+                            int64_t src_row_stride, int64_t dst_row_stride, void *stream);
+
 /* End-to-end two-pass on HOST planes (the reference's Image: one pointer per
  * C-contiguous plane): streams row chunks H2D -> fused kernel -> D2H on three
  * CUDA streams with double/triple buffering, on `device`. In-place

@@ -295,6 +295,64 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
 }
 
 // --------------------------------------------------------------------------
+// Fused read_ppm -> two-pass -> write_ppm on interleaved u8 (kern_u8.cu)
+
+int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long drs, int R, int C, const float* taps,
+                   int width, int flags, cudaStream_t s) {
+    const int rad = width / 2;
+    const void* kern = kernel_u8(rad);
+    if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(width));
+    U8Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.src = src;
+    p.dst = dst;
+    p.srs = srs;
+    p.drs = drs;
+    p.R = R;
+    p.C = C;
+    p.hrow_lo = (flags & SC_EXTENDED) ? 0 : rad;
+    p.hrow_hi = (flags & SC_EXTENDED) ? R : R - rad;
+    p.flags = flags;
+    p.one = 1.0f;
+    for (int i = 0; i < width; ++i) p.w[i] = taps[i];
+    // 4 columns per consumer thread; strips of TW = 4*nt columns, nt minimising padding
+    static const int cand[] = {128, 96, 64, 160, 192, 256, 32};
+    int nt = 128;
+    long long best = -1;
+    for (int c : cand) {
+        const long long tw = 4LL * c, waste = ((C + tw - 1) / tw) * tw - C;
+        if (best < 0 || waste < best) { best = waste; nt = c; }
+    }
+    p.tw = 4 * nt;
+    p.nstrips = (C + p.tw - 1) / p.tw;
+    int ns = env_int("SC_NS", 4);
+    if (ns < 3) ns = 3;
+    if (ns > 32) ns = 32;
+    p.ns = ns;
+    const int threads = 32 + nt;
+    const size_t smem = (size_t)((2 * ns * 8 + ns * 4 + 127) / 128) * 128 + (size_t)ns * 4 * 3 * (p.tw + 32);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const DevInfo di = dev_info(dev);
+    const int occ = occupancy(kern, threads, smem);
+    const long long G = (long long)di.sms * occ;
+    int band_h = env_int("SC_BAND_H", 64);
+    while (band_h > 8 && (long long)p.nstrips * ((R + band_h - 1) / band_h) < 2 * G) band_h /= 2;
+    if (band_h > R) band_h = R;
+    p.band_h = band_h;
+    const long long nitems = (long long)p.nstrips * ((R + band_h - 1) / band_h);
+    p.nitems = (int)nitems;
+    const int grid = (int)(nitems < G ? nitems : G);
+    p.work = work_slot(dev);
+    if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
+    void* args[] = {&p};
+    cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    count_launch();
+    return SC_OK;
+}
+
+// --------------------------------------------------------------------------
 // Validation helpers
 
 static int check_width(int width) {

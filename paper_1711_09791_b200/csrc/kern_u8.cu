@@ -1,0 +1,353 @@
+// kern_u8.cu -- the PPM data format either side of the path.
+//
+// The reference reads a binary P6 file into 3 float32 planes (u8 HWC -> planes,
+// S/ppm.py:72-73), convolves, and writes it back with round-half-even + clip
+// (S/ppm.py:87-89). Here:
+//   * hwc_to_planes_kernel / planes_to_hwc_kernel: the two conversions alone;
+//   * sepconv_u8_kernel: read_ppm -> two-pass -> write_ppm FUSED in one pass over
+//     the interleaved bytes: 3 B/pixel in + 3 B/pixel out instead of 24 B/pixel,
+//     with the very same float32 arithmetic (bit-identical output bytes).
+// The fused kernel reuses the row-streaming design of kernels.cuh: a TMA
+// producer warp streams 3*(TW+32) bytes per row into a shared-memory ring,
+// consumer threads own 4 columns x 3 planes and fold the column pass through a
+// register shift register.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace sc {
+
+// float(b) for a byte via the 2^23 magic number: exact, 1 PRMT + 1 FADD.
+__device__ __forceinline__ float u8f(uint32_t word, int byte) {
+    const uint32_t bits = __byte_perm(word, 0x4B000000u, 0x7650 + byte);  // 0x4B0000bb
+    return __fsub_rn(__uint_as_float(bits), 8388608.0f);
+}
+
+// clip(rint(x), 0, 255) as a byte (S/ppm.py:88): clamp first (equivalent at
+// integer bounds), then round-half-even via 1.5*2^23.
+__device__ __forceinline__ uint32_t f2u8(float x) {
+    const float c = fminf(fmaxf(x, 0.0f), 255.0f);
+    return __float_as_uint(__fadd_rn(c, 12582912.0f)) & 0xFFu;
+}
+
+template <int RAD>
+__global__ void __launch_bounds__(32 + 256, 1) sepconv_u8_kernel(const __grid_constant__ U8Params p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
+    const int NS = p.ns;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* empty = full + NS;
+    int* sitem = reinterpret_cast<int*>(empty + NS);
+    uint8_t* ring = smem_raw + ((2 * NS * 8 + NS * 4 + 127) / 128) * 128;
+    const int SWB = 3 * (p.tw + 2 * U8_HALO);  // bytes per staged row
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncw = (blockDim.x >> 5) - 1;
+    const int units = p.nstrips;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&full[i], 1u);
+            mbar_init(&empty[i], (uint32_t)ncw);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    auto decode = [&](int item, int& x0, int& ylo, int& yhi, int& in_lo, int& in_hi) {
+        const int band = item / units;
+        const int strip = item - band * units;
+        x0 = strip * p.tw;
+        ylo = band * p.band_h;
+        yhi = min(ylo + p.band_h, p.R);
+        in_lo = max(ylo - RAD, 0);
+        in_hi = min(yhi + RAD, p.R);
+    };
+
+    if (warp == 0) {
+        if (lane != 0) return;
+        const uint64_t pol = policy_evict_normal();
+        int slot = 0, gs = 0;
+        uint32_t phase = 0;
+        for (;;) {
+            const int item = atomicAdd(&p.work[0], 1);
+            if (item >= p.nitems) {
+                if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
+                sitem[slot] = -1;
+                mbar_arrive_expect_tx(&full[slot], 0u);
+                __threadfence();
+                if (atomicAdd(&p.work[1], 1) == (int)gridDim.x - 1) {
+                    atomicExch(&p.work[0], 0);
+                    atomicExch(&p.work[1], 0);
+                }
+                return;
+            }
+            int x0, ylo, yhi, in_lo, in_hi;
+            decode(item, x0, ylo, yhi, in_lo, in_hi);
+            const int cx0 = max(x0 - U8_HALO, 0);
+            const int cx1 = min(x0 + p.tw + U8_HALO, p.C);
+            const uint32_t bytes = 3u * (uint32_t)(cx1 - cx0);
+            const int soff = 3 * (cx0 - (x0 - U8_HALO));
+            for (int r0 = in_lo; r0 < in_hi; r0 += U8_SROWS, ++gs) {
+                if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
+                const int nrows = min(U8_SROWS, in_hi - r0);
+                sitem[slot] = item;
+                mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
+                for (int k = 0; k < nrows; ++k)
+                    bulk_g2s(ring + (slot * U8_SROWS + k) * SWB + soff, p.src + (long long)(r0 + k) * p.srs + 3LL * cx0,
+                             bytes, &full[slot], pol);
+                if (++slot == NS) { slot = 0; phase ^= 1u; }
+            }
+        }
+    }
+
+    // ---- consumers: 4 columns x 3 planes per thread
+    const int ct = threadIdx.x - 32;
+    const int R = p.R, C = p.C;
+    const float2 one2 = make_float2(p.one, p.one);
+    const bool ring_copy = !(p.flags & F_NO_RING);
+    int slot = 0, gs = 0;
+    uint32_t phase = 0;
+    for (;;) {
+        mbar_wait(&full[slot], phase);
+        const int item = sitem[slot];
+        if (item < 0) break;
+        int x0, ylo, yhi, in_lo, in_hi;
+        decode(item, x0, ylo, yhi, in_lo, in_hi);
+        const int x4 = x0 + 4 * ct;
+        const bool fast = x4 >= RAD && x4 + 4 <= C - RAD;
+        const int emit_lo = max(max(ylo, RAD), in_lo + RAD);
+        const int emit_hi = min(yhi, R - RAD);
+        F4 acc[3][NACC];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+            for (int j = 0; j < NACC; ++j)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[q][j].v[c] = 0.0f;
+
+        for (int r0 = in_lo; r0 < in_hi; r0 += U8_SROWS, ++gs) {
+            if (r0 != in_lo) mbar_wait(&full[slot], phase);
+#pragma unroll
+            for (int k = 0; k < U8_SROWS; ++k) {
+                const int yi = r0 + k;
+                if (yi >= in_hi) break;
+                // 12 columns x 3 planes = 36 bytes at byte 12*ct + 36 of the staged row
+                const uint8_t* srow = ring + (slot * U8_SROWS + k) * SWB + 12 * ct + 3 * (U8_HALO - 4);
+                uint32_t wd[9];
+#pragma unroll
+                for (int i = 0; i < 9; ++i) wd[i] = reinterpret_cast<const uint32_t*>(srow)[i];
+                const bool live = yi >= p.hrow_lo && yi < p.hrow_hi;
+                const int yo = yi - RAD;
+                const bool emit = yo >= emit_lo && yo < emit_hi;
+                F4 outv[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    float win[12];
+#pragma unroll
+                    for (int c = 0; c < 12; ++c) {
+                        const int b = 3 * c + q;  // byte index in the 36-byte window
+                        win[c] = u8f(wd[b >> 2], b & 3);
+                    }
+                    F4 v;
+                    if (live) {
+                        v = row_pass<RAD>(win, p.w, p.one);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) v.v[c] = 0.0f;
+                    }
+                    outv[q] = col_fold<RAD, NACC>(acc[q], v, p.w, p.one);
+                }
+                (void)one2;
+                if (emit && x4 < C) {
+                    // ring columns keep the input byte of row yo (pixel ring == input)
+                    uint32_t ob[12];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int q = 0; q < 3; ++q) ob[3 * c + q] = f2u8(outv[q].v[c]);
+                    if (!fast) {
+                        int rr = slot * U8_SROWS + k - RAD;
+                        if (rr < 0) rr += NS * U8_SROWS;
+                        const uint8_t* yrow = ring + rr * SWB + 12 * ct + 3 * U8_HALO;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const int col = x4 + c;
+                            if (col < RAD || col >= C - RAD) {
+#pragma unroll
+                                for (int q = 0; q < 3; ++q) ob[3 * c + q] = ring_copy ? yrow[3 * c + q] : 0xFFFFFFFFu;
+                            }
+                        }
+                    }
+                    uint8_t* drow = p.dst + (long long)yo * p.drs + 3LL * x4;
+                    if (fast || (ring_copy && x4 + 4 <= C)) {
+                        uint32_t* d32 = reinterpret_cast<uint32_t*>(drow);
+#pragma unroll
+                        for (int i = 0; i < 3; ++i)
+                            d32[i] = ob[4 * i] | (ob[4 * i + 1] << 8) | (ob[4 * i + 2] << 16) | (ob[4 * i + 3] << 24);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const int col = x4 + c;
+                            if (col >= C) break;
+                            if (col >= RAD && col < C - RAD)
+#pragma unroll
+                                for (int q = 0; q < 3; ++q) drow[3 * c + q] = (uint8_t)ob[3 * c + q];
+                        }
+                    }
+                }
+                if (ring_copy && yi >= ylo && yi < yhi && (yi < RAD || yi >= R - RAD) && x4 < C) {
+                    // ring rows: the input bytes unchanged
+                    uint8_t* drow = p.dst + (long long)yi * p.drs + 3LL * x4;
+                    const uint8_t* irow = ring + (slot * U8_SROWS + k) * SWB + 12 * ct + 3 * U8_HALO;
+                    const int nb = 3 * min(4, C - x4);
+                    for (int b = 0; b < nb; ++b) drow[b] = irow[b];
+                }
+            }
+            constexpr int LAGS = (RAD + U8_SROWS - 1) / U8_SROWS > 0 ? (RAD + U8_SROWS - 1) / U8_SROWS : 1;
+            if (gs >= LAGS) {
+                int rel = slot - LAGS;
+                if (rel < 0) rel += NS;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[rel]);
+            }
+            if (++slot == NS) { slot = 0; phase ^= 1u; }
+        }
+    }
+}
+
+// u8 HWC -> float32 planes (S/ppm.py:72-73), one thread per pixel.
+__global__ void hwc_to_planes_kernel(const uint8_t* __restrict__ src, float* __restrict__ dst, long long srs,
+                                     long long dps, long long drs, int R, int C) {
+    const long long total = (long long)R * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / C), x = (int)(i - (long long)y * C);
+        const uint8_t* s = src + y * srs + 3LL * x;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) dst[q * dps + y * drs + x] = (float)s[q];
+    }
+}
+
+// float32 planes -> u8 HWC with clip(rint(x), 0, 255) (S/ppm.py:87-89).
+__global__ void planes_to_hwc_kernel(const float* __restrict__ src, uint8_t* __restrict__ dst, long long sps,
+                                     long long srs, long long drs, int R, int C) {
+    const long long total = (long long)R * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / C), x = (int)(i - (long long)y * C);
+        uint8_t* d = dst + y * drs + 3LL * x;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) d[q] = (uint8_t)f2u8(src[q * sps + y * srs + x]);
+    }
+}
+
+const void* kernel_u8(int rad) {
+    switch (rad) {
+        case 0: return (const void*)sepconv_u8_kernel<0>;
+        case 1: return (const void*)sepconv_u8_kernel<1>;
+        case 2: return (const void*)sepconv_u8_kernel<2>;
+        case 3: return (const void*)sepconv_u8_kernel<3>;
+        case 4: return (const void*)sepconv_u8_kernel<4>;
+        default: return nullptr;
+    }
+}
+
+static int grid_cap(long long total, int threads) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long b = (total + threads - 1) / threads;
+    if (b > (long long)sms * 8) b = (long long)sms * 8;
+    return b < 1 ? 1 : (int)b;
+}
+
+cudaError_t launch_hwc_to_planes(const uint8_t* src, float* dst, long long srs, long long dps, long long drs, int R,
+                                 int C, cudaStream_t s) {
+    hwc_to_planes_kernel<<<grid_cap((long long)R * C, 256), 256, 0, s>>>(src, dst, srs, dps, drs, R, C);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_planes_to_hwc(const float* src, uint8_t* dst, long long sps, long long srs, long long drs, int R,
+                                 int C, cudaStream_t s) {
+    planes_to_hwc_kernel<<<grid_cap((long long)R * C, 256), 256, 0, s>>>(src, dst, sps, srs, drs, R, C);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace sc
+
+// ---------------------------------------------------------------------------
+// C ABI (declared in include/sepconv_b200.h)
+
+namespace sc {
+int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long drs, int R, int C, const float* taps,
+                   int width, int flags, cudaStream_t s);
+}
+
+using namespace sc;
+
+static int u8_fail(int code, const char* msg) {
+    set_error(msg);
+    return code;
+}
+
+static bool dev_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return false;
+    cudaSetDevice(a.device);
+    return true;
+}
+
+extern "C" int sc_two_pass_u8hwc(const uint8_t* src, uint8_t* dst, int rows, int cols, int64_t src_row_stride,
+                                 int64_t dst_row_stride, const float* taps, int width, int flags, void* stream) {
+    set_error("");
+    if (!src || !dst || !taps || rows < 1 || cols < 1) return u8_fail(1, "null pointer or non-positive dimension");
+    if (width < 1 || width % 2 == 0) return u8_fail(1, "kernel width must be odd and >= 1");
+    if (width > MAX_W) return u8_fail(3, "kernel width > 9 not supported");
+    if (rows < width || cols < width) return u8_fail(2, "image smaller than kernel width");
+    if (src_row_stride < 3LL * cols || dst_row_stride < 3LL * cols) return u8_fail(1, "row stride shorter than a row");
+    if (cols % 16 || src_row_stride % 16 || dst_row_stride % 16 || (reinterpret_cast<uintptr_t>(src) & 15) ||
+        (reinterpret_cast<uintptr_t>(dst) & 3))
+        return u8_fail(1, "fused u8 path needs cols % 16 == 0, 16-B aligned rows (use unpack / two_pass / pack)");
+    if (!dev_ptr(src) || !dev_ptr(dst)) return u8_fail(1, "buffer is not device memory");
+    const long long ns = (long long)(rows - 1) * src_row_stride + 3LL * cols;
+    const long long nd = (long long)(rows - 1) * dst_row_stride + 3LL * cols;
+    const char* a = reinterpret_cast<const char*>(src);
+    const char* b = reinterpret_cast<const char*>(dst);
+    if (a < b + nd && b < a + ns) return u8_fail(1, "source and destination must be distinct buffers");
+    return launch_rows_u8(src, dst, src_row_stride, dst_row_stride, rows, cols, taps, width, flags,
+                          static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sc_hwc_u8_to_planes_f32(const uint8_t* src, float* dst, int rows, int cols, int64_t src_row_stride,
+                                       int64_t dst_plane_stride, int64_t dst_row_stride, void* stream) {
+    set_error("");
+    if (!src || !dst || rows < 1 || cols < 1 || src_row_stride < 3LL * cols || dst_row_stride < cols ||
+        dst_plane_stride < (long long)rows * dst_row_stride)
+        return u8_fail(1, "bad geometry");
+    if (!dev_ptr(src) || !dev_ptr(dst)) return u8_fail(1, "buffer is not device memory");
+    cudaError_t e = launch_hwc_to_planes(src, dst, src_row_stride, dst_plane_stride, dst_row_stride, rows, cols,
+                                         static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return u8_fail(4, cudaGetErrorString(e));
+    return 0;
+}
+
+extern "C" int sc_planes_f32_to_hwc_u8(const float* src, uint8_t* dst, int rows, int cols, int64_t src_plane_stride,
+                                       int64_t src_row_stride, int64_t dst_row_stride, void* stream) {
+    set_error("");
+    if (!src || !dst || rows < 1 || cols < 1 || dst_row_stride < 3LL * cols || src_row_stride < cols ||
+        src_plane_stride < (long long)rows * src_row_stride)
+        return u8_fail(1, "bad geometry");
+    if (!dev_ptr(src) || !dev_ptr(dst)) return u8_fail(1, "buffer is not device memory");
+    cudaError_t e = launch_planes_to_hwc(src, dst, src_plane_stride, src_row_stride, dst_row_stride, rows, cols,
+                                         static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return u8_fail(4, cudaGetErrorString(e));
+    return 0;
+}

@@ -74,6 +74,23 @@ struct Params {
     float k[MAX_W * MAX_W];
 };
 
+// Interleaved-u8 (PPM payload) fused path, csrc/kern_u8.cu
+constexpr int U8_HALO = 16;   // columns either side of a strip (16*3 bytes keeps TMA 16-B aligned)
+constexpr int U8_SROWS = 4;
+
+struct U8Params {
+    const uint8_t* src;
+    uint8_t* dst;
+    long long srs, drs;  // row strides in BYTES
+    int R, C;
+    int hrow_lo, hrow_hi;
+    int flags;
+    int tw, nstrips, band_h, nitems, ns;
+    float w[MAX_W];
+    float one;
+    int* work;
+};
+
 // ---------------------------------------------------------------------------
 // PTX helpers (mbarrier + bulk copy)
 

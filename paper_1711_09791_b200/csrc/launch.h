@@ -20,6 +20,12 @@ const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);
 const void* kernel_single_direct(int rad);
 
+const void* kernel_u8(int rad);
+cudaError_t launch_hwc_to_planes(const uint8_t* src, float* dst, long long srs, long long dps, long long drs, int R,
+                                 int C, cudaStream_t s);
+cudaError_t launch_planes_to_hwc(const float* src, uint8_t* dst, long long sps, long long srs, long long drs, int R,
+                                 int C, cudaStream_t s);
+
 cudaError_t launch_copy_region(const float* src, float* dst, long long sps, long long dps, long long srs,
                                long long drs, int nplanes, int row_lo, int nrows, int col_lo, int ncols,
                                cudaStream_t s);

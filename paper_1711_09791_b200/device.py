@@ -230,3 +230,65 @@ def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring:
     L = _lib.load()
     _lib.check(L.sc_two_pass_host_f32(ctypes.cast(arr_in, ctypes.c_void_p), ctypes.cast(arr_out, ctypes.c_void_p),
                                       n, shape[0], shape[1], _fp(w), w.size, flags, int(device)))
+
+
+# ---------------------------------------------------------------------------
+# PPM payload (interleaved u8 HWC, S/ppm.py) either side of the path
+
+def _hwc(t: torch.Tensor, what: str):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.uint8:
+        raise InvalidArgumentError(f"{what} must be a CUDA uint8 tensor")
+    if t.dim() != 3 or t.shape[2] != 3 or t.stride(2) != 1 or t.stride(1) != 3:
+        raise InvalidArgumentError(f"{what} must be (rows, cols, 3) with interleaved pixels")
+    return t.shape[0], t.shape[1], t.stride(0)
+
+
+def hwc_to_planes(src: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """(R, C, 3) uint8 -> (3, R, C) float32 (read_ppm_bytes, S/ppm.py:72-73)."""
+    R, C, srs = _hwc(src, "src")
+    if out is None:
+        out = torch.empty((3, R, C), dtype=torch.float32, device=src.device)
+    n, R2, C2, ps, rs = _planes(out, "out")
+    if (n, R2, C2) != (3, R, C):
+        raise InvalidArgumentError("out must be (3, rows, cols)")
+    L = _lib.load()
+    _lib.check(L.sc_hwc_u8_to_planes_f32(src.data_ptr(), out.data_ptr(), R, C, srs, ps, rs, _stream(src)))
+    return out
+
+
+def planes_to_hwc(src: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """(3, R, C) float32 -> (R, C, 3) uint8 with clip(rint(x), 0, 255) (S/ppm.py:87-89)."""
+    n, R, C, ps, rs = _planes(src, "src")
+    if n != 3:
+        raise InvalidArgumentError(f"PPM output needs exactly 3 planes, image has {n}")
+    if out is None:
+        out = torch.empty((R, C, 3), dtype=torch.uint8, device=src.device)
+    R2, C2, drs = _hwc(out, "out")
+    if (R2, C2) != (R, C):
+        raise InvalidArgumentError("out must be (rows, cols, 3)")
+    L = _lib.load()
+    _lib.check(L.sc_planes_f32_to_hwc_u8(src.data_ptr(), out.data_ptr(), R, C, ps, rs, drs, _stream(src)))
+    return out
+
+
+def two_pass_u8hwc(src: torch.Tensor, taps, out: torch.Tensor | None = None, *,
+                   extended: bool = False) -> torch.Tensor:
+    """read_ppm -> two-pass -> write_ppm on a (R, C, 3) uint8 payload: one fused
+    kernel when cols % 16 == 0 (3 B/pixel each way); otherwise unpack, fused
+    float two-pass and pack, all on the GPU. Same output bytes either way."""
+    w = _taps(taps)
+    R, C, srs = _hwc(src, "src")
+    if out is None:
+        out = torch.empty_like(src)
+    R2, C2, drs = _hwc(out, "out")
+    if (R2, C2) != (R, C):
+        raise InvalidArgumentError("source and destination dimensions differ")
+    flags = _lib.SC_EXTENDED if extended else 0
+    L = _lib.load()
+    if C % 16 == 0 and srs % 16 == 0 and drs % 16 == 0 and src.data_ptr() % 16 == 0 and out.data_ptr() % 4 == 0:
+        _lib.check(L.sc_two_pass_u8hwc(src.data_ptr(), out.data_ptr(), R, C, srs, drs, _fp(w), w.size, flags,
+                                       _stream(src)))
+        return out
+    planes = hwc_to_planes(src)
+    conv = two_pass(planes, w, extended=extended)
+    return planes_to_hwc(conv, out)

@@ -174,6 +174,41 @@ def main():
     syn["splitmix64_smax_64"] = ref.splitmix64(2**64 - 1, 64)
     np.savez(os.path.join(OUT, "synthetic.npz"), **syn)
 
+    # 5. PPM either side of the path (S/ppm.py): read -> convolve_image(TWO_PASS) -> write
+    ppm = {}
+    rng = np.random.default_rng(4242)
+    for (R, C, tname) in ((16, 16, "gauss5"), (37, 48, "sharpen"), (64, 80, "gauss5"), (100, 160, "sigma1"),
+                          (29, 131, "sharpen"), (24, 1040, "gauss5")):
+        pix = rng.integers(0, 256, size=(R, C, 3), dtype=np.uint8)
+        pix[0, :4] = 0
+        pix[-1, -4:] = 255
+        data = f"P6\n{C} {R}\n255\n".encode() + pix.tobytes()
+        img = ref.read_ppm_bytes(data)
+        k = ref.SeparableKernel(CONFIG_TAPS[tname])
+        ref.convolve_image(img, k, ref.ConvVariant(ref.Algorithm.TWO_PASS), ref.Sequential())
+        out = ref.write_ppm_bytes(img)
+        key = f"{R}x{C}_{tname}"
+        ppm[f"in_{key}"] = np.frombuffer(data, dtype=np.uint8)
+        ppm[f"out_{key}"] = np.frombuffer(out, dtype=np.uint8)
+        ppm[f"taps_{key}"] = k.weights
+        ppm[f"planes_{key}"] = np.stack([p.data for p in ref.read_ppm_bytes(data).planes])
+    # malformed headers: the reference's error message and byte offset
+    bad = [b"P5\n2 2\n255\n" + bytes(12), b"P6x2 2\n255\n" + bytes(12), b"P6\n2 2\n255\n" + bytes(11),
+           b"P6\n2 2\n255\n" + bytes(13), b"P6\n2 2\n65535\n" + bytes(24), b"P6\n0 2\n255\n",
+           b"P6\n2 # c\n2\n255\n" + bytes(12), b"P6\n2 a\n255\n", b"P6\n2 2\n255", b"P6\n2 2\n255x" + bytes(12),
+           b"P6\n2", b"P6 2 2 255\n" + bytes(12)]
+    errs = []
+    for i, d in enumerate(bad):
+        try:
+            ref.read_ppm_bytes(d)
+            errs.append(("ok", -1))
+        except ref.PpmParseError as e:
+            errs.append((str(e), e.byte_offset))
+        ppm[f"bad_{i}"] = np.frombuffer(d, dtype=np.uint8)
+    ppm["bad_messages"] = np.array([m for m, _ in errs])
+    ppm["bad_offsets"] = np.array([o for _, o in errs])
+    np.savez(os.path.join(OUT, "ppm.npz"), **ppm)
+
     total = sum(os.path.getsize(p) for p in written)
     print(f"wrote {len(written)} plane fixtures ({total / 1e6:.2f} MB) + synthetic.npz")
 

@@ -1,0 +1,92 @@
+"""PPM payload either side of the path (S/ppm.py): header parsing on CPU against
+the reference's own errors/offsets; GPU unpack/pack and the fused
+read -> two-pass -> write kernel against bytes the reference wrote."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+
+def test_header_errors_match_reference():
+    from paper_1711_09791_b200.errors import PpmParseError
+    from paper_1711_09791_b200.ppm import parse_header
+
+    z = load_golden("ppm")
+    for i, (msg, off) in enumerate(zip(z["bad_messages"], z["bad_offsets"])):
+        data = z[f"bad_{i}"].tobytes()
+        if off < 0:
+            parse_header(data)
+            continue
+        with pytest.raises(PpmParseError) as ei:
+            parse_header(data)
+        assert str(ei.value) == str(msg) and ei.value.byte_offset == int(off), i
+
+
+def test_header_of_valid_files():
+    from paper_1711_09791_b200.ppm import parse_header
+
+    z = load_golden("ppm")
+    for key in z:
+        if key.startswith("in_"):
+            R, C = (int(v) for v in key[3:].split("_")[0].split("x"))
+            rows, cols, pos = parse_header(z[key].tobytes())
+            assert (rows, cols) == (R, C) and len(z[key]) - pos == R * C * 3
+
+
+def _cases():
+    z = load_golden("ppm")
+    return sorted(k[3:] for k in z if k.startswith("in_"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", _cases())
+def test_fused_ppm_convolution_matches_reference_bytes(key):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_09791_b200.ppm import convolve_ppm_bytes, read_ppm_bytes, write_ppm_bytes
+
+    z = load_golden("ppm")
+    data = z[f"in_{key}"].tobytes()
+    want = z[f"out_{key}"].tobytes()
+    assert convolve_ppm_bytes(data, z[f"taps_{key}"]) == want
+    img = read_ppm_bytes(data)
+    assert np.array_equal(np.stack([p.data for p in img.planes]), z[f"planes_{key}"])
+    dimg = read_ppm_bytes(data, device="cuda")
+    assert write_ppm_bytes(dimg) == data  # integer planes round-trip byte for byte
+
+
+@pytest.mark.gpu
+def test_pack_rounding_half_even_and_clip():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_09791_b200 import device as dev
+
+    vals = np.array([-3.0, -0.5, -0.0, 0.4999, 0.5, 1.5, 2.5, 2.5000002, 127.5, 128.5, 254.5, 255.49, 255.5,
+                     300.0, np.inf, -np.inf, 1e30], dtype=np.float32)
+    n = vals.size
+    planes = np.stack([vals, vals[::-1], np.roll(vals, 3)]).reshape(3, 1, n).astype(np.float32)
+    got = dev.planes_to_hwc(torch.from_numpy(planes).cuda()).cpu().numpy()
+    want = np.clip(np.rint(np.moveaxis(planes, 0, -1)), 0, 255).astype(np.uint8)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+def test_fused_u8_large_against_float_path():
+    """cfg-sized payload: the fused u8 kernel equals unpack -> fused f32 -> pack."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_09791_b200 import device as dev
+
+    R, C = 1080, 1920
+    g = torch.Generator(device="cuda").manual_seed(3)
+    src = torch.randint(0, 256, (R, C, 3), dtype=torch.uint8, device="cuda", generator=g)
+    for taps in ([1 / 16, 4 / 16, 6 / 16, 4 / 16, 1 / 16], [-1, -2, 7, -2, -1]):
+        fused = dev.two_pass_u8hwc(src, np.asarray(taps, np.float32))
+        ref = dev.planes_to_hwc(dev.two_pass(dev.hwc_to_planes(src), np.asarray(taps, np.float32)))
+        assert torch.equal(fused, ref)
