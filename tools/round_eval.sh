@@ -7,6 +7,7 @@ timeout -s KILL 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.
 timeout -s KILL 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>&1; cat gpurun_out/bench_ref.json
 for c in cfg1 cfg2 cfg3 cfg4; do timeout -s KILL 300 python tools/quick_perf.py --cfg $c --ops fused,split,single,copy 2>&1 | grep -v "^\[sc\]"; done > gpurun_out/configs.jsonl; cat gpurun_out/configs.jsonl
 CMD="python bench.py --steps 20 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+for c in cfg1 cfg2 cfg3 cfg4; do timeout -s KILL 300 python bench.py --config $c --steps 200 --e2e-steps 1 --no-cpu-baseline 2>/dev/null; done > gpurun_out/bench_configs.jsonl; cat gpurun_out/bench_configs.jsonl
 $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-python tools/prof_one.py --op fused > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:sepconv_rows -s 2 -c 1 -o gpurun_out/prof_fused_cfg5 python tools/prof_one.py --op fused > gpurun_out/ncu_full.log 2>&1
+python tools/prof_one.py --op fused > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:sepconv_rows -s 2 -c 1 -o gpurun_out/prof_fused_cfg5_r01c python tools/prof_one.py --op fused > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
