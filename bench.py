@@ -233,10 +233,16 @@ def main():
     from paper_1711_09791_b200.multi import BandStepper, band_plan, band_two_pass, frame_shard
 
     world, rank, local = dist_env()
+    backend = os.environ.get("SEPCONV_BENCH_BACKEND", "nccl")  # gloo: orchestration check on one GPU
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
         dist.barrier()  # all ranks join the communicator before the first P2P group
     w = wl.tap_vector()
     r = len(w) // 2
@@ -316,7 +322,7 @@ def main():
     launches = _lib.launch_count() - launches0
     sampler.stop()
     if world > 1:
-        t = torch.tensor([ms], device=device)
+        t = torch.tensor([ms], device=device if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = total_px / (ms / 1e3) / 1e9
@@ -403,7 +409,7 @@ def main():
             e2e_step()
         e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
         if world > 1:
-            t = torch.tensor([e_ms], device=device)
+            t = torch.tensor([e_ms], device=device if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": round(total_px / (e_ms / 1e3) / 1e9, 4), "unit": "Gpix/s", "h2d_bytes_per_step": int(h2d),

@@ -23,6 +23,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Callable
 
+import torch
+
 from .errors import InvalidArgumentError
 
 
@@ -185,10 +187,9 @@ class BandStepper:
     step is ~0.13 ms of GPU time, so host overhead per step matters.
     """
 
-    def __init__(self, local_src, local_dst, band: Band, taps, *, extended: bool = False, group=None):
+    def __init__(self, local_src, local_dst, band: Band, taps, *, extended: bool = False, group=None,
+                 host_staged: bool | None = None):
         import ctypes
-
-        import torch
 
         from . import _lib
         from . import device as dev
@@ -219,12 +220,41 @@ class BandStepper:
             self._boundary = head + (band.lo, i_lo, i_hi, band.hi) + tail
         else:
             self._boundary = head + (band.lo, band.hi, 0, 0) + tail
-        self._ops = halo_ops(local_src, band, group)
+        # Backends that cannot move CUDA tensors (gloo: used to exercise the
+        # multi-rank orchestration on one GPU / in CI) stage the halo rows
+        # through host memory; NCCL exchanges device rows directly.
+        if host_staged is None:
+            import torch.distributed as dist
+
+            host_staged = dist.is_initialized() and dist.get_backend(group) != "nccl" and local_src.is_cuda
+        self._staged = host_staged
+        if host_staged:
+            self._host = torch.empty(local_src.shape, dtype=local_src.dtype, pin_memory=True)
+            self._ops = halo_ops(self._host, band, group)
+        else:
+            self._ops = halo_ops(local_src, band, group)
 
     def _exchange(self):
         import torch.distributed as dist
 
-        return dist.batch_isend_irecv(self._ops) if self._ops else []
+        if not self._ops:
+            return []
+        if not self._staged:
+            return dist.batch_isend_irecv(self._ops)
+        b = self.band
+        o0, o1 = b.owned.start, b.owned.stop
+        top, bot = b.lo - b.in_lo, b.in_hi - b.hi
+        # owned boundary rows down, exchange on the host, halo rows back up
+        self._host[:, o0:o0 + top].copy_(self.src[:, o0:o0 + top])
+        self._host[:, o1 - bot:o1].copy_(self.src[:, o1 - bot:o1])
+        torch.cuda.current_stream().synchronize()
+        for wk in dist.batch_isend_irecv(self._ops):
+            wk.wait()
+        if top:
+            self.src[:, 0:top].copy_(self._host[:, 0:top], non_blocking=True)
+        if bot:
+            self.src[:, o1:o1 + bot].copy_(self._host[:, o1:o1 + bot], non_blocking=True)
+        return []
 
     def step(self):
         L = self._lib
