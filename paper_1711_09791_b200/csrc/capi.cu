@@ -123,26 +123,7 @@ static int* work_slot(int dev) {
 // --------------------------------------------------------------------------
 // Planner
 
-// Consumer threads per CTA: strip width TW = 4*nt; minimise padding columns.
-static constexpr int COLS_PER_THREAD = 4 * GROUPS;
-
-static int choose_nt(int C) {
-    int forced = env_int("SC_NT", 0);
-    if (forced >= 32 && forced <= 256 && forced % 32 == 0) return forced;
-    static const int cand[] = {128, 96, 64, 160, 192, 256, 32};
-    int best = 128;
-    long long best_waste = -1;
-    for (int nt : cand) {
-        const long long tw = (long long)COLS_PER_THREAD * nt;
-        const long long strips = (C + tw - 1) / tw;
-        const long long waste = strips * tw - C;
-        if (best_waste < 0 || waste < best_waste) {
-            best_waste = waste;
-            best = nt;
-        }
-    }
-    return best;
-}
+static constexpr int COLS_PER_THREAD = 4 * GROUPS;  // two 4-column groups per consumer thread
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -202,68 +183,117 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         p.tw = 128;
         threads = 32 * DWARPS;
     } else {
-        nt = choose_nt(j.C);
-        p.tw = COLS_PER_THREAD * nt;
-        ns = env_int("SC_NS", 16 / SROWS);
-        const int lags = (rad + SROWS - 1) / SROWS > 0 ? (rad + SROWS - 1) / SROWS : 1;
-        if (ns < lags + 2) ns = lags + 2;
-        if (ns > 32) ns = 32;
-        threads = 32 + nt;
-        smem = (size_t)((2 * ns * 8 + ns * 4 + 127) / 128) * 128 + (size_t)ns * SROWS * (p.tw + 2 * HALO) * 4;
+        nt = 0;
+        threads = 0;
     }
-    p.nstrips = (j.C + p.tw - 1) / p.tw;
-    p.ns = ns;
 
     int dev = 0;
     cudaGetDevice(&dev);
     const DevInfo di = dev_info(dev);
-    int occ = occupancy(kern, threads, smem);
     const int occ_cap = env_int("SC_OCC", 0);
-    if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;
-    const long long G = (long long)di.sms * occ * (direct ? DWARPS : 1);  // concurrent workers
+    const int lags = (rad + SROWS - 1) / SROWS > 0 ? (rad + SROWS - 1) / SROWS : 1;
+    int ns_req = env_int("SC_NS", 16 / SROWS);
+    if (ns_req < lags + 2) ns_req = lags + 2;
+    if (ns_req > 32) ns_req = 32;
+    auto smem_for = [&](int tw, int ns_) {
+        return (size_t)((2 * ns_ * 8 + ns_ * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * (tw + 2 * HALO) * 4;
+    };
+    auto occ_for = [&](int threads_, size_t smem_) {
+        int o = occupancy(kern, threads_, smem_);
+        if (occ_cap > 0 && o > occ_cap) o = occ_cap;
+        return o;
+    };
 
-    // Row-band height. Items are claimed dynamically (atomic ticket), so short
-    // bands cost nothing in balance; they only re-read a 2r-row halo (mostly
-    // from L2, since neighbouring bands run concurrently). ~64 rows measured
-    // best on B200 at 16384^2 (tools/sweep.py); keep >= ~2 items per worker.
-    // Work split ("guided" schedule). Items are claimed from an atomic ticket in
-    // order, so the tail of a launch is what load balance depends on, while every
-    // item re-reads a 2r-row halo (from DRAM: an item runs ~100 us, long enough
-    // for the neighbouring band's rows to leave L2). A single output range is
-    // therefore cut into a head of tall bands (halo overhead 4/128) and a tail of
-    // short bands sized to ~2 waves of workers; explicit two-segment jobs (the
-    // band boundary strips) use short bands throughout.
+    // Work split. Items are (plane, strip, row band), claimed from an atomic ticket
+    // in order, so load balance only depends on the tail of a launch; every item
+    // re-reads a 2r-row halo and every strip an 8-column halo.
+    //  * large jobs (>= ~6 items of 128 rows per CTA): 1024-column strips, a head of
+    //    128-row bands (halo 4/128) and a tail of 32-row bands sized to two waves;
+    //  * small jobs: the strip width and a uniform band height are chosen together to
+    //    give every CTA ~2 items at the least halo + padding cost (narrow strips are
+    //    cheaper than short bands: 8/TW vs 2r/bh);
+    //  * explicit two-segment jobs (a band's boundary strips) use short bands.
     int lo1 = j.out_lo, hi1 = j.out_hi, lo2 = seg2 ? j.out_lo2 : 0, hi2 = seg2 ? j.out_hi2 : 0;
     if (hi1 <= lo1) { lo1 = lo2; hi1 = hi2; lo2 = hi2 = 0; }
-    const long long units = (long long)j.nplanes * p.nstrips;
+    const int rows_total = (hi1 - lo1) + (hi2 > lo2 ? hi2 - lo2 : 0);
     int bh_tall = env_int("SC_BAND_H", 128);
     int bh_short = env_int("SC_BAND_H2", 32);
     if (bh_tall < 1) bh_tall = 1;
     if (bh_short < 1) bh_short = 1;
-    int h1, h2;
-    if (hi2 > lo2) {
-        h1 = h2 = bh_short;
+    int occ = 1, h1 = bh_short, h2 = bh_short;
+    long long G = 1;
+    if (direct) {
+        occ = occ_for(threads, 0);
+        G = (long long)di.sms * occ * DWARPS;
+        p.nstrips = (j.C + p.tw - 1) / p.tw;
+        const long long units = (long long)j.nplanes * p.nstrips;
+        h1 = 64;
+        while (h1 > 4 && units * ((rows_total + h1 - 1) / h1) < 2 * G) h1 /= 2;
+        h2 = h1;
     } else {
+        const int forced = env_int("SC_NT", 0);
+        static const int cand[] = {128, 96, 64, 160, 192, 256};
+        double best_cost = 1e30;
+        int best_head = 0;
         const int rows = hi1 - lo1;
-        long long tail_rows = ((2 * G + units - 1) / units) * (long long)bh_short;
-        if (tail_rows >= rows || bh_tall <= bh_short) {
-            // small job: short bands only, shrunk until every worker has work
-            h1 = bh_short;
-            while (h1 > 4 && units * ((rows + h1 - 1) / h1) < 2 * G) h1 /= 2;
-            h2 = h1;
-        } else {
-            const int head = (int)(((rows - tail_rows) / bh_tall) * bh_tall);
-            if (head <= 0) {
-                h1 = h2 = bh_short;
+        for (int c : cand) {
+            if (forced && c != forced) continue;
+            const int tw = COLS_PER_THREAD * c;
+            const int strips = (j.C + tw - 1) / tw;
+            const long long units = (long long)j.nplanes * strips;
+            const size_t sm = smem_for(tw, ns_req);
+            const int o = occ_for(32 + c, sm);
+            const long long g = (long long)di.sms * o;
+            // padding columns + the 8-column halo of every strip
+            double cost = (double)(strips * tw + 2 * HALO * strips) / j.C;
+            int head = 0, bh = bh_short;
+            if (seg2) {
+                cost *= (double)(bh_short + 2 * rad) / bh_short;
             } else {
-                lo2 = lo1 + head;
-                hi2 = hi1;
-                hi1 = lo2;
-                h1 = bh_tall;
-                h2 = bh_short;
+                const long long tail_rows = ((2 * g + units - 1) / units) * (long long)bh_short;
+                if (rows > tail_rows + bh_tall) {
+                    head = (int)(((rows - tail_rows) / bh_tall) * bh_tall);
+                    const long long bands = head / bh_tall + (rows - head + bh_short - 1) / bh_short;
+                    cost *= 1.0 + (double)(2 * rad) * bands / rows;
+                } else {
+                    long long b = units * (long long)rows / (2 * g);
+                    if (b > bh_tall) b = bh_tall;
+                    if (b < 4) b = 4;
+                    bh = (int)b;
+                    cost *= (double)(bh + 2 * rad) / bh;
+                }
+            }
+            // fewer than ~12 consumer warps per SM cannot keep enough rows in flight
+            const double warps = (double)o * c / 32.0;
+            if (warps < 12.0) cost *= 12.0 / warps;
+            // prefer the first (widest default) candidate unless another is clearly cheaper
+            if (cost < best_cost * 0.99) {
+                best_cost = cost;
+                nt = c;
+                occ = o;
+                G = g;
+                best_head = head;
+                h1 = h2 = bh;
             }
         }
+        if (nt == 0) nt = forced ? forced : 128;
+        p.tw = COLS_PER_THREAD * nt;
+        p.nstrips = (j.C + p.tw - 1) / p.tw;
+        ns = ns_req;
+        threads = 32 + nt;
+        smem = smem_for(p.tw, ns);
+        if (seg2) {
+            h1 = h2 = bh_short;
+        } else if (best_head > 0) {
+            lo2 = lo1 + best_head;
+            hi2 = hi1;
+            hi1 = lo2;
+            h1 = bh_tall;
+            h2 = bh_short;
+        }
     }
+    p.ns = ns;
+    const long long units = (long long)j.nplanes * p.nstrips;
     if (h1 > hi1 - lo1 && hi1 > lo1) h1 = hi1 - lo1;
     if (hi2 > lo2 && h2 > hi2 - lo2) h2 = hi2 - lo2;
     p.out_lo = lo1;
