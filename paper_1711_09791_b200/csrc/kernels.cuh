@@ -49,6 +49,9 @@ constexpr int HALO = 4;       // smem columns kept either side of a strip (suppo
 constexpr int MAX_RAD = 4;
 constexpr int MAX_W = 2 * MAX_RAD + 1;
 constexpr int MAX_THREADS = 32 + 256;  // producer warp + up to 8 consumer warps
+#ifndef SC_MAXT
+#define SC_MAXT MAX_THREADS
+#endif
 
 struct Params {
     const float* src;
@@ -635,7 +638,10 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 // The kernel
 
 template <int MODE, int RAD, bool ALIGNED>
-__global__ void __launch_bounds__(MAX_THREADS, 1) sepconv_rows_kernel(const __grid_constant__ Params p) {
+#ifndef SC_MINB
+#define SC_MINB 1
+#endif
+__global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = p.ns;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);

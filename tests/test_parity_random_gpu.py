@@ -1,0 +1,142 @@
+"""Randomised parity on the GPU (hypothesis, like the reference's property tests,
+T/conftest.py:13-19): random shapes from the 5x5 minimum up, every odd width
+1..9, random taps and values, all entry points and both producer paths, bit for
+bit against the oracle (which is pinned to the reference)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def bits(a, b):
+    return np.array_equal(np.asarray(a).view(np.uint32), np.asarray(b).view(np.uint32))
+
+
+shapes = st.tuples(st.integers(1, 3), st.integers(5, 90), st.integers(5, 300))
+widths = st.sampled_from([1, 3, 5, 7, 9])
+
+
+@settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(shape=shapes, width=widths, seed=st.integers(0, 2**32 - 1), generic=st.booleans(),
+       extended=st.booleans())
+def test_random_two_pass_and_passes(oracle, monkeypatch, shape, width, seed, generic, extended):
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    P, R, C = shape
+    if R < width or C < width:
+        return
+    monkeypatch.setenv("SC_FORCE_GENERIC", "1" if generic else "0")
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(-2, 2, size=width).astype(np.float32)
+    x = rng.uniform(-300, 300, size=(P, R, C)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    got = dev.two_pass(xd, w, extended=extended).cpu().numpy()
+    assert bits(got, oracle.two_pass(x, w, extended=extended))
+    img, scr = xd.clone(), torch.zeros_like(xd)
+    dev.two_pass_split(img, scr, w, extended=extended)
+    assert bits(img.cpu().numpy(), oracle.two_pass(x, w, extended=extended))
+    assert bits(scr.cpu().numpy(), oracle.two_pass_scratch(x, w, extended=extended))
+    r = width // 2
+    for fn, ofn in ((dev.hpass, oracle.horizontal_rows), (dev.vpass, oracle.vertical_rows)):
+        d = torch.full_like(xd, -5.0)
+        fn(xd, w, d)
+        want = np.full_like(x, -5.0)
+        for p in range(P):
+            ofn(x[p], want[p], w, r, R - r)
+        assert bits(d.cpu().numpy(), want)
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(shape=shapes, width=widths, seed=st.integers(0, 2**32 - 1), generic=st.booleans(), copy=st.booleans())
+def test_random_single_pass(oracle, monkeypatch, shape, width, seed, generic, copy):
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    P, R, C = shape
+    if R < width or C < width:
+        return
+    monkeypatch.setenv("SC_FORCE_GENERIC", "1" if generic else "0")
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(-2, 2, size=width).astype(np.float32)
+    dense = oracle.outer_product(w)
+    x = rng.uniform(-300, 300, size=(P, R, C)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.zeros_like(xd)
+    dev.single_pass(xd, dense, out, copy_back=copy)
+    want = oracle.single_pass(x, dense)
+    assert bits(out.cpu().numpy(), want)
+    if copy:
+        r = width // 2
+        exp = x.copy()
+        exp[:, r:R - r, r:C - r] = want[:, r:R - r, r:C - r]
+        assert bits(xd.cpu().numpy(), exp)
+
+
+@settings(max_examples=25, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(R=st.integers(5, 200), C16=st.integers(1, 40), width=widths, seed=st.integers(0, 2**32 - 1))
+def test_random_ppm_fused(oracle, R, C16, width, seed):
+    """u8 HWC fused path (cols % 16 == 0) == oracle two-pass + rint/clip."""
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    C = 16 * C16
+    if R < width or C < width:
+        return
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(-1, 1.5, size=width).astype(np.float32)
+    pix = rng.integers(0, 256, size=(R, C, 3), dtype=np.uint8)
+    got = dev.two_pass_u8hwc(torch.from_numpy(pix).cuda(), w).cpu().numpy()
+    planes = np.moveaxis(pix, -1, 0).astype(np.float32)
+    conv = oracle.two_pass(np.ascontiguousarray(planes), w)
+    want = np.clip(np.rint(np.moveaxis(conv, 0, -1)), 0, 255).astype(np.uint8)
+    assert np.array_equal(got, want)
+
+
+def test_cuda_graph_capture_replays_bit_exact():
+    """The C-ABI launches are capturable (launch-bound small images run as graphs)."""
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    w = np.array([1, 4, 6, 4, 1], np.float32) / 16
+    x = dev.synthetic((3, 96, 1152), 3, 1)
+    y = torch.empty_like(x)
+    want = dev.two_pass(x, w)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        dev.two_pass(x, w, y)  # warm-up outside capture (caches, work counters)
+        with torch.cuda.graph(g, stream=s):
+            dev.two_pass(x, w, y)
+    y.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
+
+
+def test_side_stream_ordering():
+    """Launches follow torch's current stream: a producer/consumer chain on a side
+    stream sees its own writes."""
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    w = np.array([-1, -2, 7, -2, -1], np.float32)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x = dev.synthetic((3, 257, 1024), 9, 2)
+        y = dev.two_pass(x, w)
+        z = dev.two_pass(y, w)
+    s.synchronize()
+    assert torch.equal(z, dev.two_pass(dev.two_pass(x, w), w))
