@@ -196,7 +196,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     if (ns_req < lags + 2) ns_req = lags + 2;
     if (ns_req > 32) ns_req = 32;
     auto smem_for = [&](int tw, int ns_) {
-        return (size_t)((2 * ns_ * 8 + ns_ * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * (tw + 2 * HALO) * 4;
+        const int sw = aligned ? tw + 2 * HALO : tw + 2 * HALO + 16;  // row_width<ALIGNED>
+        return (size_t)((2 * ns_ * 8 + ns_ * 4 + ns_ * SROWS * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * sw * 4;
     };
     auto occ_for = [&](int threads_, size_t smem_) {
         int o = occupancy(kern, threads_, smem_);

@@ -202,6 +202,14 @@ __device__ __forceinline__ void st4(float* p, const F4& a, bool streaming = fals
 constexpr int SROWS = SC_SROWS;
 constexpr int GROUPS = SC_GROUPS;
 
+// Shared-memory row width (floats): the segment [x0-4, x0+TW+4), plus room for
+// the 16-B realignment of unaligned rows (up to 3 floats before and after, and
+// the 4-float pad the segment starts after).
+template <bool ALIGNED>
+__device__ __forceinline__ int row_width(int tw) {
+    return ALIGNED ? tw + 2 * HALO : tw + 2 * HALO + 16;
+}
+
 struct Item {
     int plane, x0, ylo, yhi, in_lo, in_hi;
 };
@@ -249,13 +257,17 @@ __device__ __forceinline__ bool item_rows_edge(const Params& p, const Item& it) 
 
 template <int MODE, int RAD, bool ALIGNED>
 __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t* full, uint64_t* empty,
-                                         int* sitem) {
+                                         int* sitem, int* sshift) {
     // Items are claimed dynamically (atomic ticket), so CTAs that get more
     // bandwidth do more items and no SM idles in a tail. The claimed item id
     // rides in sitem[slot] of its first stage; id -1 tells consumers to stop.
+    // ALIGNED: rows start 16-B aligned, so each row segment is one bulk copy
+    // straight into place. Otherwise (any width / stride) the copy starts at the
+    // 16-B boundary below the segment and the row's shift (0..3 floats) is
+    // published in sshift[] for the consumers. Either way one lane issues TMA.
     const int lane = threadIdx.x & 31;
-    if (ALIGNED && lane != 0) return;
-    const int SW = p.tw + 2 * HALO;
+    if (lane != 0) return;
+    const int SW = row_width<ALIGNED>(p.tw);
     const int NS = p.ns;
     uint64_t pol = 0;
     if (ALIGNED) pol = (p.flags & F_L2_EVICT_FIRST) ? policy_evict_first() : policy_evict_normal();
@@ -263,19 +275,12 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
     uint32_t phase = 0;
     int gs = 0;
     for (;;) {
-        int item = 0;
-        if (lane == 0) item = atomicAdd(&p.work[0], 1);
-        if (!ALIGNED) item = __shfl_sync(0xffffffffu, item, 0);
+        const int item = atomicAdd(&p.work[0], 1);
         if (item >= p.nitems) {
             if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
-            if (lane == 0) sitem[slot] = -1;
-            if (ALIGNED) {
-                mbar_arrive_expect_tx(&full[slot], 0u);
-            } else {
-                __syncwarp();
-                mbar_arrive(&full[slot]);
-            }
-            if (lane == 0) {
+            sitem[slot] = -1;
+            mbar_arrive_expect_tx(&full[slot], 0u);
+            {
                 // the last CTA out re-arms the ticket pair for the next launch
                 __threadfence();
                 if (atomicAdd(&p.work[1], 1) == (int)gridDim.x - 1) {
@@ -296,20 +301,30 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
             const int nrows = min(SROWS, it.in_hi - r0);
             float* sbase = ring + slot * SROWS * SW + soff;
             const float* g0 = gbase + (long long)(r0 - p.src_row0) * p.src_row_stride;
-            if (lane == 0) sitem[slot] = item;
+            sitem[slot] = item;
             if (ALIGNED) {
                 const uint32_t bytes = (uint32_t)n * 4u;
                 mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
                 for (int k = 0; k < nrows; ++k)
                     bulk_g2s(sbase + k * SW, g0 + (long long)k * p.src_row_stride, bytes, &full[slot], pol);
             } else {
+                // the segment [g, g+n) lands at the 16-B aligned smem index 4 + soff, preceded
+                // by its shift s = (g mod 16 B) / 4 floats: column c sits at c - x0 + 8 + s
+                uint32_t total = 0;
                 for (int k = 0; k < nrows; ++k) {
-                    const float* gr = g0 + (long long)k * p.src_row_stride;
-                    float* sr = sbase + k * SW;
-                    for (int c = lane; c < n; c += 32) sr[c] = __ldg(gr + c);
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(g0 + (long long)k * p.src_row_stride);
+                    const uintptr_t e = a + 4u * (uintptr_t)n;
+                    total += (uint32_t)(((e + 15) & ~(uintptr_t)15) - (a & ~(uintptr_t)15));
                 }
-                __syncwarp();
-                mbar_arrive(&full[slot]);
+                mbar_arrive_expect_tx(&full[slot], total);
+                for (int k = 0; k < nrows; ++k) {
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(g0 + (long long)k * p.src_row_stride);
+                    const uintptr_t a_dn = a & ~(uintptr_t)15;
+                    const uintptr_t e_up = (a + 4u * (uintptr_t)n + 15) & ~(uintptr_t)15;
+                    sshift[slot * SROWS + k] = (int)((a - a_dn) >> 2);
+                    bulk_g2s(sbase + k * SW + 4, reinterpret_cast<const void*>(a_dn), (uint32_t)(e_up - a_dn),
+                             &full[slot], pol);
+                }
             }
             if (++slot == NS) { slot = 0; phase ^= 1u; }
         }
@@ -500,15 +515,102 @@ __device__ __forceinline__ void load_win(float (&win)[12], const float* s) {
     }
 }
 
+// Window of an unaligned row: columns x4-4..x4+7 start `shift` floats past a
+// 16-B boundary. 4 x LDS.128 from the boundary, then a compile-time selection
+// per shift (the shift is uniform across the warp, so the switch never diverges).
+template <int S>
+__device__ __forceinline__ void win_from(float (&win)[12], const float* a) {
+    const F4 q0 = ld4(a), q1 = ld4(a + 4), q2 = ld4(a + 8);
+    float buf[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { buf[i] = q0.v[i]; buf[4 + i] = q1.v[i]; buf[8 + i] = q2.v[i]; }
+    if (S > 0) {
+        const F4 q3 = ld4(a + 12);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) buf[12 + i] = q3.v[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) win[i] = buf[i + S];
+}
+
+__device__ __forceinline__ void load_win_shift(float (&win)[12], const float* aligned_base, int shift) {
+    switch (shift) {
+        case 0: win_from<0>(win, aligned_base); break;
+        case 1: win_from<1>(win, aligned_base); break;
+        case 2: win_from<2>(win, aligned_base); break;
+        default: win_from<3>(win, aligned_base); break;
+    }
+}
+
+// Store 4 columns of an output row whose start is not 16-B aligned. The row's
+// 16-B aligned float4 groups begin e columns into each thread's 4 (e = 0..3,
+// uniform per row): lane l stores the aligned group [x4+e, x4+e+4), gathering
+// column x4+e+c from lane l + (e+c)/4 with one indexed shuffle each, as a
+// single STG.128; lane 0 and lane 31 store their split-off columns one by one.
+// Columns the policy must not touch are never written.
+// ring_mode as store_edge: 0 keep, 1 copy ringv, 2 zero.
+__device__ __forceinline__ void store_shift(float* drow, int x4, int C, int rad, const F4& val, const F4& ringv,
+                                           int ring_mode, int lane) {
+    float o[4];
+    unsigned m = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int col = x4 + c;
+        const bool valid = col >= rad && col < C - rad;
+        o[c] = valid ? val.v[c] : (ring_mode == 1 ? ringv.v[c] : 0.0f);
+        if (col < C && (valid || ring_mode != 0)) m |= 1u << c;
+    }
+    const int e = (4 - (int)((reinterpret_cast<uintptr_t>(drow) >> 2) & 3)) & 3;
+    if (e == 0) {
+        if (m == 0xFu) {
+            st4(drow + x4, F4{{o[0], o[1], o[2], o[3]}});
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (m & (1u << c)) drow[x4 + c] = o[c];
+        }
+        return;
+    }
+    float g[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int k = c + e;              // 1..6
+        const int q = k & 3;              // element index in the source lane
+        const float pick = q == 0 ? o[0] : (q == 1 ? o[1] : (q == 2 ? o[2] : o[3]));
+        g[c] = __shfl_sync(0xffffffffu, pick, min(lane + (k >> 2), 31));
+    }
+    const unsigned nbm = __shfl_down_sync(0xffffffffu, m, 1);
+    if (lane == 0) {  // own columns before the first aligned group
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            if (c < e && (m & (1u << c))) drow[x4 + c] = o[c];
+    }
+    if (lane == 31) {  // the aligned group would reach into the next warp's columns
+#pragma unroll
+        for (int c = 1; c < 4; ++c)
+            if (c >= e && (m & (1u << c))) drow[x4 + c] = o[c];
+        return;
+    }
+    const unsigned gm = ((m >> e) | (nbm << (4 - e))) & 0xFu;
+    if (gm == 0xFu) {
+        st4(drow + x4 + e, F4{{g[0], g[1], g[2], g[3]}});
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (gm & (1u << c)) drow[x4 + e + c] = g[c];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Consumer: one item (plane, strip, band). ROW_EDGE items contain ring rows or
 // rows with a dead row pass; all others run the lean loop.
 
 template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE>
 __device__ __forceinline__ void consume_item(const Params& p, const Item& it, const float* ring, uint64_t* full,
-                                             uint64_t* empty, int& slot, uint32_t& phase, int& gs) {
+                                             uint64_t* empty, const int* sshift, int& slot, uint32_t& phase,
+                                             int& gs) {
     constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
-    const int SW = p.tw + 2 * HALO;
+    const int SW = row_width<ALIGNED>(p.tw);
     const int NS = p.ns;
     const int ct = threadIdx.x - 32;
     const int lane = threadIdx.x & 31;
@@ -556,11 +658,15 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                 const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
                 const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
                 const bool emit = yo >= emit_lo && yo < emit_hi;
+                const int shift = ALIGNED ? 0 : sshift[slot * SROWS + k];
 #pragma unroll
                 for (int g = 0; g < GROUPS; ++g) {
-                    const float* srow = sstage + k * SW + g * tw2;
                     float win[12];
-                    load_win(win, srow);
+                    if (ALIGNED) {
+                        load_win(win, sstage + k * SW + g * tw2);
+                    } else {
+                        load_win_shift(win, sstage + k * SW + g * tw2 + 4, shift);
+                    }
                     F4 own;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) own.v[i] = win[4 + i];
@@ -593,6 +699,8 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                         if (emit && (live || zero_fill)) {
                             if (fast[g] && live)
                                 st4(dcur + 4 * ct + g * tw2 + (it.x0), outv);
+                            else if (!ALIGNED)
+                                store_shift(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0, lane);
                             else
                                 store_edge<ALIGNED>(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
                         }
@@ -604,18 +712,30 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                             if (ring_copy) {
                                 int rr = slot * SROWS + k - RAD;  // ring row of input row yo
                                 if (rr < 0) rr += NS * SROWS;
-                                const float* rrow = ring + rr * SW + 4 * ct;
-                                ringv = ld4(rrow + g * tw2 + 4);
+                                const float* rrow = ring + rr * SW + 4 * ct + g * tw2;
+                                if (ALIGNED) {
+                                    ringv = ld4(rrow + 4);
+                                } else {
+                                    const float* q = rrow + 8 + sshift[rr];
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) ringv.v[i] = q[i];
+                                }
                             } else {
 #pragma unroll
                                 for (int i = 0; i < 4; ++i) ringv.v[i] = 0.0f;
                             }
-                            store_edge<ALIGNED>(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                            if (ALIGNED)
+                                store_edge<ALIGNED>(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                            else
+                                store_shift(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0, lane);
                         }
                     }
                     if (ROW_EDGE && ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD)) {
                         float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
-                        store_edge<ALIGNED>(drow, x4[g], C, 0, own, own, 1);
+                        if (ALIGNED)
+                            store_edge<ALIGNED>(drow, x4[g], C, 0, own, own, 1);
+                        else
+                            store_shift(drow, x4[g], C, 0, own, own, 1, lane);
                     }
                 }
                 if (emit) dcur += p.dst_row_stride;
@@ -647,13 +767,14 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* empty = full + NS;
     int* sitem = reinterpret_cast<int*>(empty + NS);
-    float* ring = reinterpret_cast<float*>(smem_raw + ((2 * NS * 8 + NS * 4 + 127) / 128) * 128);
+    int* sshift = sitem + NS;  // per ring row (NS * SROWS): float shift of an unaligned row
+    float* ring = reinterpret_cast<float*>(smem_raw + ((2 * NS * 8 + NS * 4 + NS * SROWS * 4 + 127) / 128) * 128);
     const int warp = threadIdx.x >> 5;
     const int ncw = (blockDim.x >> 5) - 1;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) {
-            mbar_init(&full[i], ALIGNED ? 1u : 32u);
+            mbar_init(&full[i], 1u);
             mbar_init(&empty[i], (uint32_t)ncw);
         }
         mbar_fence_init();
@@ -661,7 +782,7 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     __syncthreads();
 
     if (warp == 0) {
-        producer<MODE, RAD, ALIGNED>(p, ring, full, empty, sitem);
+        producer<MODE, RAD, ALIGNED>(p, ring, full, empty, sitem, sshift);
         return;
     }
 
@@ -674,9 +795,9 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
         if (item < 0) break;
         const Item it = decode_item<MODE, RAD>(p, item);
         if (item_rows_edge<MODE, RAD>(p, it))
-            consume_item<MODE, RAD, ALIGNED, true>(p, it, ring, full, empty, slot, phase, gs);
+            consume_item<MODE, RAD, ALIGNED, true>(p, it, ring, full, empty, sshift, slot, phase, gs);
         else
-            consume_item<MODE, RAD, ALIGNED, false>(p, it, ring, full, empty, slot, phase, gs);
+            consume_item<MODE, RAD, ALIGNED, false>(p, it, ring, full, empty, sshift, slot, phase, gs);
     }
 }
 

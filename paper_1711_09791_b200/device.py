@@ -42,6 +42,9 @@ def _fp(a: np.ndarray):
 
 def _planes(t: torch.Tensor, what: str):
     """(nplanes, R, C, plane_stride, row_stride) of a CUDA float32 plane stack."""
+    if type(t) is torch.Tensor and t.is_cuda and t.dtype == torch.float32 and t.dim() >= 2 and t.is_contiguous():
+        R, C = t.shape[-2], t.shape[-1]  # fast path: dense stack
+        return t.numel() // (R * C) if R * C else 0, R, C, R * C, C
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise InvalidArgumentError(f"{what} must be a CUDA tensor")
     if t.dtype != torch.float32:
@@ -59,7 +62,13 @@ def _planes(t: torch.Tensor, what: str):
     return v.shape[0], R, C, ps, v.stride(1)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(t: torch.Tensor) -> int:
+    """cudaStream_t of torch's current stream on t's device."""
+    if _raw_stream is not None:
+        return _raw_stream(t.device.index)
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
