@@ -162,7 +162,6 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.flags = j.flags;
     p.one = 1.0f;
     if (env_int("SC_L2_EVICT_FIRST", 0)) p.flags |= F_L2_EVICT_FIRST;
-    if (env_int("SC_ST_CS", 0)) p.flags |= F_ST_CS;
     for (int i = 0; i < j.width; ++i) p.w[i] = j.taps ? j.taps[i] : 0.0f;
     if (j.dense)
         for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];

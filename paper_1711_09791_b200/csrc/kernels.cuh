@@ -43,7 +43,6 @@ constexpr int F_ZERO_FILL = 0x4;
 // tuning flags (set by the planner from SC_* environment variables)
 constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (default: evict_normal,
                                          // which lets neighbouring bands' halo rows hit in L2)
-constexpr int F_ST_CS = 0x200;      // streaming (.cs) stores
 
 constexpr int HALO = 4;       // smem columns kept either side of a strip (supports r <= 4)
 constexpr int MAX_RAD = 4;
@@ -175,12 +174,8 @@ __device__ __forceinline__ F4 ld4(const float* p) {
     return r;
 }
 
-__device__ __forceinline__ void st4(float* p, const F4& a, bool streaming = false) {
-    const float4 t = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
-    if (streaming)
-        __stcs(reinterpret_cast<float4*>(p), t);
-    else
-        *reinterpret_cast<float4*>(p) = t;
+__device__ __forceinline__ void st4(float* p, const F4& a) {
+    *reinterpret_cast<float4*>(p) = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
 }
 
 // ---------------------------------------------------------------------------
