@@ -10,17 +10,21 @@
 //   MODE_VPASS  vertical_rows_vec                         S/conv.py:269-293
 //   MODE_SINGLE single_pass_rows_vec / unrolled5_rows_vec S/conv.py:86-114, :146-175
 //
-// Work decomposition: an "item" is (plane, column strip of TW = 4*NT output
-// columns, row band). A persistent grid walks items round-robin. Per CTA:
-//   warp 0      producer: streams input rows [x0-4, x0+TW+4) of the strip into a
-//               ring of NR shared-memory row slots with the bulk-copy TMA engine
-//               (cp.async.bulk + mbarrier complete_tx); generic (unaligned) mode
-//               uses plain loads by the 32 producer lanes instead.
-//   warps 1..   consumers: thread t owns 4 adjacent output columns. Per input
-//               row it reads 12 samples (3 x LDS.128), computes the row pass for
-//               its 4 columns and pushes them through a shift register of 2r
-//               partial column sums, emitting output row y-r as soon as input
-//               row y arrived. Results go straight to HBM with STG.128.
+// Work decomposition: an "item" is (plane, column strip of TW = 8*NT output
+// columns, row band). A persistent grid claims items from an atomic ticket
+// (dynamic scheduling); the planner in capi.cu picks TW and the band schedule.
+// Per CTA:
+//   warp 0      producer (one lane): streams input rows [x0-4, x0+TW+4) of the
+//               strip into a ring of NS shared-memory stages x SROWS rows with
+//               the bulk-copy TMA engine (cp.async.bulk + mbarrier complete_tx).
+//               Unaligned rows are copied from the 16-B boundary below them and
+//               their shift is published in shared memory.
+//   warps 1..   consumers: thread t owns two 4-column groups (strip offsets 4t
+//               and 4t + TW/2). Per input row and group it reads a 12-sample
+//               window (3 x LDS.128), computes the row pass for its 4 columns
+//               and pushes them through a shift register of 2r partial column
+//               sums, emitting output row y-r as soon as input row y arrived.
+//               Results go straight to HBM with STG.128.
 //
 // Bit-exactness: every product/sum is __fmul_rn/__fadd_rn (never contracted to
 // FMA) in the reference's fold order: left-to-right from the first product,
@@ -66,7 +70,7 @@ struct Params {
     int nitems0;             // items of the first segment; the rest belong to the second
     int hrow_lo, hrow_hi;    // rows where the row pass is live (else H0 = 0 / zero fill)
     int flags;
-    int tw;                  // strip width = 4 * consumer threads
+    int tw;                  // strip width = 8 * consumer threads (two 4-column groups each)
     int nstrips, band_h, nitems;
     int band_h2;             // band height of the second segment
     int ns;                  // smem stages (SROWS rows each)
