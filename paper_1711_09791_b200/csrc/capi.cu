@@ -232,9 +232,10 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         h2 = h1;
     } else {
         const int forced = env_int("SC_NT", 0);
+        const int tail_waves = env_int("SC_TAIL_WAVES", 2) > 0 ? env_int("SC_TAIL_WAVES", 2) : 1;
         static const int cand[] = {128, 96, 64, 160, 192, 256};
         double best_cost = 1e30;
-        int best_head = 0;
+        int best_head = 0, best_tall = bh_tall, best_short = bh_short;
         const int rows = hi1 - lo1;
         for (int c : cand) {
             if (forced && c != forced) continue;
@@ -244,20 +245,28 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
             const size_t sm = smem_for(tw, ns_req);
             const int o = occ_for(32 + c, sm);
             const long long g = (long long)di.sms * o;
+            // band heights scale with the job: fewer than ~8 waves of 128-row items
+            // per CTA -> 64/16 (measured: cfg2 -11%, cfg3 -2.5% time; cfg5 keeps 128/32)
+            int tall = bh_tall, shrt = bh_short;
+            if (!env_int("SC_BAND_H", 0) && !env_int("SC_BAND_H2", 0) &&
+                units * (long long)rows < 8LL * g * 128) {
+                tall = 64;
+                shrt = 16;
+            }
             // padding columns + the 8-column halo of every strip
             double cost = (double)(strips * tw + 2 * HALO * strips) / j.C;
-            int head = 0, bh = bh_short;
+            int head = 0, bh = shrt;
             if (seg2) {
                 cost *= (double)(bh_short + 2 * rad) / bh_short;
             } else {
-                const long long tail_rows = ((2 * g + units - 1) / units) * (long long)bh_short;
-                if (rows > tail_rows + bh_tall) {
-                    head = (int)(((rows - tail_rows) / bh_tall) * bh_tall);
-                    const long long bands = head / bh_tall + (rows - head + bh_short - 1) / bh_short;
+                const long long tail_rows = ((tail_waves * g + units - 1) / units) * (long long)shrt;
+                if (rows > tail_rows + tall) {
+                    head = (int)(((rows - tail_rows) / tall) * tall);
+                    const long long bands = head / tall + (rows - head + shrt - 1) / shrt;
                     cost *= 1.0 + (double)(2 * rad) * bands / rows;
                 } else {
                     long long b = units * (long long)rows / (2 * g);
-                    if (b > bh_tall) b = bh_tall;
+                    if (b > tall) b = tall;
                     if (b < 4) b = 4;
                     bh = (int)b;
                     cost *= (double)(bh + 2 * rad) / bh;
@@ -273,6 +282,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
                 occ = o;
                 G = g;
                 best_head = head;
+                best_tall = tall;
+                best_short = shrt;
                 h1 = h2 = bh;
             }
         }
@@ -288,8 +299,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
             lo2 = lo1 + best_head;
             hi2 = hi1;
             hi1 = lo2;
-            h1 = bh_tall;
-            h2 = bh_short;
+            h1 = best_tall;
+            h2 = best_short;
         }
     }
     p.ns = ns;
