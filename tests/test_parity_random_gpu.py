@@ -140,3 +140,38 @@ def test_side_stream_ordering():
         z = dev.two_pass(y, w)
     s.synchronize()
     assert torch.equal(z, dev.two_pass(dev.two_pass(x, w), w))
+
+
+@pytest.mark.parametrize("off", [0, 1, 2, 3])
+def test_no_out_of_bounds_writes(oracle, off):
+    """compute-sanitizer is closed on this pool, so out-of-bounds writes are
+    checked with canaries: every destination is a view inside a larger buffer
+    filled with a sentinel bit pattern; after each op nothing outside the view
+    (and nothing the op must leave untouched) may change. Offsets 1-3 make the
+    rows unaligned (shifted-TMA path)."""
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    canary = -123.25
+    w = np.array([-1, -2, 7, -2, -1], np.float32)
+    for (P, R, C) in ((3, 37, 131), (2, 64, 256), (1, 5, 5)):
+        x = dev.synthetic((P, R, C), 11, 2)
+        n = P * R * C
+        big = torch.full((n + 64,), canary, device="cuda")
+        dst = big[8 + off: 8 + off + n].view(P, R, C)
+        dev.two_pass(x, w, dst)
+        rest = torch.cat([big[: 8 + off], big[8 + off + n:]])
+        assert bool((rest == canary).all()), "fused wrote outside its destination"
+        assert bits(dst.cpu().numpy(), oracle.two_pass(x.cpu().numpy(), w))
+        # valid-only and single pass must also leave the ring of the view untouched
+        big.fill_(canary)
+        dev.two_pass(x, w, dst, ring=False)
+        dev_ring = dst.clone()
+        dev_ring[:, 2:R - 2, 2:C - 2] = canary
+        assert bool((dev_ring == canary).all()) and bool((torch.cat([big[: 8 + off], big[8 + off + n:]]) == canary).all())
+        big.fill_(canary)
+        dev.single_pass(x, oracle.outer_product(w), dst)
+        assert bool((torch.cat([big[: 8 + off], big[8 + off + n:]]) == canary).all())
+        d2 = dst.clone()
+        d2[:, 2:R - 2, 2:C - 2] = canary
+        assert bool((d2 == canary).all())
