@@ -301,6 +301,18 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
             hi1 = lo2;
             h1 = best_tall;
             h2 = best_short;
+            // SC_EXACT_WAVES=1: stretch the head bands so the head is a whole number
+            // of waves of items (every CTA gets the same number of head items)
+            if (env_int("SC_EXACT_WAVES", 0)) {
+                const long long units = (long long)j.nplanes * ((j.C + COLS_PER_THREAD * nt - 1) / (COLS_PER_THREAD * nt));
+                const int head_rows = hi1 - lo1;
+                long long waves = (units * ((head_rows + best_tall - 1) / best_tall) + G / 2) / G;
+                if (waves < 1) waves = 1;
+                // smallest band count >= waves*G/units, i.e. units*nb is a multiple of G when possible
+                long long nb = (waves * G + units - 1) / units;
+                const int hb = (int)((head_rows + nb - 1) / nb);
+                if (hb >= 8) h1 = hb;
+            }
         }
     }
     p.ns = ns;

@@ -19,7 +19,7 @@ y = torch.empty_like(x)
 dense = np.outer(w, w).astype(np.float32)
 op = {"fused": lambda: dev.two_pass(x, w, y), "single": lambda: dev.single_pass(x, dense, y),
       "hpass": lambda: dev.hpass(x, w, y), "vpass": lambda: dev.vpass(x, w, y)}[a.op]
-KEYS = ["SC_NS", "SC_OCC", "SC_NT", "SC_BAND_H", "SC_BAND_H2", "SC_TAIL_WAVES", "SC_L2_EVICT_FIRST"]
+KEYS = ["SC_NS", "SC_OCC", "SC_NT", "SC_BAND_H", "SC_BAND_H2", "SC_TAIL_WAVES", "SC_EXACT_WAVES", "SC_L2_EVICT_FIRST"]
 def run(env):
     for k in KEYS: os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
