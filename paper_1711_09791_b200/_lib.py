@@ -65,7 +65,7 @@ _vp = ctypes.c_void_p
 _i32 = ctypes.c_int
 _i64 = ctypes.c_int64
 _u64 = ctypes.c_uint64
-_fp = ctypes.POINTER(ctypes.c_float)
+_fp = ctypes.c_void_p  # const float* (taps / dense matrix), passed as an address
 
 _STRIDED = [_vp, _vp, _i32, _i32, _i32, _i64, _i64, _i64, _i64]
 

@@ -16,6 +16,8 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <array>
+#include <unistd.h>
 
 #include "../../include/sepconv_b200.h"
 #include "direct.cuh"
@@ -39,10 +41,37 @@ static int cuda_fail(cudaError_t e, const char* what) {
     return fail(SC_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-static int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    if (!v || !*v) return dflt;
-    return std::atoi(v);
+// Tuning knobs (SC_* environment variables, 0 = unset), read in ONE pass over the
+// environment per launch so a knob changed between calls still takes effect
+// while the common case costs no getenv() per knob.
+struct Knobs {
+    int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
+    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0;
+};
+
+static Knobs read_knobs() {
+    Knobs k;
+    for (char** e = environ; e && *e; ++e) {
+        const char* s = *e;
+        if (s[0] != 'S' || s[1] != 'C' || s[2] != '_') continue;
+        const char* eq = std::strchr(s, '=');
+        if (!eq || !eq[1]) continue;
+        const std::string name(s + 3, eq - s - 3);
+        const int v = std::atoi(eq + 1);
+        if (name == "FORCE_GENERIC") k.force_generic = v;
+        else if (name == "DIRECT") k.direct = v;
+        else if (name == "L2_EVICT_FIRST") k.l2_evict_first = v;
+        else if (name == "DEBUG_PLAN") k.debug_plan = v;
+        else if (name == "OCC") k.occ = v;
+        else if (name == "NS") k.ns = v;
+        else if (name == "NT") k.nt = v;
+        else if (name == "BAND_H") k.band_h = v;
+        else if (name == "BAND_H2") k.band_h2 = v;
+        else if (name == "TAIL_WAVES") k.tail_waves = v;
+        else if (name == "EXACT_WAVES") k.exact_waves = v;
+        else if (name == "IPC") k.ipc = v;
+    }
+    return k;
 }
 
 // --------------------------------------------------------------------------
@@ -56,7 +85,8 @@ static int select_device(const void* ptr) {
         return -1;
     }
     if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged) return -1;
-    cudaSetDevice(attr.device);
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != attr.device) cudaSetDevice(attr.device);
     return attr.device;
 }
 
@@ -87,11 +117,12 @@ static int occupancy(const void* kern, int threads, size_t smem) {
     if (it != cache.end()) return it->second;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) {
+    if (smem > 227 * 1024 ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) {
         cudaGetLastError();
-        occ = 1;
+        occ = 0;  // infeasible (e.g. an SC_NS ring larger than shared memory)
     }
-    if (occ < 1) occ = 1;
+    if (occ < 0) occ = 0;
     cache[key] = occ;
     return occ;
 }
@@ -127,77 +158,39 @@ static constexpr int COLS_PER_THREAD = 4 * GROUPS;  // two 4-column groups per c
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-int launch_rows(const RowsJob& j, cudaStream_t s) {
+// Launch geometry of one job; memoised per (kernel, device, shape, knobs) because
+// planning costs more host time than the launch itself for small images.
+struct Plan {
+    int nt = 0, threads = 0, ns = 0, tw = 0, nstrips = 0, occ = 1, grid = 0;
+    size_t smem = 0;
+    int lo1 = 0, hi1 = 0, lo2 = 0, hi2 = 0, band_h = 1, band_h2 = 1, nitems = 0, nitems0 = 0;
+};
+
+using PlanKey = std::array<long long, 16>;
+
+static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool direct, int dev, const Knobs& kn,
+                     Plan& pl) {
     const int rad = j.width / 2;
-    const void* kern = nullptr;
-    const bool aligned = (j.C % 4 == 0) && aligned16(j.src) && aligned16(j.dst) && (j.sps % 4 == 0) &&
-                         (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) &&
-                         env_int("SC_FORCE_GENERIC", 0) == 0;
-    switch (j.mode) {
-        case MODE_FUSED: kern = kernel_fused(rad, aligned); break;
-        case MODE_HPASS: kern = kernel_hpass(rad, aligned); break;
-        case MODE_VPASS: kern = kernel_vpass(rad, aligned); break;
-        case MODE_SINGLE: kern = kernel_single(rad, aligned); break;
-    }
-    if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(j.width));
     const bool seg2 = j.out_hi2 > j.out_lo2;
-    if ((j.out_hi <= j.out_lo && !seg2) || j.nplanes <= 0) return SC_OK;
-
-    Params p;
-    std::memset(&p, 0, sizeof(p));
-    p.src = j.src;
-    p.dst = j.dst;
-    p.src_plane_stride = j.sps;
-    p.dst_plane_stride = j.dps;
-    p.src_row_stride = j.srs;
-    p.dst_row_stride = j.drs;
-    p.nplanes = j.nplanes;
-    p.R = j.R;
-    p.C = j.C;
-    p.src_row0 = j.src_row0;
-    p.src_rows = j.src_rows;
-    p.dst_row0 = j.dst_row0;
-    p.hrow_lo = j.hrow_lo;
-    p.hrow_hi = j.hrow_hi;
-    p.flags = j.flags;
-    p.one = 1.0f;
-    if (env_int("SC_L2_EVICT_FIRST", 0)) p.flags |= F_L2_EVICT_FIRST;
-    for (int i = 0; i < j.width; ++i) p.w[i] = j.taps ? j.taps[i] : 0.0f;
-    if (j.dense)
-        for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];
-
-    // Kernel family: the TMA stage pipeline (default) or the register-streaming
-    // direct kernel (SC_DIRECT=1), both bit-identical.
-    const bool direct = aligned && env_int("SC_DIRECT", 0) != 0;
-    int nt, threads, ns = 0;
+    int nt = 0, threads = 0, ns = 0, tw = 0;
     size_t smem = 0;
     if (direct) {
-        switch (j.mode) {
-            case MODE_FUSED: kern = kernel_fused_direct(rad); break;
-            case MODE_HPASS: kern = kernel_hpass_direct(rad); break;
-            case MODE_VPASS: kern = kernel_vpass_direct(rad); break;
-            case MODE_SINGLE: kern = kernel_single_direct(rad); break;
-        }
         nt = 32;
-        p.tw = 128;
+        tw = 128;
         threads = 32 * DWARPS;
-    } else {
-        nt = 0;
-        threads = 0;
     }
-
-    int dev = 0;
-    cudaGetDevice(&dev);
     const DevInfo di = dev_info(dev);
-    const int occ_cap = env_int("SC_OCC", 0);
+    const int occ_cap = kn.occ;
     const int lags = (rad + SROWS - 1) / SROWS > 0 ? (rad + SROWS - 1) / SROWS : 1;
-    int ns_req = env_int("SC_NS", 16 / SROWS);
+    int ns_req = kn.ns ? kn.ns : 16 / SROWS;
     if (ns_req < lags + 2) ns_req = lags + 2;
     if (ns_req > 32) ns_req = 32;
-    auto smem_for = [&](int tw, int ns_) {
-        const int sw = aligned ? tw + 2 * HALO : tw + 2 * HALO + 16;  // row_width<ALIGNED>
+    auto smem_for = [&](int tw_, int ns_) {
+        const int sw = aligned ? tw_ + 2 * HALO : tw_ + 2 * HALO + 16;  // row_width<ALIGNED>
         return (size_t)((2 * ns_ * 8 + ns_ * 4 + ns_ * SROWS * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * sw * 4;
     };
+    // an SC_NS ring deeper than shared memory holds for the narrowest strip is clamped
+    while (ns_req > lags + 2 && smem_for(COLS_PER_THREAD * 64, ns_req) > 227 * 1024) --ns_req;
     auto occ_for = [&](int threads_, size_t smem_) {
         int o = occupancy(kern, threads_, smem_);
         if (occ_cap > 0 && o > occ_cap) o = occ_cap;
@@ -216,45 +209,44 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     int lo1 = j.out_lo, hi1 = j.out_hi, lo2 = seg2 ? j.out_lo2 : 0, hi2 = seg2 ? j.out_hi2 : 0;
     if (hi1 <= lo1) { lo1 = lo2; hi1 = hi2; lo2 = hi2 = 0; }
     const int rows_total = (hi1 - lo1) + (hi2 > lo2 ? hi2 - lo2 : 0);
-    int bh_tall = env_int("SC_BAND_H", 128);
-    int bh_short = env_int("SC_BAND_H2", 32);
-    if (bh_tall < 1) bh_tall = 1;
-    if (bh_short < 1) bh_short = 1;
-    int occ = 1, h1 = bh_short, h2 = bh_short;
+    const int bh_tall = kn.band_h > 0 ? kn.band_h : 128;
+    const int bh_short = kn.band_h2 > 0 ? kn.band_h2 : 32;
+    int occ = 1, h1 = bh_short, h2 = bh_short, nstrips = 0;
     long long G = 1;
     if (direct) {
         occ = occ_for(threads, 0);
+        if (occ < 1) return fail(SC_CUDA_ERROR, "direct kernel cannot be resident");
         G = (long long)di.sms * occ * DWARPS;
-        p.nstrips = (j.C + p.tw - 1) / p.tw;
-        const long long units = (long long)j.nplanes * p.nstrips;
+        nstrips = (j.C + tw - 1) / tw;
+        const long long units = (long long)j.nplanes * nstrips;
         h1 = 64;
         while (h1 > 4 && units * ((rows_total + h1 - 1) / h1) < 2 * G) h1 /= 2;
         h2 = h1;
     } else {
-        const int forced = env_int("SC_NT", 0);
-        const int tail_waves = env_int("SC_TAIL_WAVES", 2) > 0 ? env_int("SC_TAIL_WAVES", 2) : 1;
+        const int forced = kn.nt;
+        const int tail_waves = kn.tail_waves > 0 ? kn.tail_waves : 2;
         static const int cand[] = {128, 96, 64, 160, 192, 256};
         double best_cost = 1e30;
         int best_head = 0, best_tall = bh_tall, best_short = bh_short;
         const int rows = hi1 - lo1;
         for (int c : cand) {
             if (forced && c != forced) continue;
-            const int tw = COLS_PER_THREAD * c;
-            const int strips = (j.C + tw - 1) / tw;
+            const int tw_ = COLS_PER_THREAD * c;
+            const int strips = (j.C + tw_ - 1) / tw_;
             const long long units = (long long)j.nplanes * strips;
-            const size_t sm = smem_for(tw, ns_req);
+            const size_t sm = smem_for(tw_, ns_req);
             const int o = occ_for(32 + c, sm);
+            if (o < 1) continue;
             const long long g = (long long)di.sms * o;
             // band heights scale with the job: fewer than ~8 waves of 128-row items
             // per CTA -> 64/16 (measured: cfg2 -11%, cfg3 -2.5% time; cfg5 keeps 128/32)
             int tall = bh_tall, shrt = bh_short;
-            if (!env_int("SC_BAND_H", 0) && !env_int("SC_BAND_H2", 0) &&
-                units * (long long)rows < 8LL * g * 128) {
+            if (!kn.band_h && !kn.band_h2 && units * (long long)rows < 8LL * g * 128) {
                 tall = 64;
                 shrt = 16;
             }
             // padding columns + the 8-column halo of every strip
-            double cost = (double)(strips * tw + 2 * HALO * strips) / j.C;
+            double cost = (double)(strips * tw_ + 2 * HALO * strips) / j.C;
             int head = 0, bh = shrt;
             if (seg2) {
                 cost *= (double)(bh_short + 2 * rad) / bh_short;
@@ -265,7 +257,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
                     const long long bands = head / tall + (rows - head + shrt - 1) / shrt;
                     cost *= 1.0 + (double)(2 * rad) * bands / rows;
                 } else {
-                    long long b = units * (long long)rows / (2 * g);
+                    long long b = units * (long long)rows / ((kn.ipc > 0 ? kn.ipc : 2) * g);
                     if (b > tall) b = tall;
                     if (b < 4) b = 4;
                     bh = (int)b;
@@ -287,12 +279,12 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
                 h1 = h2 = bh;
             }
         }
-        if (nt == 0) nt = forced ? forced : 128;
-        p.tw = COLS_PER_THREAD * nt;
-        p.nstrips = (j.C + p.tw - 1) / p.tw;
+        if (nt == 0) return fail(SC_INVALID_ARGUMENT, "no launch configuration fits shared memory (SC_NS / SC_NT too large)");
+        tw = COLS_PER_THREAD * nt;
+        nstrips = (j.C + tw - 1) / tw;
         ns = ns_req;
         threads = 32 + nt;
-        smem = smem_for(p.tw, ns);
+        smem = smem_for(tw, ns);
         if (seg2) {
             h1 = h2 = bh_short;
         } else if (best_head > 0) {
@@ -303,47 +295,146 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
             h2 = best_short;
             // SC_EXACT_WAVES=1: stretch the head bands so the head is a whole number
             // of waves of items (every CTA gets the same number of head items)
-            if (env_int("SC_EXACT_WAVES", 0)) {
-                const long long units = (long long)j.nplanes * ((j.C + COLS_PER_THREAD * nt - 1) / (COLS_PER_THREAD * nt));
+            if (kn.exact_waves) {
+                const long long units = (long long)j.nplanes * nstrips;
                 const int head_rows = hi1 - lo1;
                 long long waves = (units * ((head_rows + best_tall - 1) / best_tall) + G / 2) / G;
                 if (waves < 1) waves = 1;
                 // smallest band count >= waves*G/units, i.e. units*nb is a multiple of G when possible
-                long long nb = (waves * G + units - 1) / units;
+                const long long nb = (waves * G + units - 1) / units;
                 const int hb = (int)((head_rows + nb - 1) / nb);
                 if (hb >= 8) h1 = hb;
             }
         }
     }
-    p.ns = ns;
-    const long long units = (long long)j.nplanes * p.nstrips;
+    const long long units = (long long)j.nplanes * nstrips;
     if (h1 > hi1 - lo1 && hi1 > lo1) h1 = hi1 - lo1;
     if (hi2 > lo2 && h2 > hi2 - lo2) h2 = hi2 - lo2;
-    p.out_lo = lo1;
-    p.out_hi = hi1;
-    p.out_lo2 = lo2;
-    p.out_hi2 = hi2;
-    p.band_h = h1 > 0 ? h1 : 1;
-    p.band_h2 = h2 > 0 ? h2 : 1;
-    const long long nitems0 = hi1 > lo1 ? units * ((hi1 - lo1 + p.band_h - 1) / p.band_h) : 0;
-    const long long nitems = nitems0 + (hi2 > lo2 ? units * ((hi2 - lo2 + p.band_h2 - 1) / p.band_h2) : 0);
+    pl.band_h = h1 > 0 ? h1 : 1;
+    pl.band_h2 = h2 > 0 ? h2 : 1;
+    const long long nitems0 = hi1 > lo1 ? units * ((hi1 - lo1 + pl.band_h - 1) / pl.band_h) : 0;
+    const long long nitems = nitems0 + (hi2 > lo2 ? units * ((hi2 - lo2 + pl.band_h2 - 1) / pl.band_h2) : 0);
     if (nitems > 0x7fffffffLL) return fail(SC_INVALID_ARGUMENT, "too many work items");
-    p.nitems = (int)nitems;
-    p.nitems0 = (int)nitems0;
-    const int band_h = p.band_h;
     const long long ctas = direct ? (nitems + DWARPS - 1) / DWARPS : nitems;
-    const int grid = (int)(ctas < (long long)di.sms * occ ? ctas : (long long)di.sms * occ);
+    pl.nt = nt;
+    pl.threads = threads;
+    pl.ns = ns;
+    pl.tw = tw;
+    pl.nstrips = nstrips;
+    pl.occ = occ;
+    pl.smem = smem;
+    pl.lo1 = lo1;
+    pl.hi1 = hi1;
+    pl.lo2 = lo2;
+    pl.hi2 = hi2;
+    pl.nitems = (int)nitems;
+    pl.nitems0 = (int)nitems0;
+    pl.grid = (int)(ctas < (long long)di.sms * occ ? ctas : (long long)di.sms * occ);
+    return SC_OK;
+}
+
+static int cached_plan(const RowsJob& j, const void* kern, bool aligned, bool direct, int dev, const Knobs& kn,
+                       Plan& pl) {
+    static std::mutex mu;
+    static std::map<PlanKey, Plan> cache;
+    const PlanKey key = {(long long)(uintptr_t)kern, (long long)direct, dev, j.nplanes, j.C, j.out_lo, j.out_hi,
+                         j.out_lo2, j.out_hi2, kn.occ, kn.ns, kn.nt, kn.band_h, kn.band_h2,
+                         (long long)kn.tail_waves * 2 + (kn.exact_waves != 0), (long long)aligned * 1024 + kn.ipc};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            pl = it->second;
+            return SC_OK;
+        }
+    }
+    const int rc = plan_rows(j, kern, aligned, direct, dev, kn, pl);
+    if (rc != SC_OK) return rc;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 4096) cache.clear();
+    cache[key] = pl;
+    return SC_OK;
+}
+
+int launch_rows(const RowsJob& j, cudaStream_t s) {
+    const int rad = j.width / 2;
+    const Knobs kn = read_knobs();
+    const void* kern = nullptr;
+    const bool aligned = (j.C % 4 == 0) && aligned16(j.src) && aligned16(j.dst) && (j.sps % 4 == 0) &&
+                         (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) && kn.force_generic == 0;
+    switch (j.mode) {
+        case MODE_FUSED: kern = kernel_fused(rad, aligned); break;
+        case MODE_HPASS: kern = kernel_hpass(rad, aligned); break;
+        case MODE_VPASS: kern = kernel_vpass(rad, aligned); break;
+        case MODE_SINGLE: kern = kernel_single(rad, aligned); break;
+    }
+    if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(j.width));
+    const bool seg2 = j.out_hi2 > j.out_lo2;
+    if ((j.out_hi <= j.out_lo && !seg2) || j.nplanes <= 0) return SC_OK;
+
+    // Kernel family: the TMA stage pipeline (default) or the register-streaming
+    // direct kernel (SC_DIRECT=1), both bit-identical.
+    const bool direct = aligned && kn.direct != 0;
+    if (direct) {
+        switch (j.mode) {
+            case MODE_FUSED: kern = kernel_fused_direct(rad); break;
+            case MODE_HPASS: kern = kernel_hpass_direct(rad); break;
+            case MODE_VPASS: kern = kernel_vpass_direct(rad); break;
+            case MODE_SINGLE: kern = kernel_single_direct(rad); break;
+        }
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Plan pl;
+    {
+        const int rc = cached_plan(j, kern, aligned, direct, dev, kn, pl);
+        if (rc != SC_OK) return rc;
+    }
+
+    Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.src = j.src;
+    p.dst = j.dst;
+    p.src_plane_stride = j.sps;
+    p.dst_plane_stride = j.dps;
+    p.src_row_stride = j.srs;
+    p.dst_row_stride = j.drs;
+    p.nplanes = j.nplanes;
+    p.R = j.R;
+    p.C = j.C;
+    p.src_row0 = j.src_row0;
+    p.src_rows = j.src_rows;
+    p.dst_row0 = j.dst_row0;
+    p.hrow_lo = j.hrow_lo;
+    p.hrow_hi = j.hrow_hi;
+    p.flags = j.flags;
+    p.one = 1.0f;
+    if (kn.l2_evict_first) p.flags |= F_L2_EVICT_FIRST;
+    for (int i = 0; i < j.width; ++i) p.w[i] = j.taps ? j.taps[i] : 0.0f;
+    if (j.dense)
+        for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];
+    p.tw = pl.tw;
+    p.nstrips = pl.nstrips;
+    p.ns = pl.ns;
+    p.out_lo = pl.lo1;
+    p.out_hi = pl.hi1;
+    p.out_lo2 = pl.lo2;
+    p.out_hi2 = pl.hi2;
+    p.band_h = pl.band_h;
+    p.band_h2 = pl.band_h2;
+    p.nitems = pl.nitems;
+    p.nitems0 = pl.nitems0;
     p.work = work_slot(dev);
     if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
 
     void* args[] = {&p};
-    cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, s);
+    cudaError_t e = cudaLaunchKernel(kern, dim3(pl.grid), dim3(pl.threads), args, pl.smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     count_launch();
-    if (env_int("SC_DEBUG_PLAN", 0))
+    if (kn.debug_plan)
         std::fprintf(stderr, "[sc] mode=%d rad=%d aligned=%d nt=%d tw=%d strips=%d ns=%d seg1=[%d,%d)/%d seg2=[%d,%d)/%d items=%d grid=%d occ=%d smem=%zu\n",
-                     j.mode, rad, (int)aligned, nt, p.tw, p.nstrips, ns, p.out_lo, p.out_hi, band_h, p.out_lo2, p.out_hi2,
-                     p.band_h2, p.nitems, grid, occ, smem);
+                     j.mode, rad, (int)aligned, pl.nt, p.tw, p.nstrips, pl.ns, p.out_lo, p.out_hi, p.band_h, p.out_lo2,
+                     p.out_hi2, p.band_h2, p.nitems, pl.grid, pl.occ, pl.smem);
     return SC_OK;
 }
 
@@ -378,7 +469,8 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
     }
     p.tw = 4 * nt;
     p.nstrips = (C + p.tw - 1) / p.tw;
-    int ns = env_int("SC_NS", 4);
+    const Knobs kn = read_knobs();
+    int ns = kn.ns ? kn.ns : 4;
     if (ns < 3) ns = 3;
     if (ns > 32) ns = 32;
     p.ns = ns;
@@ -388,8 +480,9 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
     cudaGetDevice(&dev);
     const DevInfo di = dev_info(dev);
     const int occ = occupancy(kern, threads, smem);
+    if (occ < 1) return fail(SC_INVALID_ARGUMENT, "no launch configuration fits shared memory (SC_NS too large)");
     const long long G = (long long)di.sms * occ;
-    int band_h = env_int("SC_BAND_H", 64);
+    int band_h = kn.band_h ? kn.band_h : 64;
     while (band_h > 8 && (long long)p.nstrips * ((R + band_h - 1) / band_h) < 2 * G) band_h /= 2;
     if (band_h > R) band_h = R;
     p.band_h = band_h;

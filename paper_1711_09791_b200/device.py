@@ -20,6 +20,8 @@ from .errors import InvalidArgumentError
 
 def _taps(taps) -> np.ndarray:
     w = getattr(taps, "weights", taps)  # SeparableKernel or array-like
+    if type(w) is np.ndarray and w.dtype == np.float32 and w.ndim == 1 and w.flags.c_contiguous:
+        return w
     if isinstance(w, torch.Tensor):
         w = w.detach().cpu().numpy()
     w = np.ascontiguousarray(w, dtype=np.float32).reshape(-1)
@@ -36,8 +38,9 @@ def _dense(dense) -> np.ndarray:
     return m
 
 
-def _fp(a: np.ndarray):
-    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+def _fp(a: np.ndarray) -> int:
+    """Address of a float32 host array (the caller keeps `a` alive across the call)."""
+    return a.ctypes.data
 
 
 def _planes(t: torch.Tensor, what: str):

@@ -6,7 +6,7 @@ from paper_1711_09791_b200 import device as dev, _lib
 L = _lib.load()
 x = dev.synthetic((3, 64, 1024), 1, 1); y = torch.empty_like(x)
 w = np.array([1, 4, 6, 4, 1], np.float32) / 16
-taps = w.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+taps = w.ctypes.data
 stream = torch.cuda.current_stream().cuda_stream
 def bench(fn, n=2000):
     for _ in range(50): fn()

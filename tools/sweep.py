@@ -10,6 +10,7 @@ ap.add_argument("--cfg", default="cfg5")
 ap.add_argument("--op", default="fused")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--grid", default="")
+ap.add_argument("--graph", action="store_true", help="time 20 launches captured in a CUDA graph (no host overhead)")
 a = ap.parse_args()
 wl = CONFIGS[a.cfg]
 w = wl.tap_vector()
@@ -19,12 +20,25 @@ y = torch.empty_like(x)
 dense = np.outer(w, w).astype(np.float32)
 op = {"fused": lambda: dev.two_pass(x, w, y), "single": lambda: dev.single_pass(x, dense, y),
       "hpass": lambda: dev.hpass(x, w, y), "vpass": lambda: dev.vpass(x, w, y)}[a.op]
-KEYS = ["SC_NS", "SC_OCC", "SC_NT", "SC_BAND_H", "SC_BAND_H2", "SC_TAIL_WAVES", "SC_EXACT_WAVES", "SC_L2_EVICT_FIRST"]
+KEYS = ["SC_NS", "SC_OCC", "SC_NT", "SC_BAND_H", "SC_BAND_H2", "SC_TAIL_WAVES", "SC_EXACT_WAVES", "SC_L2_EVICT_FIRST", "SC_IPC"]
 def run(env):
     for k in KEYS: os.environ.pop(k, None)
     os.environ.update({k: str(v) for k, v in env.items()})
     for _ in range(3): op()
     torch.cuda.synchronize()
+    if a.graph:
+        g = torch.cuda.CUDAGraph(); st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                for _ in range(20): op()
+        g.replay(); torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(a.reps):
+            s.record(); g.replay(); e.record(); e.synchronize(); ts.append(s.elapsed_time(e) / 20)
+        med = float(np.median(ts))
+        print(json.dumps({"env": env, "ms": round(med, 5), "GBps": round(wl.alg_bytes / med / 1e6, 1), "graph": True}), flush=True)
+        return
     ts = []
     for _ in range(a.reps):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
