@@ -151,6 +151,19 @@ static int* work_slot(int dev) {
     return b + 2 * k;
 }
 
+#ifdef SC_TRACE
+// dev-only timeline buffer of the last launch (see TRACE_SLOTS in kernels.cuh)
+static constexpr int kTraceCtas = 4096;
+static unsigned long long* g_trace = nullptr;
+static unsigned long long* trace_buffer() {
+    if (!g_trace && cudaMalloc(&g_trace, sizeof(unsigned long long) * TRACE_SLOTS * kTraceCtas) != cudaSuccess) {
+        cudaGetLastError();
+        g_trace = nullptr;
+    }
+    return g_trace;
+}
+#endif
+
 // --------------------------------------------------------------------------
 // Planner
 
@@ -426,6 +439,11 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.nitems0 = pl.nitems0;
     p.work = work_slot(dev);
     if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
+#ifdef SC_TRACE
+    p.trace = trace_buffer();
+    if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * TRACE_SLOTS * kTraceCtas, s);
+    if (pl.grid > kTraceCtas) p.trace = nullptr;
+#endif
 
     void* args[] = {&p};
     cudaError_t e = cudaLaunchKernel(kern, dim3(pl.grid), dim3(pl.threads), args, pl.smem, s);
@@ -557,6 +575,16 @@ int sc_abi_version(void) { return 1; }
 const char* sc_last_error(void) { return t_err.c_str(); }
 
 uint64_t sc_launch_count(void) { return g_launches.load(); }
+
+#ifdef SC_TRACE
+// dev-only (SC_TRACE builds): copy the last launch's per-CTA timeline to host
+int sc_trace_copy(void* host, long long words) {
+    if (!g_trace) return SC_INVALID_ARGUMENT;
+    const long long n = words < (long long)TRACE_SLOTS * kTraceCtas ? words : (long long)TRACE_SLOTS * kTraceCtas;
+    return cudaMemcpy(host, g_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) == cudaSuccess
+               ? SC_OK : SC_CUDA_ERROR;
+}
+#endif
 
 int sc_two_pass_band2_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
                           int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,

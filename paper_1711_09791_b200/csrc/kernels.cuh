@@ -76,9 +76,28 @@ struct Params {
     int ns;                  // smem stages (SROWS rows each)
     float one;               // 1.0f, passed at run time (see mad2)
     int* work;               // [next item, finished CTAs]: dynamic scheduling ticket pair (zero at launch)
+    unsigned long long* trace;  // SC_TRACE builds only: per-CTA timeline (else null)
     float w[MAX_W];
     float k[MAX_W * MAX_W];
 };
+
+// SC_TRACE (a dev-only build variant): per-CTA timeline of TRACE_SLOTS words.
+//   [0] globaltimer at start, [1] clock64 at start, [2..9] clock64 when the
+//   producer's claim for item i returned, [10..17] item ids, [20..27] clock64 when
+//   the consumers saw item i's first stage, [30..37] clock64 when they finished it,
+//   [40] clock64 at consumer exit, [41] globaltimer at exit, [42] items, [43] smid
+constexpr int TRACE_SLOTS = 48;
+#ifdef SC_TRACE
+__device__ __forceinline__ unsigned long long trace_gt() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SC_TR(p, idx, val) \
+    do { if ((p).trace) (p).trace[(size_t)blockIdx.x * TRACE_SLOTS + (idx)] = (unsigned long long)(val); } while (0)
+#else
+#define SC_TR(p, idx, val) do { } while (0)
+#endif
 
 // Interleaved-u8 (PPM payload) fused path, csrc/kern_u8.cu
 constexpr int U8_HALO = 16;   // columns either side of a strip (16*3 bytes keeps TMA 16-B aligned)
@@ -273,8 +292,18 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
     int slot = 0;
     uint32_t phase = 0;
     int gs = 0;
+#ifdef SC_TRACE
+    int ntr = 0;
+#endif
     for (;;) {
         const int item = atomicAdd(&p.work[0], 1);
+#ifdef SC_TRACE
+        if (ntr < 8) {
+            SC_TR(p, 2 + ntr, clock64());
+            SC_TR(p, 10 + ntr, item);
+        }
+        ++ntr;
+#endif
         if (item >= p.nitems) {
             if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
             sitem[slot] = -1;
@@ -654,6 +683,10 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                 const int shift = ALIGNED ? 0 : sshift[slot * SROWS + k];
 #pragma unroll
                 for (int g = 0; g < GROUPS; ++g) {
+                    // a warp whose group lies wholly right of the image (the padding of a
+                    // partial last strip) has nothing to store: skip its arithmetic. The
+                    // test is warp-uniform (lane 0's columns), as store_shift shuffles.
+                    if (x4[g] - 4 * lane >= C) continue;
                     float win[12];
                     if (ALIGNED) {
                         load_win(win, sstage + k * SW + g * tw2);
@@ -677,7 +710,11 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                         F4 v;
                         if (MODE == MODE_FUSED) {
                             if (live) {
+#ifdef SC_NOCOMPUTE
+                                v = own;
+#else
                                 v = row_pass<RAD>(win, p.w, p.one);
+#endif
                             } else {
 #pragma unroll
                                 for (int i = 0; i < 4; ++i) v.v[i] = 0.0f;  // faithful: scratch row stays 0
@@ -685,7 +722,11 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                         } else {
                             v = own;  // VPASS: src already holds the row-pass result
                         }
+#ifdef SC_NOCOMPUTE
+                        outv = v;  // dev-only variant: pipeline cost without the arithmetic
+#else
                         outv = col_fold<RAD, NACC>(acc[g], v, p.w, p.one);
+#endif
                     }
                     if (MODE == MODE_HPASS) {
                         // dead rows are written only under zero fill
@@ -775,6 +816,15 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     __syncthreads();
 
     if (warp == 0) {
+#ifdef SC_TRACE
+        if (threadIdx.x == 0) {
+            SC_TR(p, 0, trace_gt());
+            SC_TR(p, 1, clock64());
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            SC_TR(p, 43, smid);
+        }
+#endif
         producer<MODE, RAD, ALIGNED>(p, ring, full, empty, sitem, sshift);
         return;
     }
@@ -782,16 +832,33 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     int slot = 0;
     uint32_t phase = 0;
     int gs = 0;
+#ifdef SC_TRACE
+    int ntr = 0;
+#endif
     for (;;) {
         mbar_wait(&full[slot], phase);
         const int item = sitem[slot];
         if (item < 0) break;
+#ifdef SC_TRACE
+        if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 20 + ntr, clock64());
+#endif
         const Item it = decode_item<MODE, RAD>(p, item);
         if (item_rows_edge<MODE, RAD>(p, it))
             consume_item<MODE, RAD, ALIGNED, true>(p, it, ring, full, empty, sshift, slot, phase, gs);
         else
             consume_item<MODE, RAD, ALIGNED, false>(p, it, ring, full, empty, sshift, slot, phase, gs);
+#ifdef SC_TRACE
+        if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 30 + ntr, clock64());
+        ++ntr;
+#endif
     }
+#ifdef SC_TRACE
+    if (threadIdx.x == 32) {
+        SC_TR(p, 40, clock64());
+        SC_TR(p, 41, trace_gt());
+        SC_TR(p, 42, ntr);
+    }
+#endif
 }
 
 }  // namespace sc

@@ -11,8 +11,12 @@ ap.add_argument("--op", default="fused")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--grid", default="")
 ap.add_argument("--graph", action="store_true", help="time 20 launches captured in a CUDA graph (no host overhead)")
+ap.add_argument("--size", type=int, default=0, help="override: 3 x size x size, gauss5")
 a = ap.parse_args()
 wl = CONFIGS[a.cfg]
+if a.size:
+    import dataclasses
+    wl = dataclasses.replace(wl, rows=a.size, cols=a.size, frames=1, planes=3)
 w = wl.tap_vector()
 shape = (wl.frames, wl.planes, wl.rows, wl.cols) if wl.frames > 1 else (wl.planes, wl.rows, wl.cols)
 x = dev.synthetic(shape, wl.seed, wl.kind)
