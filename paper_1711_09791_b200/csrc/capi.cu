@@ -167,7 +167,6 @@ static unsigned long long* trace_buffer() {
 // --------------------------------------------------------------------------
 // Planner
 
-static constexpr int COLS_PER_THREAD = 4 * GROUPS;  // two 4-column groups per consumer thread
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -185,6 +184,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
                      Plan& pl) {
     const int rad = j.width / 2;
     const bool seg2 = j.out_hi2 > j.out_lo2;
+    const int COLS_PER_THREAD = 4 * groups_of(j.mode);  // 4-column groups per consumer thread
     int nt = 0, threads = 0, ns = 0, tw = 0;
     size_t smem = 0;
     if (direct) {

@@ -85,8 +85,9 @@ struct Params {
 //   [0] globaltimer at start, [1] clock64 at start, [2..9] clock64 when the
 //   producer's claim for item i returned, [10..17] item ids, [20..27] clock64 when
 //   the consumers saw item i's first stage, [30..37] clock64 when they finished it,
-//   [40] clock64 at consumer exit, [41] globaltimer at exit, [42] items, [43] smid
-constexpr int TRACE_SLOTS = 48;
+//   [40] clock64 at consumer exit, [41] globaltimer at exit, [42] items, [43] smid,
+//   [48..55] clock64 when stage s (CTA-wide count) was ready, [56..63] when it was done
+constexpr int TRACE_SLOTS = 64;
 #ifdef SC_TRACE
 __device__ __forceinline__ unsigned long long trace_gt() {
     unsigned long long t;
@@ -204,12 +205,18 @@ __device__ __forceinline__ void st4(float* p, const F4& a) {
 // ---------------------------------------------------------------------------
 // Geometry
 //
-// Strip = TW = 8*NT output columns; consumer thread t owns two 4-column groups
-// at strip offsets 4t and 4t + TW/2, so each warp-wide STG.128 writes 512
-// contiguous bytes. Rows travel in stages of SROWS rows per mbarrier pair.
+// Strip = TW = 4*GROUPS*NT output columns; consumer thread t owns GROUPS
+// 4-column groups at strip offsets 4t + g*TW/GROUPS, so each warp-wide STG.128
+// writes 512 contiguous bytes. Rows travel in stages of SROWS rows per mbarrier
+// pair. GROUPS per mode (measured on B200): the two-pass modes run one group per
+// thread (fewer registers -> 4 CTAs/SM; fused 2592^2 -17%, cfg5 -1%), the
+// FP32-bound single pass keeps two (more independent FMA chains per thread).
 
 #ifndef SC_GROUPS
-#define SC_GROUPS 2
+#define SC_GROUPS 1
+#endif
+#ifndef SC_GROUPS_SINGLE
+#define SC_GROUPS_SINGLE 2
 #endif
 #ifndef SC_F2
 #define SC_F2 1
@@ -218,7 +225,7 @@ __device__ __forceinline__ void st4(float* p, const F4& a) {
 #define SC_SROWS 4
 #endif
 constexpr int SROWS = SC_SROWS;
-constexpr int GROUPS = SC_GROUPS;
+__host__ __device__ constexpr int groups_of(int mode) { return mode == MODE_SINGLE ? SC_GROUPS_SINGLE : SC_GROUPS; }
 
 // Shared-memory row width (floats): the segment [x0-4, x0+TW+4), plus room for
 // the 16-B realignment of unaligned rows (up to 3 floats before and after, and
@@ -636,6 +643,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
     const int NS = p.ns;
     const int ct = threadIdx.x - 32;
     const int lane = threadIdx.x & 31;
+    constexpr int GROUPS = groups_of(MODE);
     const int tw2 = p.tw / GROUPS;  // column offset between a thread's groups
     const int R = p.R, C = p.C;
     const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);
@@ -671,6 +679,9 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 
     for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
         if (r0 != it.in_lo) mbar_wait(&full[slot], phase);  // the item's first stage was waited by the caller
+#ifdef SC_TRACE
+        if (threadIdx.x == 32 && gs < 8) SC_TR(p, 48 + gs, clock64());
+#endif
         // stages are contiguous in smem: the ring is one circular buffer of NS*SROWS rows
         const float* sstage = ring + slot * SROWS * SW + 4 * ct;
 #pragma unroll
@@ -775,6 +786,9 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                 if (emit) dcur += p.dst_row_stride;
             }
         }
+#ifdef SC_TRACE
+        if (threadIdx.x == 32 && gs < 8) SC_TR(p, 56 + gs, clock64());
+#endif
         // this stage is done; release the one LAGS stages back (rows up to RAD back
         // are still read for the ring columns)
         constexpr int LAGS = (RAD + SROWS - 1) / SROWS > 0 ? (RAD + SROWS - 1) / SROWS : 1;

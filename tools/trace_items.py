@@ -19,7 +19,7 @@ os.environ["SC_DEBUG_PLAN"] = "1"
 dev.two_pass(x, w, y)
 torch.cuda.synchronize()
 os.environ.pop("SC_DEBUG_PLAN")
-S = 48
+S = 64
 buf = np.zeros(S * 4096, np.uint64)
 assert L.sc_trace_copy(buf.ctypes.data, buf.size) == 0
 t = buf.reshape(4096, S).astype(np.int64)
@@ -64,3 +64,10 @@ if os.environ.get("TRACE_DETAIL"):
         items = [(int(r[10 + i]), round(base + c2u(r[2 + i] - r[1]), 2), round(base + c2u(r[20 + i] - r[1]), 2) if r[20 + i] else None,
                   round(base + c2u(r[30 + i] - r[1]), 2) if r[30 + i] else None) for i in range(n)]
         print(json.dumps({"cta": int(k), "sm": int(r[43]), "end_us": round(float(end[k]), 2), "items": items}))
+
+if os.environ.get("TRACE_STAGES"):
+    # stage readiness/done times (us from CTA start) of the first 8 stages for a few CTAs
+    for k in range(min(4, len(ctas))):
+        r = ctas[k]
+        st = [(round(c2u(r[48 + i] - r[1]), 2), round(c2u(r[56 + i] - r[1]), 2)) for i in range(8) if r[48 + i]]
+        print(json.dumps({"cta": k, "claim0": round(c2u(r[2] - r[1]), 2), "stages_ready_done": st}))
