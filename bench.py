@@ -208,6 +208,21 @@ def host_chunk_bytes(rows, cols, planes, r, band_lo, band_hi, in_lo, in_hi):
     return h2d * planes, d2h * planes
 
 
+def halo_mode(choice: str, world: int) -> str:
+    """Row-band halo transport for N>1: 'peer' needs peer access between every
+    pair of local GPUs (NVLink/NVSwitch) -- or, in the one-GPU multi-rank debug
+    mode, IPC on the same device."""
+    import torch
+
+    if choice != "auto":
+        return choice
+    n = torch.cuda.device_count()
+    if n < 2:
+        return "peer"  # ranks share the one device: IPC within a device needs no peer access
+    ok = all(torch.cuda.can_device_access_peer(a, b) for a in range(n) for b in range(n) if a != b)
+    return "peer" if ok else "nccl"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -218,6 +233,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-rows", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--halo", default="auto", choices=["auto", "peer", "nccl"],
+                    help="N>1 row bands: halo rows read in-kernel from the neighbours' memory (peer, "
+                         "CUDA IPC over NVLink) or exchanged with NCCL send/recv (nccl); auto = peer when "
+                         "every pair of local GPUs has peer access")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = CONFIGS[args.config]
@@ -230,7 +249,7 @@ def main():
 
     from paper_1711_09791_b200 import _lib
     from paper_1711_09791_b200 import device as dev
-    from paper_1711_09791_b200.multi import BandStepper, band_plan, band_two_pass, frame_shard
+    from paper_1711_09791_b200.multi import BandStepper, PeerBandStepper, band_plan, band_two_pass, frame_shard
 
     world, rank, local = dist_env()
     backend = os.environ.get("SEPCONV_BENCH_BACKEND", "nccl")  # gloo: orchestration check on one GPU
@@ -250,6 +269,7 @@ def main():
     per_frame = P * R * C
 
     # ---- inputs resident in HBM (generated in place: counter-based, no scatter)
+    halo = "none"
     if wl.frames > 1:
         f0, f1 = frame_shard(wl.frames, rank, world)
         src = torch.empty((f1 - f0, P, R, C), dtype=torch.float32, device=device)
@@ -262,13 +282,21 @@ def main():
             dev.two_pass(src, w, dst)
     else:
         band = band_plan(R, rank, world, r)
-        src = torch.empty((P, band.local_rows, C), dtype=torch.float32, device=device)
+        halo = halo_mode(args.halo, world) if world > 1 else "none"
+        rows_held = (band.lo, band.hi) if halo == "peer" else (band.in_lo, band.in_hi)
+        src = torch.empty((P, rows_held[1] - rows_held[0], C), dtype=torch.float32, device=device)
         for p in range(P):
-            # owned rows plus the halo rows (the halo is refreshed by the exchange each step)
-            dev.fill_synthetic(src[p], wl.seed, wl.kind, offset=p * R * C + band.in_lo * C)
+            # peer: owned rows only (the kernel reads the halo rows from the neighbours);
+            # nccl: owned rows plus the halo rows (refreshed by the exchange each step)
+            dev.fill_synthetic(src[p], wl.seed, wl.kind, offset=p * R * C + rows_held[0] * C)
         dst = torch.empty((P, band.hi - band.lo, C), dtype=torch.float32, device=device)
         units_px = (band.hi - band.lo) * C
-        stepper = BandStepper(src, dst, band, w) if world > 1 else None
+        stepper = None
+        if halo == "peer":
+            stepper = PeerBandStepper(src, dst, band, w)
+            stepper.sync()  # every band written before any kernel reads a neighbour's rows
+        elif halo == "nccl":
+            stepper = BandStepper(src, dst, band, w)
 
         def step():
             if world == 1:
@@ -371,22 +399,31 @@ def main():
             def e2e_step():
                 dev.two_pass_host(planes, planes, w, device=local)
         elif band is not None:
-            # N>1: each rank streams its band (+halo rows) from its own pinned buffer
-            hb = torch.empty((P, band.local_rows, C), dtype=torch.float32, pin_memory=True)
+            # N>1: each rank streams its band (nccl: + halo rows) from its own pinned buffer
+            hb = torch.empty(src.shape, dtype=torch.float32, pin_memory=True)
             hb.copy_(src.cpu())
             ho = torch.empty((P, band.hi - band.lo, C), dtype=torch.float32, pin_memory=True)
-            h2d = P * band.local_rows * C * 4
+            h2d = hb.numel() * 4
             d2h = P * (band.hi - band.lo) * C * 4
             ds = torch.empty_like(src)
             do = torch.empty_like(dst)
+            if halo == "peer":
+                e2e_stepper = PeerBandStepper(ds, do, band, w)
 
-            e2e_stepper = BandStepper(ds, do, band, w)
+                def e2e_step():
+                    ds.copy_(hb, non_blocking=True)
+                    e2e_stepper.sync()      # neighbours' rows landed before the kernel reads them
+                    e2e_stepper.step()
+                    ho.copy_(do, non_blocking=True)
+                    e2e_stepper.sync()      # nobody overwrites rows a neighbour still reads
+            else:
+                e2e_stepper = BandStepper(ds, do, band, w)
 
-            def e2e_step():
-                ds.copy_(hb, non_blocking=True)
-                e2e_stepper.step()
-                ho.copy_(do, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+                def e2e_step():
+                    ds.copy_(hb, non_blocking=True)
+                    e2e_stepper.step()
+                    ho.copy_(do, non_blocking=True)
+                    torch.cuda.current_stream().synchronize()
         else:
             # frame batch: every frame-plane is one host plane of the reference's
             # Image; the C-ABI host entry point streams them all (in place)
@@ -415,7 +452,9 @@ def main():
         e2e = {"value": round(total_px / (e_ms / 1e3) / 1e9, 4), "unit": "Gpix/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3),
                "path": "sc_two_pass_host_f32 (pinned host planes, chunked H2D/kernel/D2H on 3 streams)"
-               if (world == 1 or band is None) else "pinned H2D + BandStepper (halo exchange) + D2H per rank"}
+               if (world == 1 or band is None) else
+               ("pinned H2D + PeerBandStepper (in-kernel peer halo reads) + D2H per rank" if halo == "peer" else
+                "pinned H2D + BandStepper (NCCL halo exchange) + D2H per rank")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -430,7 +469,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": f"{wl.name}: {wl.note}", "frames": wl.frames, "planes": P, "rows": R, "cols": C,
                        "taps": [float(v) for v in w], "parallelism": f"rowband{world}" if wl.frames == 1
-                       else f"frames{world}", "l2": l2_note},
+                       else f"frames{world}", "l2": l2_note,
+                       **({"halo": halo} if band is not None and world > 1 else {})},
             "effective_GBps": round(eff, 1), "pct_of_8TBps": round(100 * eff / NOMINAL_HBM_GBPS, 2),
             "pct_of_measured_copy": round(100 * eff / peak, 2),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

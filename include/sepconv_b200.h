@@ -75,6 +75,31 @@ int sc_two_pass_band2_f32(const float *src, float *dst, int nplanes, int global_
                           int src_row0, int src_rows, int dst_row0, int out_lo, int out_hi,
                           int out_lo2, int out_hi2, const float *taps, int width, int flags, void *stream);
 
+/* One row band whose halo rows are read straight from the neighbouring bands'
+ * buffers (other GPUs' memory mapped with sc_ipc_open; multi-GPU without a
+ * separate exchange step). src holds global rows
+ * [src_row0, src_row0+src_rows); `above` (may be NULL) holds
+ * [above_row0, src_row0), `below` (may be NULL) holds
+ * [src_row0+src_rows, below_row0+below_rows). Output rows [out_lo,out_hi) go
+ * to dst (row 0 = global row dst_row0). The caller orders the neighbours'
+ * writes of those rows before this call (e.g. a stream-ordered barrier). */
+int sc_two_pass_band_peer_f32(const float *src, float *dst, int nplanes, int global_rows, int cols,
+                              int64_t src_plane_stride, int64_t dst_plane_stride,
+                              int64_t src_row_stride, int64_t dst_row_stride, int src_row0, int src_rows,
+                              const float *above, int above_row0, int above_rows,
+                              int64_t above_plane_stride, int64_t above_row_stride,
+                              const float *below, int below_row0, int below_rows,
+                              int64_t below_plane_stride, int64_t below_row_stride,
+                              int dst_row0, int out_lo, int out_hi, const float *taps, int width, int flags,
+                              void *stream);
+
+/* CUDA IPC for the band buffers: export a device buffer (64-byte handle of its
+ * allocation + the buffer's byte offset in it), map another process's buffer for
+ * use by `device` (peer access enabled on demand), and unmap it. */
+int sc_ipc_export(const void *dev_ptr, void *handle_out /* 64 bytes */, int64_t *offset_out);
+int sc_ipc_open(const void *handle /* 64 bytes */, int64_t offset, int device, void **ptr_out);
+int sc_ipc_close(void *ptr, int64_t offset);
+
 /* horizontal_rows_vec over rows [row_lo,row_hi) (S/conv.py:215-240; public
  * horizontal_pass uses [r, R-r), S/conv.py:362-375). SC_ZERO_FILL also zeroes
  * every other dst element (the two-pass scratch convention). */

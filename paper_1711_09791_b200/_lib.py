@@ -41,6 +41,10 @@ EXPORTS = (
     "sc_two_pass_fused_f32",
     "sc_two_pass_band_f32",
     "sc_two_pass_band2_f32",
+    "sc_two_pass_band_peer_f32",
+    "sc_ipc_export",
+    "sc_ipc_open",
+    "sc_ipc_close",
     "sc_hpass_f32",
     "sc_vpass_f32",
     "sc_two_pass_split_f32",
@@ -76,6 +80,11 @@ _SIGNATURES = {
     "sc_two_pass_fused_f32": (_STRIDED + [_fp, _i32, _i32, _vp], _i32),
     "sc_two_pass_band_f32": (_STRIDED + [_i32, _i32, _i32, _i32, _i32, _fp, _i32, _i32, _vp], _i32),
     "sc_two_pass_band2_f32": (_STRIDED + [_i32] * 7 + [_fp, _i32, _i32, _vp], _i32),
+    "sc_two_pass_band_peer_f32": (_STRIDED + [_i32, _i32, _vp, _i32, _i32, _i64, _i64, _vp, _i32, _i32, _i64, _i64,
+                                              _i32, _i32, _i32, _fp, _i32, _i32, _vp], _i32),
+    "sc_ipc_export": ([_vp, _vp, ctypes.POINTER(_i64)], _i32),
+    "sc_ipc_open": ([_vp, _i64, _i32, ctypes.POINTER(_vp)], _i32),
+    "sc_ipc_close": ([_vp, _i64], _i32),
     "sc_hpass_f32": (_STRIDED + [_i32, _i32, _fp, _i32, _i32, _vp], _i32),
     "sc_vpass_f32": (_STRIDED + [_i32, _i32, _fp, _i32, _i32, _vp], _i32),
     "sc_two_pass_split_f32": (_STRIDED + [_fp, _i32, _i32, _vp], _i32),

@@ -373,8 +373,11 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     const int rad = j.width / 2;
     const Knobs kn = read_knobs();
     const void* kern = nullptr;
+    const bool peers_aligned = (!j.above || (aligned16(j.above) && j.above_ps % 4 == 0 && j.above_rs % 4 == 0)) &&
+                               (!j.below || (aligned16(j.below) && j.below_ps % 4 == 0 && j.below_rs % 4 == 0));
     const bool aligned = (j.C % 4 == 0) && aligned16(j.src) && aligned16(j.dst) && (j.sps % 4 == 0) &&
-                         (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) && kn.force_generic == 0;
+                         (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) && peers_aligned &&
+                         kn.force_generic == 0;
     switch (j.mode) {
         case MODE_FUSED: kern = kernel_fused(rad, aligned); break;
         case MODE_HPASS: kern = kernel_hpass(rad, aligned); break;
@@ -387,7 +390,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
 
     // Kernel family: the TMA stage pipeline (default) or the register-streaming
     // direct kernel (SC_DIRECT=1), both bit-identical.
-    const bool direct = aligned && kn.direct != 0;
+    const bool direct = aligned && kn.direct != 0 && !j.above && !j.below;  // direct reads src only
     if (direct) {
         switch (j.mode) {
             case MODE_FUSED: kern = kernel_fused_direct(rad); break;
@@ -417,6 +420,16 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.C = j.C;
     p.src_row0 = j.src_row0;
     p.src_rows = j.src_rows;
+    p.avail_lo = j.above ? j.above_row0 : j.src_row0;
+    p.avail_hi = j.below ? j.below_row0 + j.below_rows : j.src_row0 + j.src_rows;
+    p.above = j.above;
+    p.below = j.below;
+    p.above_ps = j.above_ps;
+    p.above_rs = j.above_rs;
+    p.below_ps = j.below_ps;
+    p.below_rs = j.below_rs;
+    p.above_row0 = j.above_row0;
+    p.below_row0 = j.below_row0;
     p.dst_row0 = j.dst_row0;
     p.hrow_lo = j.hrow_lo;
     p.hrow_hi = j.hrow_hi;
@@ -640,6 +653,137 @@ int sc_two_pass_band2_f32(const float* src, float* dst, int nplanes, int global_
     j.width = width;
     j.taps = taps;
     return launch_rows(j, static_cast<cudaStream_t>(stream));
+}
+
+int sc_two_pass_band_peer_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
+                              int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                              int64_t dst_row_stride, int src_row0, int src_rows, const float* above,
+                              int above_row0, int above_rows, int64_t above_plane_stride, int64_t above_row_stride,
+                              const float* below, int below_row0, int below_rows, int64_t below_plane_stride,
+                              int64_t below_row_stride, int dst_row0, int out_lo, int out_hi, const float* taps,
+                              int width, int flags, void* stream) {
+    set_error("");
+    SC_TRY(check_width(width));
+    SC_TRY(check_dims(nplanes, global_rows, cols, width));
+    if (!taps) return fail(SC_INVALID_ARGUMENT, "null taps");
+    const int r = width / 2;
+    if (out_lo < 0 || out_hi > global_rows || out_lo > out_hi) return fail(SC_INVALID_ARGUMENT, "output rows out of range");
+    if (out_hi == out_lo) return SC_OK;
+    if (src_row0 < 0 || src_rows < 1 || src_row0 + src_rows > global_rows)
+        return fail(SC_INVALID_ARGUMENT, "source band outside the image");
+    // neighbours must be the adjacent bands: above ends where src starts, below starts where src ends
+    if (above && (above_rows < 1 || above_row0 < 0 || above_row0 + above_rows != src_row0))
+        return fail(SC_INVALID_ARGUMENT, "the band above must end at src_row0");
+    if (below && (below_rows < 1 || below_row0 != src_row0 + src_rows || below_row0 + below_rows > global_rows))
+        return fail(SC_INVALID_ARGUMENT, "the band below must start at src_row0 + src_rows");
+    const int avail_lo = above ? above_row0 : src_row0;
+    const int avail_hi = below ? below_row0 + below_rows : src_row0 + src_rows;
+    const int need_lo = out_lo - r > 0 ? out_lo - r : 0;
+    const int need_hi = out_hi + r < global_rows ? out_hi + r : global_rows;
+    if (avail_lo > need_lo || avail_hi < need_hi)
+        return fail(SC_INVALID_ARGUMENT, "source band and neighbours do not cover the output rows plus halo");
+    if (dst_row0 > out_lo) return fail(SC_INVALID_ARGUMENT, "destination band starts after the output rows");
+    SC_TRY(check_strides(nplanes, src_rows, cols, src_plane_stride, src_row_stride, "src"));
+    SC_TRY(check_strides(nplanes, out_hi - dst_row0, cols, dst_plane_stride, dst_row_stride, "dst"));
+    if (above) SC_TRY(check_strides(nplanes, above_rows, cols, above_plane_stride, above_row_stride, "above"));
+    if (below) SC_TRY(check_strides(nplanes, below_rows, cols, below_plane_stride, below_row_stride, "below"));
+    // the caller's own buffers pick the device; neighbours are peer mappings (never
+    // passed to the device selection, which would switch to their owning GPU)
+    SC_TRY(prepare(src));
+    SC_TRY(prepare(dst));
+    if (overlaps(src, extent_bytes(nplanes, src_rows, cols, src_plane_stride, src_row_stride), dst,
+                 extent_bytes(nplanes, out_hi - dst_row0, cols, dst_plane_stride, dst_row_stride)))
+        return fail(SC_INVALID_ARGUMENT, "source and destination must be distinct buffers");
+    RowsJob j{};
+    j.mode = MODE_FUSED;
+    j.src = src;
+    j.dst = dst;
+    j.sps = src_plane_stride;
+    j.dps = dst_plane_stride;
+    j.srs = src_row_stride;
+    j.drs = dst_row_stride;
+    j.nplanes = nplanes;
+    j.R = global_rows;
+    j.C = cols;
+    j.src_row0 = src_row0;
+    j.src_rows = src_rows;
+    j.dst_row0 = dst_row0;
+    j.out_lo = out_lo;
+    j.out_hi = out_hi;
+    j.hrow_lo = (flags & SC_EXTENDED) ? 0 : r;
+    j.hrow_hi = (flags & SC_EXTENDED) ? global_rows : global_rows - r;
+    j.flags = flags;
+    j.width = width;
+    j.taps = taps;
+    j.above = above;
+    j.above_row0 = above_row0;
+    j.above_rows = above_rows;
+    j.above_ps = above_plane_stride;
+    j.above_rs = above_row_stride;
+    j.below = below;
+    j.below_row0 = below_row0;
+    j.below_rows = below_rows;
+    j.below_ps = below_plane_stride;
+    j.below_rs = below_row_stride;
+    return launch_rows(j, static_cast<cudaStream_t>(stream));
+}
+
+// IPC: export a device buffer to another process (its allocation's handle plus the
+// buffer's offset inside the allocation), and map such a buffer into this process
+// on the CURRENT device (peer access over NVLink enabled on demand).
+typedef int (*AddrRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+int sc_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out) {
+    set_error("");
+    if (!ptr || !handle_out || !offset_out) return fail(SC_INVALID_ARGUMENT, "null argument");
+    SC_TRY(prepare(ptr));
+    static AddrRangeFn range = nullptr;
+    if (!range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            cudaGetLastError();
+            return fail(SC_CUDA_ERROR, "cuMemGetAddressRange unavailable");
+        }
+        range = reinterpret_cast<AddrRangeFn>(fn);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0)
+        return fail(SC_CUDA_ERROR, "cannot resolve the allocation of the buffer");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (int64_t)(reinterpret_cast<unsigned long long>(ptr) - base);
+    return SC_OK;
+}
+
+int sc_ipc_open(const void* handle, int64_t offset, int device, void** ptr_out) {
+    set_error("");
+    if (!handle || !ptr_out || offset < 0) return fail(SC_INVALID_ARGUMENT, "null argument or negative offset");
+    // this library carries its own CUDA runtime: its current device is not the
+    // caller's, so the device that will read the mapping is named explicitly
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != device) {
+        cudaError_t se = cudaSetDevice(device);
+        if (se != cudaSuccess) return cuda_fail(se, "cudaSetDevice");
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    *ptr_out = static_cast<char*>(base) + offset;
+    return SC_OK;
+}
+
+int sc_ipc_close(void* ptr, int64_t offset) {
+    set_error("");
+    if (!ptr) return fail(SC_INVALID_ARGUMENT, "null pointer");
+    cudaError_t e = cudaIpcCloseMemHandle(static_cast<char*>(ptr) - offset);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+    return SC_OK;
 }
 
 int sc_two_pass_band_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,

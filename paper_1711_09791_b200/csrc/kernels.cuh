@@ -77,6 +77,15 @@ struct Params {
     float one;               // 1.0f, passed at run time (see mad2)
     int* work;               // [next item, finished CTAs]: dynamic scheduling ticket pair (zero at launch)
     unsigned long long* trace;  // SC_TRACE builds only: per-CTA timeline (else null)
+    // Input rows the producer may fetch: [avail_lo, avail_hi). Rows of that range
+    // outside src's own [src_row0, src_row0 + src_rows) come from the neighbouring
+    // bands `above` / `below` (other GPUs' buffers mapped over NVLink, multi.py
+    // PeerBandStepper): the halo exchange is the kernel's own TMA reads.
+    int avail_lo, avail_hi;
+    const float* above;
+    const float* below;
+    long long above_ps, above_rs, below_ps, below_rs;
+    int above_row0, below_row0;  // global row of row 0 of above / below
     float w[MAX_W];
     float k[MAX_W * MAX_W];
 };
@@ -261,8 +270,8 @@ __device__ __forceinline__ Item decode_item(const Params& p, int item) {
         it.in_lo = it.ylo;
         it.in_hi = it.yhi;
     } else {
-        it.in_lo = max(max(it.ylo - RAD, 0), p.src_row0);
-        it.in_hi = min(min(it.yhi + RAD, p.R), p.src_row0 + p.src_rows);
+        it.in_lo = max(max(it.ylo - RAD, 0), p.avail_lo);
+        it.in_hi = min(min(it.yhi + RAD, p.R), p.avail_hi);
     }
     return it;
 }
@@ -275,6 +284,16 @@ __device__ __forceinline__ bool item_rows_edge(const Params& p, const Item& it) 
     if (MODE == MODE_FUSED)
         return it.in_lo < p.hrow_lo || it.in_hi > p.hrow_hi || it.ylo < RAD || it.yhi > p.R - RAD;
     return false;
+}
+
+// Global input row y of `plane`: from this band's buffer, or from a neighbouring
+// band's (peer) buffer for halo rows outside it.
+__device__ __forceinline__ const float* src_row(const Params& p, int plane, int y) {
+    if (y < p.src_row0)
+        return p.above + (long long)plane * p.above_ps + (long long)(y - p.above_row0) * p.above_rs;
+    if (y >= p.src_row0 + p.src_rows)
+        return p.below + (long long)plane * p.below_ps + (long long)(y - p.below_row0) * p.below_rs;
+    return p.src + (long long)plane * p.src_plane_stride + (long long)(y - p.src_row0) * p.src_row_stride;
 }
 
 // ---------------------------------------------------------------------------
@@ -329,31 +348,29 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
         const int cx0 = max(it.x0 - HALO, 0);
         const int cx1 = min(it.x0 + p.tw + HALO, p.C);
         const int n = cx1 - cx0;
-        const float* gbase = p.src + (long long)it.plane * p.src_plane_stride + cx0;
         const int soff = cx0 - (it.x0 - HALO);
         for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
             if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
             const int nrows = min(SROWS, it.in_hi - r0);
             float* sbase = ring + slot * SROWS * SW + soff;
-            const float* g0 = gbase + (long long)(r0 - p.src_row0) * p.src_row_stride;
             sitem[slot] = item;
             if (ALIGNED) {
                 const uint32_t bytes = (uint32_t)n * 4u;
                 mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
                 for (int k = 0; k < nrows; ++k)
-                    bulk_g2s(sbase + k * SW, g0 + (long long)k * p.src_row_stride, bytes, &full[slot], pol);
+                    bulk_g2s(sbase + k * SW, src_row(p, it.plane, r0 + k) + cx0, bytes, &full[slot], pol);
             } else {
                 // the segment [g, g+n) lands at the 16-B aligned smem index 4 + soff, preceded
                 // by its shift s = (g mod 16 B) / 4 floats: column c sits at c - x0 + 8 + s
                 uint32_t total = 0;
                 for (int k = 0; k < nrows; ++k) {
-                    const uintptr_t a = reinterpret_cast<uintptr_t>(g0 + (long long)k * p.src_row_stride);
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(src_row(p, it.plane, r0 + k) + cx0);
                     const uintptr_t e = a + 4u * (uintptr_t)n;
                     total += (uint32_t)(((e + 15) & ~(uintptr_t)15) - (a & ~(uintptr_t)15));
                 }
                 mbar_arrive_expect_tx(&full[slot], total);
                 for (int k = 0; k < nrows; ++k) {
-                    const uintptr_t a = reinterpret_cast<uintptr_t>(g0 + (long long)k * p.src_row_stride);
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(src_row(p, it.plane, r0 + k) + cx0);
                     const uintptr_t a_dn = a & ~(uintptr_t)15;
                     const uintptr_t e_up = (a + 4u * (uintptr_t)n + 15) & ~(uintptr_t)15;
                     sshift[slot * SROWS + k] = (int)((a - a_dn) >> 2);

@@ -46,6 +46,12 @@ struct RowsJob {
     int width;
     const float* taps;   // width floats (host)
     const float* dense;  // width*width floats (host), SINGLE only
+    // optional neighbouring bands (peer memory) holding the halo rows just above /
+    // below [src_row0, src_row0 + src_rows); rows 0 = global rows above_row0 / below_row0
+    const float* above = nullptr;
+    const float* below = nullptr;
+    long long above_ps = 0, above_rs = 0, below_ps = 0, below_rs = 0;
+    int above_row0 = 0, above_rows = 0, below_row0 = 0, below_rows = 0;
 };
 
 // Plans and launches one row-streaming kernel; returns an SC_* status and sets

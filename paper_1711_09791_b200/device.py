@@ -126,6 +126,76 @@ def two_pass_band(src: torch.Tensor, taps, out: torch.Tensor, *, global_rows: in
     return out
 
 
+class PeerRows:
+    """Rows [row0, row0 + rows) of every plane of a neighbouring band, at a device
+    address valid in this process (a local tensor, or another process's buffer
+    mapped with ipc_open). Strides in floats."""
+
+    __slots__ = ("ptr", "row0", "rows", "plane_stride", "row_stride", "keep")
+
+    def __init__(self, ptr: int, row0: int, rows: int, plane_stride: int, row_stride: int, keep=None):
+        self.ptr, self.row0, self.rows = int(ptr), int(row0), int(rows)
+        self.plane_stride, self.row_stride = int(plane_stride), int(row_stride)
+        self.keep = keep  # object owning the memory (kept alive)
+
+    @classmethod
+    def of(cls, t: torch.Tensor, row0: int) -> "PeerRows":
+        _, R, _, ps, rs = _planes(t, "neighbour band")
+        return cls(t.data_ptr(), row0, R, ps, rs, keep=t)
+
+
+def two_pass_band_peer(src: torch.Tensor, taps, out: torch.Tensor, *, global_rows: int, src_row0: int,
+                       dst_row0: int, out_lo: int, out_hi: int, above: PeerRows | None = None,
+                       below: PeerRows | None = None, extended: bool = False) -> torch.Tensor:
+    """Row band whose halo rows come straight from the neighbouring bands' memory
+    (no exchange step): src holds global rows [src_row0, src_row0 + src.shape[-2])."""
+    w = _taps(taps)
+    n, Rs, C, sps, srs = _planes(src, "src")
+    n2, Rd, C2, dps, drs = _planes(out, "out")
+    if n2 != n or C2 != C:
+        raise InvalidArgumentError("band source and destination plane counts / widths differ")
+    if out_hi - dst_row0 > Rd:
+        raise InvalidArgumentError("destination band too short for the output rows")
+    a = above or PeerRows(0, 0, 0, 0, 0)
+    b = below or PeerRows(0, 0, 0, 0, 0)
+    L = _lib.load()
+    _lib.check(L.sc_two_pass_band_peer_f32(
+        src.data_ptr(), out.data_ptr(), n, global_rows, C, sps, dps, srs, drs, src_row0, Rs,
+        a.ptr or None, a.row0, a.rows, a.plane_stride, a.row_stride,
+        b.ptr or None, b.row0, b.rows, b.plane_stride, b.row_stride,
+        dst_row0, out_lo, out_hi, _fp(w), w.size, _lib.SC_EXTENDED if extended else 0, _stream(src)))
+    return out
+
+
+def ipc_export(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t in it)."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidArgumentError("ipc_export needs a CUDA tensor")
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    L = _lib.load()
+    _lib.check(L.sc_ipc_export(t.data_ptr(), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_open(handle: bytes, offset: int, device: int | None = None) -> int:
+    """Map another process's exported buffer for `device` (default: torch's current
+    device); returns its address in this process."""
+    if len(handle) != 64:
+        raise InvalidArgumentError("an IPC handle is 64 bytes")
+    if device is None:
+        device = torch.cuda.current_device()
+    ptr = ctypes.c_void_p(0)
+    L = _lib.load()
+    _lib.check(L.sc_ipc_open(handle, int(offset), int(device), ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    L = _lib.load()
+    _lib.check(L.sc_ipc_close(ptr, int(offset)))
+
+
 def hpass(src: torch.Tensor, taps, out: torch.Tensor, row_lo: int | None = None, row_hi: int | None = None,
           *, zero_fill: bool = False) -> torch.Tensor:
     """horizontal_rows_vec (S/conv.py:215-240) over rows [row_lo, row_hi) (default: valid rows)."""

@@ -94,3 +94,62 @@ def test_band_plan_rules():
         band_plan(10, 0, 8, 2)  # bands shorter than the radius
     assert [frame_shard(512, r, 8) for r in (0, 7)] == [(0, 64), (448, 512)]
     assert sum(b - a for a, b in (frame_shard(513, r, 4) for r in range(4))) == 513
+
+
+def _meta_worker(rank, world, port, R, q):
+    import torch.distributed as dist
+
+    from paper_1711_09791_b200.multi import PeerMeta, band_plan, peer_neighbours, publish_peer_meta
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        band = band_plan(R, rank, world, 2)
+        handle = bytes([rank]) * 64  # stands in for the CUDA IPC handle
+        me = PeerMeta(rank, band.lo, band.hi, handle, 128 * rank, 7 * R, 7, 7, 3)
+        above, below = peer_neighbours(publish_peer_meta(me, band), band)
+        ok = (above is None) == (rank == 0) and (below is None) == (rank == world - 1)
+        if above is not None:
+            ok = ok and above.rank == rank - 1 and above.hi == band.lo and above.handle == bytes([rank - 1]) * 64
+            ok = ok and above.offset == 128 * (rank - 1)
+        if below is not None:
+            ok = ok and below.rank == rank + 1 and below.lo == band.hi and below.handle == bytes([rank + 1]) * 64
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_metadata_exchange(world):
+    """The peer (in-kernel halo) path's only host collective: every rank publishes
+    its band buffer's IPC handle + geometry and picks its two neighbours."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_meta_worker, args=(r, world, port, 41, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    results = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(results[r] for r in range(world)), results
+
+
+def test_peer_neighbour_validation():
+    from paper_1711_09791_b200.errors import InvalidArgumentError
+    from paper_1711_09791_b200.multi import PeerMeta, band_plan, peer_neighbours
+
+    R, world = 30, 3
+    bands = [band_plan(R, r, world, 2) for r in range(world)]
+    metas = [PeerMeta(b.rank, b.lo, b.hi, b"\0" * 64, 0, 100, 10, 10, 3) for b in bands]
+    above, below = peer_neighbours(metas, bands[1])
+    assert (above.rank, below.rank) == (0, 2)
+    assert peer_neighbours(metas, bands[0])[0] is None and peer_neighbours(metas, bands[2])[1] is None
+    with pytest.raises(InvalidArgumentError):  # a gap between bands
+        peer_neighbours([metas[0], PeerMeta(1, 11, 20, b"\0" * 64, 0, 100, 10, 10, 3), metas[2]], bands[1])
+    with pytest.raises(InvalidArgumentError):  # width mismatch
+        peer_neighbours([metas[0], metas[1], PeerMeta(2, 20, 30, b"\0" * 64, 0, 100, 10, 11, 3)], bands[1])
+    with pytest.raises(InvalidArgumentError):  # missing neighbour
+        peer_neighbours([metas[1], metas[2]], bands[1])

@@ -1,0 +1,158 @@
+"""In-kernel halo reads from neighbouring bands (multi-GPU without an exchange
+step): the band kernel fetches the r halo rows straight from the adjacent bands'
+memory. Bit-identical to the whole-image two-pass.
+
+On this one-GPU pool the neighbours are (a) other tensors in the same process
+and (b) another PROCESS's buffers mapped with CUDA IPC (the same mechanism as
+across GPUs, minus NVLink). The bands are written and synchronised before any
+kernel runs, so no kernel ever waits on another."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_09791_b200 import device
+
+    return device
+
+
+@pytest.mark.parametrize("R,C,world,taps,extended", [
+    (300, 1000, 3, [1, 4, 6, 4, 1], False),
+    (301, 999, 4, [-1, -2, 7, -2, -1], True),     # unaligned rows (generic producer)
+    (64, 256, 8, [0.25, 0.5, 0.25], False),
+    (97, 130, 5, [1, 2, 3, 4, 5, 4, 3, 2, 1], False),
+    (40, 64, 2, [0.1, 0.2, 0.4, 0.2, 0.1, 0.3, 0.7], True),
+])
+def test_peer_bands_match_whole_image(dev, R, C, world, taps, extended):
+    from paper_1711_09791_b200.multi import band_plan
+
+    w = np.asarray(taps, dtype=np.float32)
+    w /= w.sum()
+    x = dev.synthetic((3, R, C), 11, 1)
+    want = dev.two_pass(x, w, extended=extended).cpu().numpy()
+    r = len(w) // 2
+    bands = [band_plan(R, k, world, r) for k in range(world)]
+    owned = [x[:, b.lo:b.hi].clone() for b in bands]  # each band its own buffer, owned rows only
+    got = np.empty_like(want)
+    for k, b in enumerate(bands):
+        out = torch.full((3, b.hi - b.lo, C), float("nan"), device="cuda")
+        above = dev.PeerRows.of(owned[k - 1], bands[k - 1].lo) if k > 0 else None
+        below = dev.PeerRows.of(owned[k + 1], bands[k + 1].lo) if k < world - 1 else None
+        dev.two_pass_band_peer(owned[k], w, out, global_rows=R, src_row0=b.lo, dst_row0=b.lo, out_lo=b.lo,
+                               out_hi=b.hi, above=above, below=below, extended=extended)
+        got[:, b.lo:b.hi] = out.cpu().numpy()
+    assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_peer_band_validation(dev):
+    from paper_1711_09791_b200.errors import InvalidArgumentError
+
+    w = np.array([1, 4, 6, 4, 1], np.float32) / 16
+    x = dev.synthetic((3, 60, 64), 1, 1)
+    top, mid = x[:, :20].clone(), x[:, 20:40].clone()
+    out = torch.empty((3, 20, 64), device="cuda")
+    with pytest.raises(InvalidArgumentError):  # no halo source for rows 18, 19
+        dev.two_pass_band_peer(mid, w, out, global_rows=60, src_row0=20, dst_row0=20, out_lo=20, out_hi=40)
+    with pytest.raises(InvalidArgumentError):  # the band above must end at src_row0
+        dev.two_pass_band_peer(mid, w, out, global_rows=60, src_row0=20, dst_row0=20, out_lo=20, out_hi=40,
+                               above=dev.PeerRows.of(top[:, :18], 0))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _ipc_worker(rank, world, port, R, C, q):
+    import torch.distributed as dist
+
+    from paper_1711_09791_b200 import device as dev
+    from paper_1711_09791_b200.multi import PeerBandStepper, band_plan
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        w = np.array([-1, -2, 7, -2, -1], np.float32)
+        x = dev.synthetic((3, R, C), 5, 2)  # every rank can regenerate the image: check its own band
+        want = dev.two_pass(x, w).cpu().numpy()
+        band = band_plan(R, rank, world, 2)
+        src = x[:, band.lo:band.hi].clone()
+        dst = torch.full_like(src, float("nan"))
+        del x
+        stepper = PeerBandStepper(src, dst, band, w)
+        stepper.sync()          # every band written before any kernel reads a neighbour
+        for _ in range(3):
+            stepper.step()      # inputs fixed across steps: no per-step synchronisation needed
+        torch.cuda.synchronize()
+        ok = np.array_equal(_bits(dst.cpu().numpy()), _bits(want[:, band.lo:band.hi]))
+        dist.barrier()          # neighbours stop reading before anyone unmaps / frees
+        stepper.close()
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_stepper_over_cuda_ipc(world):
+    """Each process maps its neighbours' band buffers with CUDA IPC; one launch per
+    step reads the halo rows from them. Result: the whole-image bits."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, 203, 1024, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    results = dict(q.get(timeout=5) for _ in range(world))
+    assert all(results[r] for r in range(world)), results
+
+
+@pytest.mark.parametrize("halo", ["peer", "nccl"])
+def test_bench_two_ranks_on_one_gpu(halo):
+    """bench.py's N>1 row-band step, both halo transports, as 2 torchrun ranks
+    sharing this GPU (gloo for the host-side collectives; NCCL mode stages the
+    halo through host memory). It must print one well-formed JSON line."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    port = _free_port()
+    env = dict(os.environ, SEPCONV_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config",
+           "cfg3", "--steps", "5", "--warmup", "3", "--e2e-steps", "1", "--halo", halo]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["halo"] == halo and line["value"] > 0
+    assert line["gpu_launches"] >= 5 and line["e2e"]["value"] > 0
