@@ -46,7 +46,7 @@ static int cuda_fail(cudaError_t e, const char* what) {
 // while the common case costs no getenv() per knob.
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
-    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0;
+    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
 };
 
 static Knobs read_knobs() {
@@ -70,6 +70,7 @@ static Knobs read_knobs() {
         else if (name == "TAIL_WAVES") k.tail_waves = v;
         else if (name == "EXACT_WAVES") k.exact_waves = v;
         else if (name == "IPC") k.ipc = v;
+        else if (name == "NO_STAGE") k.no_stage = v;
     }
     return k;
 }
@@ -200,7 +201,9 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     if (ns_req > 32) ns_req = 32;
     auto smem_for = [&](int tw_, int ns_) {
         const int sw = aligned ? tw_ + 2 * HALO : tw_ + 2 * HALO + 16;  // row_width<ALIGNED>
-        return (size_t)((2 * ns_ * 8 + ns_ * 4 + ns_ * SROWS * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * sw * 4;
+        const size_t staging = aligned ? 0 : (size_t)2 * SROWS * (tw_ + 8) * 4;  // unaligned output staging
+        return (size_t)((2 * ns_ * 8 + ns_ * 4 + ns_ * SROWS * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * sw * 4 +
+               staging;
     };
     // an SC_NS ring deeper than shared memory holds for the narrowest strip is clamped
     while (ns_req > lags + 2 && smem_for(COLS_PER_THREAD * 64, ns_req) > 227 * 1024) --ns_req;
@@ -436,6 +439,10 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.flags = j.flags;
     p.one = 1.0f;
     if (kn.l2_evict_first) p.flags |= F_L2_EVICT_FIRST;
+    // unaligned kernels stage their output rows only when the DESTINATION rows are
+    // not all 16-B aligned (a misaligned source alone keeps direct stores)
+    const bool dst_aligned = (j.C % 4 == 0) && aligned16(j.dst) && (j.dps % 4 == 0) && (j.drs % 4 == 0);
+    if (!aligned && !dst_aligned && !kn.no_stage) p.flags |= F_STAGED_STORE;
     for (int i = 0; i < j.width; ++i) p.w[i] = j.taps ? j.taps[i] : 0.0f;
     if (j.dense)
         for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];

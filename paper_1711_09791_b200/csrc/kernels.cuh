@@ -45,6 +45,7 @@ constexpr int F_EXTENDED = 0x1;
 constexpr int F_NO_RING = 0x2;
 constexpr int F_ZERO_FILL = 0x4;
 // tuning flags (set by the planner from SC_* environment variables)
+constexpr int F_STAGED_STORE = 0x200;  // unaligned kernels: dst rows not all 16-B aligned -> staged TMA stores
 constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (default: evict_normal,
                                          // which lets neighbouring bands' halo rows hit in L2)
 
@@ -167,6 +168,20 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
             smem_u32(sdst)),
         "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+
+// Bulk shared -> global copy (TMA store, bulk-group completion) and its fences.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void consumer_bar(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ uint64_t policy_evict_normal() {
@@ -647,14 +662,52 @@ __device__ __forceinline__ void store_shift(float* drow, int x4, int C, int rad,
     }
 }
 
+// Unaligned rows: each output row of a strip is first assembled in a shared
+// staging row whose 16-B alignment matches the global row's (staging index of
+// column x = x - x0 + s, s = (row address / 4 + x0) mod 4), then written by ONE
+// bulk TMA store for its aligned middle plus <= 3 scalar stores at each end
+// (instead of realigning every warp's columns with shuffles and split-off
+// scalar stores at every warp edge). Columns the policy must not touch are
+// never staged and never stored.
+__device__ __forceinline__ int row_shift(const float* drow, int x0) {
+    return (int)(((reinterpret_cast<uintptr_t>(drow) >> 2) + (uintptr_t)x0) & 3u);
+}
+
+__device__ __forceinline__ void stage_cols(float* srow, int x4, int x0, int C, int rad, const F4& val,
+                                           const F4& ringv, int ring_mode) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int col = x4 + c;
+        const bool valid = col >= rad && col < C - rad;
+        if (col < C && (valid || ring_mode != 0))
+            srow[col - x0] = valid ? val.v[c] : (ring_mode == 1 ? ringv.v[c] : 0.0f);
+    }
+}
+
+// Columns [c_lo, c_hi) of a staged row -> global row (called by one warp).
+__device__ __forceinline__ void publish_row(float* drow, const float* srow, int x0, int c_lo, int c_hi, int lane) {
+    if (c_hi <= c_lo) return;
+    const uintptr_t f = reinterpret_cast<uintptr_t>(drow) >> 2;  // row start in floats
+    int a_lo = c_lo + (int)((4u - (unsigned)((f + (uintptr_t)c_lo) & 3u)) & 3u);
+    int a_hi = c_hi - (int)((f + (uintptr_t)c_hi) & 3u);
+    if (a_lo > c_hi) a_lo = c_hi;
+    if (a_hi < a_lo) a_hi = a_lo;
+    if (lane == 0 && a_hi > a_lo) bulk_s2g(drow + a_lo, srow + (a_lo - x0), 4u * (uint32_t)(a_hi - a_lo));
+    // the unaligned ends: [c_lo, a_lo) (<= 3 columns) and [a_hi, c_hi) (<= 7)
+    const int l = c_lo + lane;
+    if (l < a_lo) drow[l] = srow[l - x0];
+    const int r = a_hi + lane;
+    if (r < c_hi && lane < 8) drow[r] = srow[r - x0];
+}
+
 // ---------------------------------------------------------------------------
 // Consumer: one item (plane, strip, band). ROW_EDGE items contain ring rows or
 // rows with a dead row pass; all others run the lean loop.
 
 template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE>
 __device__ __forceinline__ void consume_item(const Params& p, const Item& it, const float* ring, uint64_t* full,
-                                             uint64_t* empty, const int* sshift, int& slot, uint32_t& phase,
-                                             int& gs) {
+                                             uint64_t* empty, const int* sshift, float* stage_out, int& slot,
+                                             uint32_t& phase, int& gs) {
     constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
     const int SW = row_width<ALIGNED>(p.tw);
     const int NS = p.ns;
@@ -665,6 +718,9 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
     const int R = p.R, C = p.C;
     const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);
     const bool zero_fill = (MODE == MODE_HPASS) && (p.flags & F_ZERO_FILL);
+    // unaligned kernels with 16-B aligned destination rows (only the source is
+    // misaligned) store directly; staging pays only when the stores are unaligned
+    const bool staged = !ALIGNED && (p.flags & F_STAGED_STORE);
 
     int x4[GROUPS];
     bool fast[GROUPS];
@@ -709,6 +765,11 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                 const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
                 const bool emit = yo >= emit_lo && yo < emit_hi;
                 const int shift = ALIGNED ? 0 : sshift[slot * SROWS + k];
+                // unaligned: this row's staging row, indexed so that srow[x - x0] has the
+                // global column's 16-B alignment
+                float* srow = nullptr;
+                if (staged)
+                    srow = stage_out + ((gs & 1) * SROWS + k) * (p.tw + 8) + row_shift(dcur, it.x0);
 #pragma unroll
                 for (int g = 0; g < GROUPS; ++g) {
                     // a warp whose group lies wholly right of the image (the padding of a
@@ -761,6 +822,8 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                         if (emit && (live || zero_fill)) {
                             if (fast[g] && live)
                                 st4(dcur + 4 * ct + g * tw2 + (it.x0), outv);
+                            else if (staged)
+                                stage_cols(srow, x4[g], it.x0, C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
                             else if (!ALIGNED)
                                 store_shift(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0, lane);
                             else
@@ -788,6 +851,8 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                             }
                             if (ALIGNED)
                                 store_edge<ALIGNED>(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                            else if (staged)
+                                stage_cols(srow, x4[g], it.x0, C, RAD, outv, ringv, ring_copy ? 1 : 0);
                             else
                                 store_shift(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0, lane);
                         }
@@ -801,6 +866,44 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                     }
                 }
                 if (emit) dcur += p.dst_row_stride;
+            }
+        }
+        if (staged) {
+            // publish the stage's staged output rows: fence the generic-proxy smem
+            // writes for the TMA engine, make sure the bulk stores of the previous
+            // stage have read their (other) buffer, then one warp issues this stage's
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < SROWS; ++k) {
+                const int yi = r0 + k;
+                const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
+                any = any || (yi < it.in_hi && yo >= emit_lo && yo < emit_hi);
+            }
+            if (any) {
+                fence_proxy_async_smem();
+                if (ct == 0) bulk_wait_read0();
+                consumer_bar((int)blockDim.x - 32);
+                if (ct < 32) {
+#pragma unroll
+                    for (int k = 0; k < SROWS; ++k) {
+                        const int yi = r0 + k;
+                        const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
+                        if (yi >= it.in_hi || yo < emit_lo || yo >= emit_hi) continue;
+                        const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
+                        int c_lo = RAD, c_hi = C - RAD;  // VPASS, SINGLE: valid columns only
+                        if (MODE == MODE_FUSED && ring_copy) { c_lo = 0; c_hi = C; }
+                        if (MODE == MODE_HPASS) {
+                            if (!live && !zero_fill) continue;
+                            if (zero_fill) { c_lo = 0; c_hi = C; }
+                        }
+                        c_lo = max(c_lo, it.x0);
+                        c_hi = min(c_hi, it.x0 + p.tw);
+                        float* drow = dplane + (long long)(yo - p.dst_row0) * p.dst_row_stride;
+                        const float* srow = stage_out + ((gs & 1) * SROWS + k) * (p.tw + 8) + row_shift(drow, it.x0);
+                        publish_row(drow, srow, it.x0, c_lo, c_hi, lane);
+                    }
+                    if (ct == 0) bulk_commit();
+                }
             }
         }
 #ifdef SC_TRACE
@@ -834,6 +937,8 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     int* sitem = reinterpret_cast<int*>(empty + NS);
     int* sshift = sitem + NS;  // per ring row (NS * SROWS): float shift of an unaligned row
     float* ring = reinterpret_cast<float*>(smem_raw + ((2 * NS * 8 + NS * 4 + NS * SROWS * 4 + 127) / 128) * 128);
+    // unaligned kernels: 2 x SROWS staging rows of tw + 8 floats after the ring
+    float* stage_out = ring + NS * SROWS * row_width<ALIGNED>(p.tw);
     const int warp = threadIdx.x >> 5;
     const int ncw = (blockDim.x >> 5) - 1;
 
@@ -875,14 +980,15 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
         if (item_rows_edge<MODE, RAD>(p, it))
-            consume_item<MODE, RAD, ALIGNED, true>(p, it, ring, full, empty, sshift, slot, phase, gs);
+            consume_item<MODE, RAD, ALIGNED, true>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
         else
-            consume_item<MODE, RAD, ALIGNED, false>(p, it, ring, full, empty, sshift, slot, phase, gs);
+            consume_item<MODE, RAD, ALIGNED, false>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
 #ifdef SC_TRACE
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 30 + ntr, clock64());
         ++ntr;
 #endif
     }
+    if (!ALIGNED && threadIdx.x == 32) bulk_wait_all();  // staged rows fully stored before smem goes away
 #ifdef SC_TRACE
     if (threadIdx.x == 32) {
         SC_TR(p, 40, clock64());
