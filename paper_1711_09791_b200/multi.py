@@ -177,6 +177,38 @@ def band_two_pass(local_src, local_dst, band: Band, taps, *, extended: bool = Fa
         fn(local_src, local_dst, out_lo=i_hi, out_hi=band.hi, **common)
 
 
+def band_two_pass_split(local, scratch, band: Band, taps, *, extended: bool = False, group=None,
+                        exchange: bool = True, hpass_fn=None, vpass_fn=None) -> None:
+    """The two-pass SPLIT mode (K2 + K3) on a row band, in place, with the
+    reference's buffer end state (third row; conv_two_pass,
+    S/conv.py:392-421): after the halo exchange, the row pass fills the band's
+    scratch with H0 (zero outside the live rows and on the column ring; the halo
+    rows' H0 is recomputed locally -- the row pass is row-local), then the column
+    pass writes V(H0) into the owned rows of `local`. Owned rows of `local` end as
+    the reference's image, owned rows of `scratch` as its workspace.
+
+    local, scratch: (P, band.local_rows, C). hpass_fn(src, dst, row_lo, row_hi) /
+    vpass_fn(src, dst, row_lo, row_hi) work on band-local rows (defaults: the
+    CUDA row and column passes; the CPU tests pass the oracle's)."""
+    r = band.radius
+    if hpass_fn is None or vpass_fn is None:
+        from . import device
+
+        hpass_fn = hpass_fn or (lambda s, d, lo, hi: device.hpass(s, taps, d, lo, hi, zero_fill=True))
+        vpass_fn = vpass_fn or (lambda s, d, lo, hi: device.vpass(s, taps, d, lo, hi))
+    if exchange:
+        for w in exchange_halos(local, band, group):
+            w.wait()
+    live_lo, live_hi = (0, band.rows) if extended else (r, band.rows - r)
+    h_lo = max(live_lo, band.in_lo) - band.in_lo
+    h_hi = min(live_hi, band.in_hi) - band.in_lo
+    hpass_fn(local, scratch, h_lo, max(h_lo, h_hi))
+    v_lo = max(band.lo, r) - band.in_lo
+    v_hi = min(band.hi, band.rows - r) - band.in_lo
+    if v_hi > v_lo:
+        vpass_fn(scratch, local, v_lo, v_hi)
+
+
 class BandStepper:
     """Prepared banded two-pass step for a fixed pair of band buffers.
 

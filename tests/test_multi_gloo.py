@@ -153,3 +153,58 @@ def test_peer_neighbour_validation():
         peer_neighbours([metas[0], metas[1], PeerMeta(2, 20, 30, b"\0" * 64, 0, 100, 10, 11, 3)], bands[1])
     with pytest.raises(InvalidArgumentError):  # missing neighbour
         peer_neighbours([metas[1], metas[2]], bands[1])
+
+
+def _split_worker(rank, world, port, R, C, P, taps, extended, q):
+    import torch.distributed as dist
+
+    from oracle import oracle as orc
+    from paper_1711_09791_b200.multi import band_plan, band_two_pass_split
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = np.asarray(taps, dtype=np.float32)
+        full = orc.synthetic(P * R * C, 17, kind=2).reshape(P, R, C)
+        band = band_plan(R, rank, world, len(w) // 2)
+        local = torch.full((P, band.local_rows, C), float("nan"))
+        local[:, band.owned] = torch.from_numpy(full[:, band.lo:band.hi])
+        scratch = torch.zeros((P, band.local_rows, C))  # the reference's zero workspace
+
+        def hp(s, d, lo, hi):
+            for p in range(P):
+                orc.horizontal_rows(s[p].numpy(), d[p].numpy(), w, lo, hi)
+
+        def vp(s, d, lo, hi):
+            for p in range(P):
+                orc.vertical_rows(s[p].numpy(), d[p].numpy(), w, lo, hi)
+
+        band_two_pass_split(local, scratch, band, w, extended=extended, hpass_fn=hp, vpass_fn=vp)
+        own = slice(band.lo - band.in_lo, band.hi - band.in_lo)
+        want_img = orc.two_pass(full, w, extended=extended)[:, band.lo:band.hi]
+        want_scr = orc.two_pass_scratch(full, w, extended=extended)[:, band.lo:band.hi]
+        ok = np.array_equal(local[:, own].numpy().view(np.uint32), want_img.view(np.uint32))
+        ok = ok and np.array_equal(scratch[:, own].numpy().view(np.uint32), want_scr.view(np.uint32))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,R,extended", [(2, 37, False), (3, 41, True), (4, 23, False)])
+def test_band_split_mode_matches_reference_state(world, R, extended):
+    """Split two-pass (K2 + K3) on row bands: owned image rows AND owned scratch
+    rows equal the reference's end state bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    taps = [-1.0, -2.0, 7.0, -2.0, -1.0]
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, R, 29, 3, taps, extended, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    results = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(results[r] for r in range(world)), results

@@ -156,3 +156,26 @@ def test_bench_two_ranks_on_one_gpu(halo):
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["config"]["halo"] == halo and line["value"] > 0
     assert line["gpu_launches"] >= 5 and line["e2e"]["value"] > 0
+
+
+@pytest.mark.parametrize("world,extended", [(3, False), (4, True)])
+def test_band_split_mode_on_gpu(dev, oracle, world, extended):
+    """band_two_pass_split with the CUDA row/column passes on every band of one
+    image (halo rows pre-filled, as the exchange would): owned image and scratch
+    rows equal the reference's end state."""
+    from paper_1711_09791_b200.multi import band_plan, band_two_pass_split
+
+    R, C = 203, 517
+    w = np.array([-1, -2, 7, -2, -1], np.float32)
+    full = dev.synthetic((3, R, C), 3, 2)
+    fh = full.cpu().numpy()
+    want_img = oracle.two_pass(fh, w, extended=extended)
+    want_scr = oracle.two_pass_scratch(fh, w, extended=extended)
+    for k in range(world):
+        b = band_plan(R, k, world, 2)
+        local = full[:, b.in_lo:b.in_hi].clone()
+        scratch = torch.full_like(local, float("nan"))  # zero fill must overwrite everything
+        band_two_pass_split(local, scratch, b, w, extended=extended, exchange=False)
+        own = slice(b.lo - b.in_lo, b.hi - b.in_lo)
+        assert np.array_equal(_bits(local[:, own].cpu().numpy()), _bits(want_img[:, b.lo:b.hi]))
+        assert np.array_equal(_bits(scratch[:, own].cpu().numpy()), _bits(want_scr[:, b.lo:b.hi]))
