@@ -6,9 +6,14 @@
 
 namespace sc {
 
-const void* kernel_single(int rad, bool aligned) {
+const void* kernel_single(int rad, bool aligned, bool sym) {
+    // symmetric-tap variants exist for r >= 1 (r = 0 has a single tap)
+    sym = sym && rad >= 1;
 #define SC_K(R)                                                                                   \
     case R:                                                                                       \
+        if (sym)                                                                                  \
+            return aligned ? (const void*)sepconv_rows_kernel<MODE_SINGLE, R, true, (R >= 1)>          \
+                           : (const void*)sepconv_rows_kernel<MODE_SINGLE, R, false, (R >= 1)>;        \
         return aligned ? (const void*)sepconv_rows_kernel<MODE_SINGLE, R, true>                       \
                        : (const void*)sepconv_rows_kernel<MODE_SINGLE, R, false>;
     switch (rad) {

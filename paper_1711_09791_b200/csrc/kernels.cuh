@@ -544,6 +544,54 @@ __device__ __forceinline__ F4 dense_fold(F4 (&acc)[NACC], const float (&win)[12]
     return out;
 }
 
+// Single pass with a mirror-symmetric dense matrix (K[i][j] == K[2r-i][j]
+// bitwise, e.g. outer(w, w) of symmetric taps: gaussian5, sigma1 and the sharpen
+// taps of the BASELINE configs): the products of kernel rows i and 2r-i are
+// identical IEEE results of the same operands, so each is computed once and
+// used twice. Fold order and every rounding are unchanged (bit-identical);
+// (2r+1)*r fewer multiplies per input row (25 -> 15 at r = 2) in an FP32-bound
+// kernel.
+__device__ __forceinline__ float2 add2p(float2 acc, float2 prod, float2 one) {
+    return __ffma2_rn(prod, one, acc);  // acc + prod, one rounding (see mad2)
+}
+
+template <int RAD, int NACC>
+__device__ __forceinline__ F4 dense_fold_sym(F4 (&acc)[NACC], const float (&win)[12], const float* k, float one) {
+    static_assert(RAD >= 1, "symmetric fold needs RAD >= 1");
+    constexpr int W = 2 * RAD + 1;
+    F4 out;
+    const float2 one2 = make_float2(one, one);
+#pragma unroll
+    for (int c = 0; c < 4; c += 2) {
+        const int o = HALO - RAD + c;
+        float2 pr[RAD + 1][W];  // products of kernel rows 0..RAD (rows 2r..RAD+1 mirror them)
+#pragma unroll
+        for (int i = 0; i <= RAD; ++i)
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                pr[i][j] = __fmul2_rn(make_float2(win[o + j], win[o + j + 1]), make_float2(k[i * W + j], k[i * W + j]));
+        float2 t = make_float2(acc[NACC - 1].v[c], acc[NACC - 1].v[c + 1]);
+#pragma unroll
+        for (int j = 0; j < W; ++j) t = add2p(t, pr[0][j], one2);  // kernel row W-1 == row 0
+        out.v[c] = t.x;
+        out.v[c + 1] = t.y;
+#pragma unroll
+        for (int i = NACC - 1; i >= 1; --i) {
+            t = make_float2(acc[i - 1].v[c], acc[i - 1].v[c + 1]);
+#pragma unroll
+            for (int j = 0; j < W; ++j) t = add2p(t, pr[i <= RAD ? i : W - 1 - i][j], one2);
+            acc[i].v[c] = t.x;
+            acc[i].v[c + 1] = t.y;
+        }
+        t = pr[0][0];
+#pragma unroll
+        for (int j = 1; j < W; ++j) t = add2p(t, pr[0][j], one2);
+        acc[0].v[c] = t.x;
+        acc[0].v[c + 1] = t.y;
+    }
+    return out;
+}
+
 // Store 4 columns of an output row with the column-ring policy (edge threads).
 //   ring_mode 0: keep -- only columns in [rad, C-rad) are written
 //   ring_mode 1: copy -- ring columns take `ringv` (the input samples)
@@ -704,7 +752,7 @@ __device__ __forceinline__ void publish_row(float* drow, const float* srow, int 
 // Consumer: one item (plane, strip, band). ROW_EDGE items contain ring rows or
 // rows with a dead row pass; all others run the lean loop.
 
-template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE>
+template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE, bool SYM>
 __device__ __forceinline__ void consume_item(const Params& p, const Item& it, const float* ring, uint64_t* full,
                                              uint64_t* empty, const int* sshift, float* stage_out, int& slot,
                                              uint32_t& phase, int& gs) {
@@ -794,7 +842,10 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                             for (int i = 0; i < 4; ++i) outv.v[i] = 0.0f;
                         }
                     } else if (MODE == MODE_SINGLE) {
-                        outv = dense_fold<RAD, NACC>(acc[g], win, p.k, p.one);
+                        if constexpr (SYM && SC_F2 && RAD >= 1)
+                            outv = dense_fold_sym<RAD, NACC>(acc[g], win, p.k, p.one);
+                        else
+                            outv = dense_fold<RAD, NACC>(acc[g], win, p.k, p.one);
                     } else {
                         F4 v;
                         if (MODE == MODE_FUSED) {
@@ -925,7 +976,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 // ---------------------------------------------------------------------------
 // The kernel
 
-template <int MODE, int RAD, bool ALIGNED>
+template <int MODE, int RAD, bool ALIGNED, bool SYM = false>
 #ifndef SC_MINB
 #define SC_MINB 1
 #endif
@@ -980,9 +1031,9 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
         if (item_rows_edge<MODE, RAD>(p, it))
-            consume_item<MODE, RAD, ALIGNED, true>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
+            consume_item<MODE, RAD, ALIGNED, true, SYM>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
         else
-            consume_item<MODE, RAD, ALIGNED, false>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
+            consume_item<MODE, RAD, ALIGNED, false, SYM>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
 #ifdef SC_TRACE
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 30 + ntr, clock64());
         ++ntr;

@@ -14,7 +14,7 @@ struct Params;
 const void* kernel_fused(int rad, bool aligned);
 const void* kernel_hpass(int rad, bool aligned);
 const void* kernel_vpass(int rad, bool aligned);
-const void* kernel_single(int rad, bool aligned);
+const void* kernel_single(int rad, bool aligned, bool sym = false);
 const void* kernel_fused_direct(int rad);
 const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);

@@ -260,4 +260,8 @@ def test_packed_math_keeps_two_roundings():
         if "sepconv_" not in fn:
             continue
         assert ffma == 0, f"scalar FFMA (contracted mul+add) in {fn}"
-        assert ffma2 <= fmul2, f"{fn}: {ffma2} FFMA2 vs {fmul2} FMUL2 -- contraction suspected"
+        # symmetric-matrix single-pass kernels (4th template argument true) reuse
+        # mirrored products: fewer FMUL2 than adds by design, at most 2 adds per product
+        sym = re.search(r"sepconv_rows_kernelILi\d+ELi\d+ELb[01]ELb1E", fn) is not None
+        limit = 2 * fmul2 if sym else fmul2
+        assert ffma2 <= limit, f"{fn}: {ffma2} FFMA2 vs {fmul2} FMUL2 -- contraction suspected"
