@@ -249,7 +249,7 @@ def main():
 
     from paper_1711_09791_b200 import _lib
     from paper_1711_09791_b200 import device as dev
-    from paper_1711_09791_b200.multi import BandStepper, PeerBandStepper, band_plan, band_two_pass, frame_shard
+    from paper_1711_09791_b200.multi import BandStepper, PeerBandStepper, band_plan, frame_shard
 
     world, rank, local = dist_env()
     backend = os.environ.get("SEPCONV_BENCH_BACKEND", "nccl")  # gloo: orchestration check on one GPU
@@ -384,13 +384,9 @@ def main():
     # ---- end to end through the C-ABI host entry point (pinned host planes)
     e2e = None
     if args.e2e_steps > 0:
-        if band is not None:
-            lo, hi, in_lo, in_hi = band.lo, band.hi, band.in_lo, band.in_hi
-            host = [torch.empty((R, C), dtype=torch.float32, pin_memory=True) for _ in range(P)] if world == 1 else None
-            if host is None:
-                host = None
         # host planes hold this rank's rows (N=1: the whole image); in place like conv_two_pass
         if band is not None and world == 1:
+            host = [torch.empty((R, C), dtype=torch.float32, pin_memory=True) for _ in range(P)]
             for p in range(P):
                 host[p].copy_(src[p].cpu())
             h2d, d2h = host_chunk_bytes(R, C, P, r, 0, R, 0, R)
