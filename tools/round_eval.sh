@@ -10,4 +10,7 @@ CMD="python bench.py --steps 20 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
 for c in cfg1 cfg2 cfg3 cfg4; do timeout -s KILL 300 python bench.py --config $c --steps 200 --e2e-steps 1 --no-cpu-baseline 2>/dev/null; done > gpurun_out/bench_configs.jsonl; cat gpurun_out/bench_configs.jsonl
 $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 python tools/prof_one.py --op fused > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:sepconv_rows -s 2 -c 1 -o gpurun_out/prof_fused_cfg5_r01c python tools/prof_one.py --op fused > gpurun_out/ncu_full.log 2>&1
+python tools/prof_one.py --op single > gpurun_out/plain3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:sepconv_rows -s 2 -c 1 -o gpurun_out/prof_single_cfg5_r01 python tools/prof_one.py --op single > gpurun_out/ncu_single.log 2>&1
+python tools/misalign_probe.py > gpurun_out/misalign.jsonl 2>&1; cat gpurun_out/misalign.jsonl
+python -m paper_1711_09791_b200.ladder --reps 200 --csv gpurun_out/ladder_gpu.csv > /dev/null 2>&1
 ls -la gpurun_out
