@@ -5,6 +5,8 @@ bit against the oracle (which is pinned to the reference)."""
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 from hypothesis import HealthCheck, given, settings
@@ -24,10 +26,11 @@ def bits(a, b):
 
 
 shapes = st.tuples(st.integers(1, 3), st.integers(5, 90), st.integers(5, 300))
+_N = int(os.environ.get("SC_HYPO_SCALE", "1"))  # stress runs: multiply the example counts
 widths = st.sampled_from([1, 3, 5, 7, 9])
 
 
-@settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@settings(max_examples=200 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
 @given(shape=shapes, width=widths, seed=st.integers(0, 2**32 - 1), generic=st.booleans(),
        extended=st.booleans())
 def test_random_two_pass_and_passes(oracle, monkeypatch, shape, width, seed, generic, extended):
@@ -58,9 +61,11 @@ def test_random_two_pass_and_passes(oracle, monkeypatch, shape, width, seed, gen
         assert bits(d.cpu().numpy(), want)
 
 
-@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
-@given(shape=shapes, width=widths, seed=st.integers(0, 2**32 - 1), generic=st.booleans(), copy=st.booleans())
-def test_random_single_pass(oracle, monkeypatch, shape, width, seed, generic, copy):
+@settings(max_examples=150 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(shape=shapes, width=widths, seed=st.integers(0, 2**32 - 1), generic=st.booleans(), copy=st.booleans(),
+       sym=st.booleans())
+def test_random_single_pass(oracle, monkeypatch, shape, width, seed, generic, copy, sym):
+    """sym: mirror-symmetric taps, so the dense matrix takes the product-reuse kernel."""
     _need_gpu()
     from paper_1711_09791_b200 import device as dev
 
@@ -70,6 +75,9 @@ def test_random_single_pass(oracle, monkeypatch, shape, width, seed, generic, co
     monkeypatch.setenv("SC_FORCE_GENERIC", "1" if generic else "0")
     rng = np.random.default_rng(seed)
     w = rng.uniform(-2, 2, size=width).astype(np.float32)
+    if sym:
+        w = ((w + w[::-1]) / np.float32(2)).astype(np.float32)  # bitwise w[m] == w[W-1-m]
+        assert np.array_equal(w.view(np.uint32), w[::-1].view(np.uint32))
     dense = oracle.outer_product(w)
     x = rng.uniform(-300, 300, size=(P, R, C)).astype(np.float32)
     xd = torch.from_numpy(x).cuda()
@@ -84,7 +92,7 @@ def test_random_single_pass(oracle, monkeypatch, shape, width, seed, generic, co
         assert bits(xd.cpu().numpy(), exp)
 
 
-@settings(max_examples=25, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@settings(max_examples=60 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
 @given(R=st.integers(5, 200), C16=st.integers(1, 40), width=widths, seed=st.integers(0, 2**32 - 1))
 def test_random_ppm_fused(oracle, R, C16, width, seed):
     """u8 HWC fused path (cols % 16 == 0) == oracle two-pass + rint/clip."""
