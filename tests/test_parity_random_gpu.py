@@ -183,3 +183,31 @@ def test_no_out_of_bounds_writes(oracle, off):
         d2 = dst.clone()
         d2[:, 2:R - 2, 2:C - 2] = canary
         assert bool((d2 == canary).all())
+
+
+@settings(max_examples=80 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(R=st.integers(10, 120), C=st.integers(5, 300), world=st.integers(2, 5), width=widths,
+       seed=st.integers(0, 2**32 - 1), extended=st.booleans())
+def test_random_peer_bands(R, C, world, width, seed, extended):
+    """Row bands reading their halo rows from the neighbouring bands' buffers
+    (multi-GPU peer path, neighbours in-process) == the whole-image two-pass."""
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+    from paper_1711_09791_b200.multi import band_plan
+
+    r = width // 2
+    if R < width or C < width or R // world < max(r, 1):
+        return
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(-2, 2, size=width).astype(np.float32)
+    x = torch.from_numpy(rng.uniform(-100, 100, size=(2, R, C)).astype(np.float32)).cuda()
+    want = dev.two_pass(x, w, extended=extended).cpu().numpy()
+    bands = [band_plan(R, k, world, r) for k in range(world)]
+    owned = [x[:, b.lo:b.hi].clone() for b in bands]
+    for k, b in enumerate(bands):
+        out = torch.full((2, b.hi - b.lo, C), float("nan"), device="cuda")
+        above = dev.PeerRows.of(owned[k - 1], bands[k - 1].lo) if k > 0 else None
+        below = dev.PeerRows.of(owned[k + 1], bands[k + 1].lo) if k < world - 1 else None
+        dev.two_pass_band_peer(owned[k], w, out, global_rows=R, src_row0=b.lo, dst_row0=b.lo, out_lo=b.lo,
+                               out_hi=b.hi, above=above, below=below, extended=extended)
+        assert bits(out.cpu().numpy(), want[:, b.lo:b.hi]), (k, b)
