@@ -196,9 +196,12 @@ def cpu_baseline(wl):
                       f"of the reference two-pass with StaticChunked({cores}) threads"}
 
 
-def host_chunk_bytes(rows, cols, planes, r, band_lo, band_hi, in_lo, in_hi):
-    """Bytes the host path moves per step (mirrors csrc/stream.cu chunking: 32 MiB chunks)."""
-    ch = max(16, min(rows, (32 << 20) // (cols * 4)))
+def host_chunk_bytes(rows, cols, planes, r, band_lo, band_hi, in_lo, in_hi, call_planes=None):
+    """Bytes the host path moves per step (mirrors csrc/stream.cu chunking: ~1/24 of
+    the call's planes per chunk, clamped to [4, 32] MiB; halo rows re-read per chunk)."""
+    total = (call_planes or planes) * rows * cols * 4
+    chunk_bytes = min(max(total // 24, 4 << 20), 32 << 20)
+    ch = max(16, min(rows, chunk_bytes // (cols * 4)))
     h2d = d2h = 0
     for lo in range(band_lo, band_hi, ch):
         hi = min(lo + ch, band_hi)
@@ -428,7 +431,7 @@ def main():
             planes = list(hb.view(-1, R, C).unbind(0))
             h2d = d2h = 0
             for _p in planes:
-                a_, b_ = host_chunk_bytes(R, C, 1, r, 0, R, 0, R)
+                a_, b_ = host_chunk_bytes(R, C, 1, r, 0, R, 0, R, call_planes=len(planes))
                 h2d += a_
                 d2h += b_
 
