@@ -286,6 +286,11 @@ def main():
     else:
         band = band_plan(R, rank, world, r)
         halo = halo_mode(args.halo, world) if world > 1 else "none"
+        if halo == "peer" and args.halo == "auto":
+            from paper_1711_09791_b200.multi import peer_transport_works
+
+            if not peer_transport_works():  # one-time probe: both transports, same bits on every rank
+                halo = "nccl"
         rows_held = (band.lo, band.hi) if halo == "peer" else (band.in_lo, band.in_hi)
         src = torch.empty((P, rows_held[1] - rows_held[0], C), dtype=torch.float32, device=device)
         for p in range(P):

@@ -428,3 +428,75 @@ class PeerBandStepper:
         for ptr, off in self._opened:
             dev.ipc_close(ptr, off)
         self._opened = []
+
+
+def peer_transport_works(group=None, device=None) -> bool:
+    """One-time probe run by every rank before choosing the peer transport: a tiny
+    banded image is convolved twice, with the halo read in-kernel from the
+    neighbours' IPC-mapped buffers and with a send/recv halo exchange
+    (BandStepper); True only if every rank got identical bits from both and no
+    step failed. Every rank takes part in every collective whatever happens
+    locally, so a failure anywhere cannot hang the others."""
+    import torch.distributed as dist
+
+    from . import device as dev
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return True
+    rank = dist.get_rank(group)
+    dev_t = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    R, C, P = 8 * world, 256, 2
+    w = (torch.tensor([1, 4, 6, 4, 1], dtype=torch.float32) / 16).numpy()
+    band = band_plan(R, rank, world, 2)
+    full = dev.synthetic((P, R, C), 97, 1, device=dev_t)
+    own = full[:, band.lo:band.hi].clone()
+    out_peer = torch.full((P, band.hi - band.lo, C), float("nan"), device=dev_t)
+    held = torch.full((P, band.local_rows, C), float("nan"), device=dev_t)
+    held[:, band.owned] = own
+    out_ref = torch.full_like(out_peer, float("nan"))
+    n, Rs, _, sps, srs = dev._planes(own, "own")
+
+    ok = True
+    try:
+        handle, offset = dev.ipc_export(own)
+    except Exception:  # noqa: BLE001 -- any failure means: do not use the peer path
+        ok, handle, offset = False, b"\0" * 64, 0
+    torch.cuda.synchronize(dev_t)
+    metas = publish_peer_meta(PeerMeta(rank, band.lo, band.hi, handle, offset, sps, srs, C, n), band, group)
+    everyone = [None] * world
+    dist.all_gather_object(everyone, ok, group=group)
+    opened = []
+    if all(everyone):
+        try:
+            above, below = peer_neighbours(metas, band)
+            rows = []
+            for m in (above, below):
+                if m is None:
+                    rows.append(None)
+                    continue
+                ptr = dev.ipc_open(m.handle, m.offset, dev_t.index)
+                opened.append((ptr, m.offset))
+                rows.append(dev.PeerRows(ptr, m.lo, m.hi - m.lo, m.plane_stride, m.row_stride))
+            dev.two_pass_band_peer(own, w, out_peer, global_rows=R, src_row0=band.lo, dst_row0=band.lo,
+                                   out_lo=band.lo, out_hi=band.hi, above=rows[0], below=rows[1])
+            torch.cuda.synchronize(dev_t)
+        except Exception:  # noqa: BLE001
+            ok = False
+    else:
+        ok = False
+    try:
+        BandStepper(held, out_ref, band, w, group=group).step()  # collective P2P: every rank runs it
+        torch.cuda.synchronize(dev_t)
+    except Exception:  # noqa: BLE001
+        ok = False
+    ok = ok and bool(torch.equal(out_peer, out_ref))
+    flag = torch.tensor([1 if ok else 0], device=dev_t if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    dist.barrier(group=group)  # nobody unmaps / frees while a neighbour may still read
+    for ptr, off in opened:
+        try:
+            dev.ipc_close(ptr, off)
+        except Exception:  # noqa: BLE001
+            pass
+    return bool(flag.item() == 1)

@@ -179,3 +179,38 @@ def test_band_split_mode_on_gpu(dev, oracle, world, extended):
         own = slice(b.lo - b.in_lo, b.hi - b.in_lo)
         assert np.array_equal(_bits(local[:, own].cpu().numpy()), _bits(want_img[:, b.lo:b.hi]))
         assert np.array_equal(_bits(scratch[:, own].cpu().numpy()), _bits(want_scr[:, b.lo:b.hi]))
+
+
+def _probe_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_1711_09791_b200.multi import peer_transport_works
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        q.put((rank, peer_transport_works()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_transport_probe_agrees():
+    """bench.py's one-time probe (peer halo reads vs send/recv exchange on a tiny
+    banded image) returns True on every rank when the IPC mapping works."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_probe_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    results = dict(q.get(timeout=5) for _ in range(3))
+    assert all(results.values()), results
