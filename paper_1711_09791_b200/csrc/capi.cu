@@ -275,7 +275,11 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
                     const long long bands = head / tall + (rows - head + shrt - 1) / shrt;
                     cost *= 1.0 + (double)(2 * rad) * bands / rows;
                 } else {
+                    // ~2 items per CTA for load balance; when that makes bands shorter
+                    // than 16 rows the 2r halo rows dominate, so one taller item per CTA
+                    // (measured: 3x1152^2 -7%, 3x1728^2 -5%)
                     long long b = units * (long long)rows / ((kn.ipc > 0 ? kn.ipc : 2) * g);
+                    if (kn.ipc == 0 && b < 16) b = units * (long long)rows / g;
                     if (b > tall) b = tall;
                     if (b < 4) b = 4;
                     bh = (int)b;
