@@ -146,9 +146,15 @@ __global__ void __launch_bounds__(32 + 256, 1) sepconv_u8_kernel(const __grid_co
                 for (int q = 0; q < 3; ++q) {
                     float win[12];
 #pragma unroll
-                    for (int c = 0; c < 12; ++c) {
-                        const int b = 3 * c + q;  // byte index in the 36-byte window
-                        win[c] = u8f(wd[b >> 2], b & 3);
+                    for (int c = 0; c < 12; c += 2) {
+                        // two samples per packed FADD2: (2^23 + byte) - 2^23, exact
+                        const int b0 = 3 * c + q, b1 = 3 * (c + 1) + q;  // byte indices in the 36-byte window
+                        const float2 v = __fadd2_rn(
+                            make_float2(__uint_as_float(__byte_perm(wd[b0 >> 2], 0x4B000000u, 0x7650 + (b0 & 3))),
+                                        __uint_as_float(__byte_perm(wd[b1 >> 2], 0x4B000000u, 0x7650 + (b1 & 3)))),
+                            make_float2(-8388608.0f, -8388608.0f));
+                        win[c] = v.x;
+                        win[c + 1] = v.y;
                     }
                     F4 v;
                     if (live) {
@@ -164,9 +170,17 @@ __global__ void __launch_bounds__(32 + 256, 1) sepconv_u8_kernel(const __grid_co
                     // ring columns keep the input byte of row yo (pixel ring == input)
                     uint32_t ob[12];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
+                    for (int c = 0; c < 4; c += 2)
 #pragma unroll
-                        for (int q = 0; q < 3; ++q) ob[3 * c + q] = f2u8(outv[q].v[c]);
+                        for (int q = 0; q < 3; ++q) {
+                            // clip then round half-even via 1.5*2^23, two samples per FADD2
+                            const float2 m = __fadd2_rn(
+                                make_float2(fminf(fmaxf(outv[q].v[c], 0.0f), 255.0f),
+                                            fminf(fmaxf(outv[q].v[c + 1], 0.0f), 255.0f)),
+                                make_float2(12582912.0f, 12582912.0f));
+                            ob[3 * c + q] = __float_as_uint(m.x) & 0xFFu;
+                            ob[3 * (c + 1) + q] = __float_as_uint(m.y) & 0xFFu;
+                        }
                     if (!fast) {
                         int rr = slot * U8_SROWS + k - RAD;
                         if (rr < 0) rr += NS * U8_SROWS;
