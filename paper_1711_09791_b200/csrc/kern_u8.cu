@@ -32,8 +32,14 @@ __device__ __forceinline__ uint32_t f2u8(float x) {
     return __float_as_uint(__fadd_rn(c, 12582912.0f)) & 0xFFu;
 }
 
+#ifndef SC_U8_MAXT
+#define SC_U8_MAXT (32 + 256)
+#endif
+#ifndef SC_U8_MINB
+#define SC_U8_MINB 1
+#endif
 template <int RAD>
-__global__ void __launch_bounds__(32 + 256, 1) sepconv_u8_kernel(const __grid_constant__ U8Params p) {
+__global__ void __launch_bounds__(SC_U8_MAXT, SC_U8_MINB) sepconv_u8_kernel(const __grid_constant__ U8Params p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
     const int NS = p.ns;
