@@ -12,11 +12,13 @@ ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--grid", default="")
 ap.add_argument("--graph", action="store_true", help="time 20 launches captured in a CUDA graph (no host overhead)")
 ap.add_argument("--size", type=int, default=0, help="override: 3 x size x size, gauss5")
+ap.add_argument("--rows", type=int, default=0, help="override rows (with --cols)")
+ap.add_argument("--cols", type=int, default=0)
 a = ap.parse_args()
 wl = CONFIGS[a.cfg]
-if a.size:
+if a.size or a.rows:
     import dataclasses
-    wl = dataclasses.replace(wl, rows=a.size, cols=a.size, frames=1, planes=3)
+    wl = dataclasses.replace(wl, rows=a.rows or a.size, cols=a.cols or a.size, frames=1, planes=3)
 w = wl.tap_vector()
 shape = (wl.frames, wl.planes, wl.rows, wl.cols) if wl.frames > 1 else (wl.planes, wl.rows, wl.cols)
 x = dev.synthetic(shape, wl.seed, wl.kind)
