@@ -47,7 +47,7 @@ static int cuda_fail(cudaError_t e, const char* what) {
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
     int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
-    int no_sym = 0;
+    int no_sym = 0, no_pdl = 0;
 };
 
 static Knobs read_knobs() {
@@ -73,6 +73,7 @@ static Knobs read_knobs() {
         else if (name == "IPC") k.ipc = v;
         else if (name == "NO_STAGE") k.no_stage = v;
         else if (name == "NO_SYM") k.no_sym = v;
+        else if (name == "NO_PDL") k.no_pdl = v;
     }
     return k;
 }
@@ -484,7 +485,23 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
 #endif
 
     void* args[] = {&p};
-    cudaError_t e = cudaLaunchKernel(kern, dim3(pl.grid), dim3(pl.threads), args, pl.smem, s);
+    // Programmatic dependent launch: this grid may be scheduled while the previous
+    // kernel on the stream drains (its launch and smem/mbarrier setup overlap that
+    // kernel's tail); the kernel itself waits (griddepcontrol.wait) for the
+    // previous grid to complete before touching global memory.
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = dim3(pl.grid);
+    cfg.blockDim = dim3(pl.threads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = s;
+    if (!kn.no_pdl) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    cudaError_t e = cudaLaunchKernelExC(&cfg, kern, args);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     count_launch();
     if (kn.debug_plan)

@@ -346,6 +346,9 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
         ++ntr;
 #endif
         if (item >= p.nitems) {
+            // no more work for this CTA: the next kernel on the stream may start
+            // launching (it still waits for this grid to complete before its reads)
+            asm volatile("griddepcontrol.launch_dependents;");
             if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
             sitem[slot] = -1;
             mbar_arrive_expect_tx(&full[slot], 0u);
@@ -1001,6 +1004,9 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
         mbar_fence_init();
     }
     __syncthreads();
+    // launched with programmatic stream serialization: the setup above overlapped
+    // the previous kernel's tail; no global memory is touched before it completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 0) {
 #ifdef SC_TRACE
