@@ -10,21 +10,26 @@
 //   MODE_VPASS  vertical_rows_vec                         S/conv.py:269-293
 //   MODE_SINGLE single_pass_rows_vec / unrolled5_rows_vec S/conv.py:86-114, :146-175
 //
-// Work decomposition: an "item" is (plane, column strip of TW = 8*NT output
-// columns, row band). A persistent grid claims items from an atomic ticket
-// (dynamic scheduling); the planner in capi.cu picks TW and the band schedule.
+// Work decomposition: an "item" is (plane, column strip of TW = 4*GROUPS*NT
+// output columns, row band). A persistent grid claims items from an atomic
+// ticket (dynamic scheduling); the planner in capi.cu picks TW and the band
+// schedule. Launches use programmatic dependent launch (griddepcontrol).
 // Per CTA:
 //   warp 0      producer (one lane): streams input rows [x0-4, x0+TW+4) of the
 //               strip into a ring of NS shared-memory stages x SROWS rows with
-//               the bulk-copy TMA engine (cp.async.bulk + mbarrier complete_tx).
-//               Unaligned rows are copied from the 16-B boundary below them and
-//               their shift is published in shared memory.
-//   warps 1..   consumers: thread t owns two 4-column groups (strip offsets 4t
-//               and 4t + TW/2). Per input row and group it reads a 12-sample
+//               the bulk-copy TMA engine (cp.async.bulk + mbarrier complete_tx),
+//               from this band's buffer or -- for halo rows of a multi-GPU
+//               band -- from a neighbouring band's peer-mapped buffer. Unaligned
+//               rows are copied from the 16-B boundary below them and their
+//               shift is published in shared memory.
+//   warps 1..   consumers: thread t owns GROUPS 4-column groups (strip offsets
+//               4t + g*TW/GROUPS; one group for the two-pass modes, two for the
+//               single pass). Per input row and group it reads a 12-sample
 //               window (3 x LDS.128), computes the row pass for its 4 columns
 //               and pushes them through a shift register of 2r partial column
 //               sums, emitting output row y-r as soon as input row y arrived.
-//               Results go straight to HBM with STG.128.
+//               Results go straight to HBM with STG.128 (unaligned destination
+//               rows: staged in smem and written by bulk TMA stores).
 //
 // Bit-exactness: every product/sum is __fmul_rn/__fadd_rn (never contracted to
 // FMA) in the reference's fold order: left-to-right from the first product,
