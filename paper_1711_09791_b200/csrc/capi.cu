@@ -219,11 +219,13 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     // Work split. Items are (plane, strip, row band), claimed from an atomic ticket
     // in order, so load balance only depends on the tail of a launch; every item
     // re-reads a 2r-row halo and every strip an 8-column halo.
-    //  * large jobs (>= ~6 items of 128 rows per CTA): 1024-column strips, a head of
-    //    128-row bands (halo 4/128) and a tail of 32-row bands sized to two waves;
+    //  * large jobs (>= ~8 waves of 128-row items): 512-column strips (two-pass; the
+    //    single pass, 8 columns per thread: 1024), a head of 128-row bands (halo
+    //    4/128) and a tail of 32-row bands sized to two waves; mid-size jobs the same
+    //    with 64/16-row bands;
     //  * small jobs: the strip width and a uniform band height are chosen together to
-    //    give every CTA ~2 items at the least halo + padding cost (narrow strips are
-    //    cheaper than short bands: 8/TW vs 2r/bh);
+    //    give every CTA ~2 items (1 if that makes bands < 16 rows) at the least halo +
+    //    padding cost (narrow strips are cheaper than short bands: 8/TW vs 2r/bh);
     //  * explicit two-segment jobs (a band's boundary strips) use short bands.
     int lo1 = j.out_lo, hi1 = j.out_hi, lo2 = seg2 ? j.out_lo2 : 0, hi2 = seg2 ? j.out_hi2 : 0;
     if (hi1 <= lo1) { lo1 = lo2; hi1 = hi2; lo2 = hi2 = 0; }
