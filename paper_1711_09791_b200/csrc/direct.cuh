@@ -95,6 +95,9 @@ __global__ void __launch_bounds__(32 * DWARPS, SC_DMINB) sepconv_direct_kernel(c
     const int R = p.R, C = p.C;
     const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);
     const bool zero_fill = (MODE == MODE_HPASS) && (p.flags & F_ZERO_FILL);
+    // launched with programmatic stream serialization (capi.cu): wait for the
+    // previous kernel on the stream before touching global memory
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (;;) {
         int item = 0;
         if (lane == 0) item = atomicAdd(&p.work[0], 1);
