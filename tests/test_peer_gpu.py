@@ -214,3 +214,28 @@ def test_peer_transport_probe_agrees():
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     results = dict(q.get(timeout=5) for _ in range(3))
     assert all(results.values()), results
+
+
+def test_peer_rows_in_host_mapped_memory(dev):
+    """The halo rows' bulk copies also work when the neighbouring bands live in
+    pinned HOST memory (mapped into the device address space over PCIe): the TMA
+    engine reading non-local memory through the fabric, as it does for a peer
+    GPU's HBM over NVLink."""
+    from paper_1711_09791_b200.multi import band_plan
+
+    R, C, world = 120, 1024, 3
+    w = np.array([-1, -2, 7, -2, -1], np.float32)
+    x = dev.synthetic((3, R, C), 21, 2)
+    want = dev.two_pass(x, w).cpu().numpy()
+    bands = [band_plan(R, k, world, 2) for k in range(world)]
+    host = [x[:, b.lo:b.hi].cpu().pin_memory() for b in bands]  # every band in pinned host memory
+    b = bands[1]
+    own = x[:, b.lo:b.hi].clone()
+    out = torch.full_like(own, float("nan"))
+    above = dev.PeerRows(host[0].data_ptr(), bands[0].lo, bands[0].hi - bands[0].lo, host[0].stride(0),
+                         host[0].stride(1), keep=host[0])
+    below = dev.PeerRows(host[2].data_ptr(), bands[2].lo, bands[2].hi - bands[2].lo, host[2].stride(0),
+                         host[2].stride(1), keep=host[2])
+    dev.two_pass_band_peer(own, w, out, global_rows=R, src_row0=b.lo, dst_row0=b.lo, out_lo=b.lo, out_hi=b.hi,
+                           above=above, below=below)
+    assert np.array_equal(_bits(out.cpu().numpy()), _bits(want[:, b.lo:b.hi]))
