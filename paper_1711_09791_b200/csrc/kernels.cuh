@@ -156,7 +156,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t tx
                  : "memory");
 }
 
+#ifndef SC_WAIT_HINT
+#define SC_WAIT_HINT 0  // ns; > 0: try_wait suspends the thread up to this long per poll
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SC_WAIT_HINT > 0
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "SC_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra SC_WAIT;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(SC_WAIT_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "SC_WAIT:\n\t"
@@ -164,6 +176,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!P1 bra SC_WAIT;\n}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
