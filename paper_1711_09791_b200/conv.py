@@ -19,7 +19,6 @@ from enum import Enum
 
 import numpy as np
 
-from . import _lib
 from .errors import InvalidArgumentError, InvalidDimensionError, UnsupportedWidthError
 from .image import Plane, ValidRegion, valid_region
 from .kernels import DenseKernel, SeparableKernel
@@ -125,7 +124,10 @@ class _Staged:
         torch.from_numpy(a)[r0:r1, c0:c1].copy_(t[r0:r1, c0:c1])
 
     def finish(self):
-        _torch().cuda.current_stream().synchronize() if self.host else None
+        """Host planes: wait for the write-backs (the reference's calls block);
+        device planes stay stream-ordered like any CUDA op."""
+        if self.host:
+            _torch().cuda.current_stream().synchronize()
 
 
 def _count(counter: OpCounter | None, mults: int, adds: int) -> None:
@@ -249,6 +251,3 @@ def arith_count(variant: ConvVariant, rows: int, cols: int, width: int) -> Arith
     terms = width * width
     return ArithCount(multiplications=terms * valid, additions=(terms - 1) * valid)
 
-
-def _launches() -> int:
-    return _lib.launch_count()
