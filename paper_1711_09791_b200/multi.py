@@ -221,8 +221,6 @@ class BandStepper:
 
     def __init__(self, local_src, local_dst, band: Band, taps, *, extended: bool = False, group=None,
                  host_staged: bool | None = None):
-        import ctypes
-
         from . import _lib
         from . import device as dev
 
@@ -232,7 +230,7 @@ class BandStepper:
         self._check = _lib.check
         w = dev._taps(taps)
         self._w = w  # keep alive
-        wp = w.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        wp = w.ctypes.data  # const float* taps (kept alive by self._w)
         n, Rs, C, sps, srs = dev._planes(local_src, "local_src")
         n2, Rd, C2, dps, drs = dev._planes(local_dst, "local_dst")
         if n2 != n or C2 != C or Rd != band.hi - band.lo or Rs != band.local_rows:
