@@ -199,9 +199,9 @@ def cpu_baseline(wl):
 def host_chunk_bytes(rows, cols, planes, r, band_lo, band_hi, in_lo, in_hi, call_planes=None):
     """Bytes the host path moves per step (mirrors csrc/stream.cu chunking: ~1/24 of
     the call's planes per chunk, clamped to [4, 32] MiB; halo rows re-read per chunk)."""
-    total = (call_planes or planes) * rows * cols * 4
+    total = (call_planes or planes) * (band_hi - band_lo) * cols * 4
     chunk_bytes = min(max(total // 24, 4 << 20), 32 << 20)
-    ch = max(16, min(rows, chunk_bytes // (cols * 4)))
+    ch = max(16, min(band_hi - band_lo, chunk_bytes // (cols * 4)))
     h2d = d2h = 0
     for lo in range(band_lo, band_hi, ch):
         hi = min(lo + ch, band_hi)
@@ -413,31 +413,21 @@ def main():
             def e2e_step():
                 dev.two_pass_host(planes, planes, w, device=local)
         elif band is not None:
-            # N>1: each rank streams its band (nccl: + halo rows) from its own pinned buffer
-            hb = torch.empty(src.shape, dtype=torch.float32, pin_memory=True)
-            hb.copy_(src.cpu())
-            ho = torch.empty((P, band.hi - band.lo, C), dtype=torch.float32, pin_memory=True)
-            h2d = hb.numel() * 4
-            d2h = P * (band.hi - band.lo) * C * 4
-            ds = torch.empty_like(src)
-            do = torch.empty_like(dst)
-            if halo == "peer":
-                e2e_stepper = PeerBandStepper(ds, do, band, w)
+            # N>1: each rank streams ITS row band end to end through the C-ABI host
+            # entry point: its pinned host copy holds rows [in_lo, in_hi) (owned +
+            # halo), so the halo comes from host memory and no GPU exchange is needed
+            hrows = torch.empty((P, band.in_hi - band.in_lo, C), dtype=torch.float32, device=device)
+            for p in range(P):
+                dev.fill_synthetic(hrows[p], wl.seed, wl.kind, offset=p * R * C + band.in_lo * C)
+            hb = [torch.empty((band.in_hi - band.in_lo, C), dtype=torch.float32, pin_memory=True) for _ in range(P)]
+            for p in range(P):
+                hb[p].copy_(hrows[p].cpu())
+            del hrows
+            h2d, d2h = host_chunk_bytes(R, C, P, r, band.lo, band.hi, band.in_lo, band.in_hi)
 
-                def e2e_step():
-                    ds.copy_(hb, non_blocking=True)
-                    e2e_stepper.sync()      # neighbours' rows landed before the kernel reads them
-                    e2e_stepper.step()
-                    ho.copy_(do, non_blocking=True)
-                    e2e_stepper.sync()      # nobody overwrites rows a neighbour still reads
-            else:
-                e2e_stepper = BandStepper(ds, do, band, w)
-
-                def e2e_step():
-                    ds.copy_(hb, non_blocking=True)
-                    e2e_stepper.step()
-                    ho.copy_(do, non_blocking=True)
-                    torch.cuda.current_stream().synchronize()
+            def e2e_step():
+                dev.two_pass_host_band(hb, hb, w, global_rows=R, row0=band.in_lo, out_lo=band.lo, out_hi=band.hi,
+                                       device=local)
         else:
             # frame batch: every frame-plane is one host plane of the reference's
             # Image; the C-ABI host entry point streams them all (in place)
@@ -463,12 +453,17 @@ def main():
             t = torch.tensor([e_ms], device=device if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
+            # bytes over PCIe per step for the whole job (every rank's own copies)
+            tb = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64,
+                              device=device if backend == "nccl" else "cpu")
+            dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+            h2d, d2h = int(tb[0].item()), int(tb[1].item())
         e2e = {"value": round(total_px / (e_ms / 1e3) / 1e9, 4), "unit": "Gpix/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3),
                "path": "sc_two_pass_host_f32 (pinned host planes, chunked H2D/kernel/D2H on 3 streams)"
                if (world == 1 or band is None) else
-               ("pinned H2D + PeerBandStepper (in-kernel peer halo reads) + D2H per rank" if halo == "peer" else
-                "pinned H2D + BandStepper (NCCL halo exchange) + D2H per rank")}
+               "sc_two_pass_host_band_f32 per rank (its row band + halo rows from its pinned host copy, chunked "
+               "H2D/kernel/D2H on 3 streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -166,6 +166,15 @@ int sc_planes_f32_to_hwc_u8(const float *src, uint8_t *dst, int rows, int cols, 
 int sc_two_pass_host_f32(const float *const *src_planes, float *const *dst_planes, int nplanes,
                          int rows, int cols, const float *taps, int width, int flags, int device);
 
+/* Rows [out_lo, out_hi) only (one rank's row band of a host-resident image,
+ * global-row rules): reads host rows [out_lo-r, out_hi+r) clipped to the image,
+ * writes host rows [out_lo, out_hi); plane pointers address row 0 and no other
+ * row is touched. Same streaming as sc_two_pass_host_f32 (which is the band
+ * [0, rows)). */
+int sc_two_pass_host_band_f32(const float *const *src_planes, float *const *dst_planes, int nplanes, int rows,
+                              int cols, int out_lo, int out_hi, const float *taps, int width, int flags,
+                              int device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,8 +87,30 @@ static int ensure(HostCtx* c, size_t in_floats, size_t out_floats, std::string& 
 
 using namespace sc;
 
+static int host_band(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows, int cols,
+                     int out_lo, int out_hi, const float* taps, int width, int flags, int device);
+
 extern "C" int sc_two_pass_host_f32(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows,
                                     int cols, const float* taps, int width, int flags, int device) {
+    return host_band(src_planes, dst_planes, nplanes, rows, cols, 0, rows, taps, width, flags, device);
+}
+
+extern "C" int sc_two_pass_host_band_f32(const float* const* src_planes, float* const* dst_planes, int nplanes,
+                                         int rows, int cols, int out_lo, int out_hi, const float* taps, int width,
+                                         int flags, int device) {
+    set_error("");
+    if (out_lo < 0 || out_hi > rows || out_lo >= out_hi) {
+        set_error("output rows out of range");
+        return SC_INVALID_ARGUMENT;
+    }
+    return host_band(src_planes, dst_planes, nplanes, rows, cols, out_lo, out_hi, taps, width, flags, device);
+}
+
+// Rows [out_lo, out_hi) of a rows x cols image (global-row rules), reading host
+// rows [out_lo - r, out_hi + r) clipped to the image and writing host rows
+// [out_lo, out_hi); plane pointers address row 0 (the rows outside are not touched).
+static int host_band(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows, int cols,
+                     int out_lo, int out_hi, const float* taps, int width, int flags, int device) {
     set_error("");
     if (!src_planes || !dst_planes || !taps || nplanes < 1 || rows < 1 || cols < 1) {
         set_error("null pointer or non-positive dimension");
@@ -129,14 +151,14 @@ extern "C" int sc_two_pass_host_f32(const float* const* src_planes, float* const
     if (mbs && *mbs) {
         chunk_bytes = (long long)std::atoi(mbs) << 20;
     } else {
-        const long long total = (long long)nplanes * rows * cols * 4;
+        const long long total = (long long)nplanes * (out_hi - out_lo) * cols * 4;
         chunk_bytes = total / 24;
         if (chunk_bytes < (4LL << 20)) chunk_bytes = 4LL << 20;
         if (chunk_bytes > (32LL << 20)) chunk_bytes = 32LL << 20;
     }
     long long ch = chunk_bytes / ((long long)cols * 4);
     if (ch < 16) ch = 16;
-    if (ch > rows) ch = rows;
+    if (ch > out_hi - out_lo) ch = out_hi - out_lo;
     const int chunk = (int)ch;
     std::string err;
     int rc = ensure(c, (size_t)(chunk + 2 * r) * cols, (size_t)chunk * cols, err);
@@ -150,11 +172,11 @@ extern "C" int sc_two_pass_host_f32(const float* const* src_planes, float* const
     };
     std::vector<Chunk> chunks;
     for (int p = 0; p < nplanes; ++p)
-        for (int lo = 0; lo < rows; lo += chunk) {
+        for (int lo = out_lo; lo < out_hi; lo += chunk) {
             Chunk k;
             k.plane = p;
             k.lo = lo;
-            k.hi = lo + chunk < rows ? lo + chunk : rows;
+            k.hi = lo + chunk < out_hi ? lo + chunk : out_hi;
             k.in_lo = k.lo - r > 0 ? k.lo - r : 0;
             k.in_hi = k.hi + r < rows ? k.hi + r : rows;
             chunks.push_back(k);

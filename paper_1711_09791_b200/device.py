@@ -314,6 +314,44 @@ def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring:
                                       n, shape[0], shape[1], _fp(w), w.size, flags, int(device)))
 
 
+def two_pass_host_band(src_rows, dst_rows, taps, *, global_rows: int, row0: int, out_lo: int, out_hi: int,
+                       extended: bool = False, ring: bool = True, device: int = 0) -> None:
+    """One rank's row band of a host-resident image, end to end (streamed H2D ->
+    fused kernel -> D2H, global-row rules): src_rows / dst_rows are host planes
+    holding global rows [row0, row0 + their height); output rows [out_lo, out_hi)
+    are written into dst_rows, reading src rows [out_lo - r, out_hi + r). No
+    exchange with other ranks is needed: every rank reads its halo rows from its
+    own host copy."""
+    w = _taps(taps)
+    r = w.size // 2
+    ptrs_in, ptrs_out, shape = [], [], None
+    for a, b in zip(src_rows, dst_rows):
+        for arr in (a, b):
+            if not isinstance(arr, torch.Tensor) or arr.is_cuda or arr.dtype != torch.float32 or \
+                    not arr.is_contiguous() or arr.dim() != 2:
+                raise InvalidArgumentError("band host planes must be contiguous 2-D CPU float32 tensors")
+            if shape is not None and tuple(arr.shape) != shape:
+                raise InvalidArgumentError("band host planes must share one shape")
+            shape = tuple(arr.shape)
+        C = shape[1]
+        # address of the (virtual) global row 0: the library touches rows inside the band only
+        ptrs_in.append(a.data_ptr() - row0 * C * 4)
+        ptrs_out.append(b.data_ptr() - row0 * C * 4)
+    if not ptrs_in:
+        raise InvalidArgumentError("need non-empty plane lists")
+    held_lo, held_hi = row0, row0 + shape[0]
+    if max(out_lo - r, 0) < held_lo or min(out_hi + r, global_rows) > held_hi or out_lo < held_lo or out_hi > held_hi:
+        raise InvalidArgumentError("the band's host rows do not cover the output rows plus halo")
+    n = len(ptrs_in)
+    arr_in = (ctypes.c_void_p * n)(*ptrs_in)
+    arr_out = (ctypes.c_void_p * n)(*ptrs_out)
+    flags = (_lib.SC_EXTENDED if extended else 0) | (0 if ring else _lib.SC_NO_RING)
+    L = _lib.load()
+    _lib.check(L.sc_two_pass_host_band_f32(ctypes.cast(arr_in, ctypes.c_void_p),
+                                           ctypes.cast(arr_out, ctypes.c_void_p), n, global_rows, shape[1],
+                                           out_lo, out_hi, _fp(w), w.size, flags, int(device)))
+
+
 # ---------------------------------------------------------------------------
 # PPM payload (interleaved u8 HWC, S/ppm.py) either side of the path
 

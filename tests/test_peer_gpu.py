@@ -239,3 +239,27 @@ def test_peer_rows_in_host_mapped_memory(dev):
     dev.two_pass_band_peer(own, w, out, global_rows=R, src_row0=b.lo, dst_row0=b.lo, out_lo=b.lo, out_hi=b.hi,
                            above=above, below=below)
     assert np.array_equal(_bits(out.cpu().numpy()), _bits(want[:, b.lo:b.hi]))
+
+
+@pytest.mark.parametrize("world,R,C", [(3, 301, 999), (4, 200, 1024)])
+def test_host_band_streaming(dev, oracle, world, R, C):
+    """sc_two_pass_host_band_f32: each rank's band streamed from ITS host copy of
+    rows [in_lo, in_hi) (in place), 16-row chunks; stitched == the whole image."""
+    from paper_1711_09791_b200.multi import band_plan
+
+    w = np.array([1, 4, 6, 4, 1], np.float32) / 16
+    rng = np.random.default_rng(R)
+    x = rng.uniform(-50, 50, size=(3, R, C)).astype(np.float32)
+    want = oracle.two_pass(x, w)
+    got = np.empty_like(want)
+    os.environ["SC_HOST_CHUNK_MB"] = "0"  # 16-row chunks: many seams inside each band
+    try:
+        for k in range(world):
+            b = band_plan(R, k, world, 2)
+            hb = [torch.from_numpy(np.ascontiguousarray(x[p, b.in_lo:b.in_hi])).pin_memory() for p in range(3)]
+            dev.two_pass_host_band(hb, hb, w, global_rows=R, row0=b.in_lo, out_lo=b.lo, out_hi=b.hi)
+            for p in range(3):
+                got[p, b.lo:b.hi] = hb[p].numpy()[b.lo - b.in_lo:b.hi - b.in_lo]
+    finally:
+        del os.environ["SC_HOST_CHUNK_MB"]
+    assert np.array_equal(_bits(got), _bits(want))
