@@ -211,3 +211,24 @@ def test_random_peer_bands(R, C, world, width, seed, extended):
         dev.two_pass_band_peer(owned[k], w, out, global_rows=R, src_row0=b.lo, dst_row0=b.lo, out_lo=b.lo,
                                out_hi=b.hi, above=above, below=below, extended=extended)
         assert bits(out.cpu().numpy(), want[:, b.lo:b.hi]), (k, b)
+
+
+@settings(max_examples=20 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(P=st.integers(1, 3), R=st.integers(100, 1500), C=st.integers(100, 3000), width=widths,
+       seed=st.integers(0, 2**32 - 1), generic=st.booleans())
+def test_random_larger_shapes(oracle, monkeypatch, P, R, C, width, seed, generic):
+    """Shapes large enough for multi-strip, guided (head/tail band) plans with
+    partial last strips and any width: fused two-pass and single pass."""
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    monkeypatch.setenv("SC_FORCE_GENERIC", "1" if generic else "0")
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(-2, 2, size=width).astype(np.float32)
+    x = rng.uniform(-300, 300, size=(P, R, C)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    assert bits(dev.two_pass(xd, w).cpu().numpy(), oracle.two_pass(x, w))
+    dense = oracle.outer_product(w)
+    out = torch.zeros_like(xd)
+    dev.single_pass(xd, dense, out)
+    assert bits(out.cpu().numpy(), oracle.single_pass(x, dense))
