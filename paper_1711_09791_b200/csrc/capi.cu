@@ -281,8 +281,16 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
                     // ~2 items per CTA for load balance; when that makes bands shorter
                     // than 16 rows the 2r halo rows dominate, so one taller item per CTA
                     // (measured: 3x1152^2 -7%, 3x1728^2 -5%)
-                    long long b = units * (long long)rows / ((kn.ipc > 0 ? kn.ipc : 2) * g);
-                    if (kn.ipc == 0 && b < 16) b = units * (long long)rows / g;
+                    // band height for k items per CTA, rounded UP so that the job
+                    // is at most k whole waves (a floor here left a few CTAs with one
+                    // item more than the rest: 945 items on 888 CTAs at 3x1152^2)
+                    auto bh_for = [&](long long k) {
+                        long long bands = k * g / units;
+                        if (bands < 1) bands = 1;
+                        return (rows + bands - 1) / bands;
+                    };
+                    long long b = bh_for(kn.ipc > 0 ? kn.ipc : 2);
+                    if (kn.ipc == 0 && b < 16) b = bh_for(1);
                     if (b > tall) b = tall;
                     if (b < 4) b = 4;
                     bh = (int)b;

@@ -332,6 +332,10 @@ __device__ __forceinline__ const float* src_row(const Params& p, int plane, int 
 // ---------------------------------------------------------------------------
 // Producer: one warp streams the strip's rows into the smem stage ring.
 
+#ifndef SC_STATIC_FIRST
+#define SC_STATIC_FIRST 1
+#endif
+
 template <int MODE, int RAD, bool ALIGNED>
 __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t* full, uint64_t* empty,
                                          int* sitem, int* sshift) {
@@ -354,8 +358,13 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
 #ifdef SC_TRACE
     int ntr = 0;
 #endif
+    // The first item of every CTA is its own index (no atomic: 600-900 CTAs
+    // claiming from one counter at launch serialise on it); later items come
+    // from the ticket, offset by the grid size.
+    bool first = SC_STATIC_FIRST;
     for (;;) {
-        const int item = atomicAdd(&p.work[0], 1);
+        const int item = first ? (int)blockIdx.x : (int)gridDim.x * SC_STATIC_FIRST + atomicAdd(&p.work[0], 1);
+        first = false;
 #ifdef SC_TRACE
         if (ntr < 8) {
             SC_TR(p, 2 + ntr, clock64());
