@@ -76,8 +76,10 @@ __global__ void __launch_bounds__(SC_U8_MAXT, SC_U8_MINB) sepconv_u8_kernel(cons
         const uint64_t pol = policy_evict_normal();
         int slot = 0, gs = 0;
         uint32_t phase = 0;
+        bool first = SC_STATIC_FIRST;  // first item = block index (see the row kernels' producer)
         for (;;) {
-            const int item = atomicAdd(&p.work[0], 1);
+            const int item = first ? (int)blockIdx.x : (int)gridDim.x * SC_STATIC_FIRST + atomicAdd(&p.work[0], 1);
+            first = false;
             if (item >= p.nitems) {
                 if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
                 sitem[slot] = -1;
