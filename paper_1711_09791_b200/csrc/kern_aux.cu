@@ -8,18 +8,45 @@ namespace sc {
 // Auxiliary kernels
 
 // copy_back, S/conv.py:424-449: dst[region] := src[region], per plane.
-static __global__ void copy_region_kernel(const float* __restrict__ src, float* __restrict__ dst, long long sps,
-                                   long long dps, long long srs, long long drs, int nplanes, int row_lo, int nrows,
-                                   int col_lo, int ncols) {
-    const long long total = (long long)nplanes * nrows * ncols;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int c = (int)(i % ncols);
-        const long long t = i / ncols;
-        const int r = (int)(t % nrows);
-        const int pl = (int)(t / nrows);
-        const int y = row_lo + r, x = col_lo + c;
-        dst[pl * dps + (long long)y * drs + x] = src[pl * sps + (long long)y * srs + x];
+// One warp per region row (grid-stride over rows). The body moves float4s when
+// source and destination rows share their 16-B phase (always, for equal
+// strides and aligned bases), four loads in flight per lane before the stores;
+// the <= 3 columns before the first aligned destination float and the tail are
+// scalar. Rows of mismatched phase fall back to coalesced scalar copies.
+static __global__ void __launch_bounds__(256) copy_region_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                                                 long long sps, long long dps, long long srs,
+                                                                 long long drs, int nplanes, int row_lo, int nrows,
+                                                                 int col_lo, int ncols) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long rows = (long long)nplanes * nrows;
+    for (long long rr = warp; rr < rows; rr += nwarps) {
+        const long long pl = rr / nrows;
+        const int y = row_lo + (int)(rr - pl * nrows);
+        const float* s = src + pl * sps + (long long)y * srs + col_lo;
+        float* d = dst + pl * dps + (long long)y * drs + col_lo;
+        int head = (int)(((16u - (unsigned)(reinterpret_cast<uintptr_t>(d) & 15u)) & 15u) >> 2);
+        if (head > ncols) head = ncols;
+        if ((reinterpret_cast<uintptr_t>(s + head) & 15u) != 0) {
+            for (int c = lane; c < ncols; c += 32) d[c] = s[c];
+            continue;
+        }
+        if (lane < head) d[lane] = s[lane];
+        const int nv = (ncols - head) >> 2;
+        const float4* s4 = reinterpret_cast<const float4*>(s + head);
+        float4* d4 = reinterpret_cast<float4*>(d + head);
+        int i = lane;
+        for (; i + 96 < nv; i += 128) {
+            const float4 a = s4[i], b = s4[i + 32], c = s4[i + 64], e = s4[i + 96];
+            d4[i] = a;
+            d4[i + 32] = b;
+            d4[i + 64] = c;
+            d4[i + 96] = e;
+        }
+        for (; i < nv; i += 32) d4[i] = s4[i];
+        const int t0 = head + 4 * nv;
+        if (t0 + lane < ncols) d[t0 + lane] = s[t0 + lane];
     }
 }
 
@@ -63,8 +90,9 @@ cudaError_t launch_copy_region(const float* src, float* dst, long long sps, long
                                cudaStream_t s) {
     const long long total = (long long)nplanes * nrows * ncols;
     if (total <= 0) return cudaSuccess;
-    copy_region_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, dst, sps, dps, srs, drs, nplanes, row_lo, nrows,
-                                                             col_lo, ncols);
+    // one warp per row: up to 8 warps x 8 CTAs per SM
+    copy_region_kernel<<<grid_for((long long)nplanes * nrows * 32, 256), 256, 0, s>>>(
+        src, dst, sps, dps, srs, drs, nplanes, row_lo, nrows, col_lo, ncols);
     count_launch();
     return cudaGetLastError();
 }
