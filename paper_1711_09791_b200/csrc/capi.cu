@@ -47,7 +47,7 @@ static int cuda_fail(cudaError_t e, const char* what) {
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
     int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
-    int no_sym = 0, no_pdl = 0;
+    int no_sym = 0, no_pdl = 0, split_passes = 0;
 };
 
 static Knobs read_knobs() {
@@ -74,6 +74,7 @@ static Knobs read_knobs() {
         else if (name == "NO_STAGE") k.no_stage = v;
         else if (name == "NO_SYM") k.no_sym = v;
         else if (name == "NO_PDL") k.no_pdl = v;
+        else if (name == "SPLIT_PASSES") k.split_passes = v;
     }
     return k;
 }
@@ -415,6 +416,10 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         case MODE_HPASS: kern = kernel_hpass(rad, aligned); break;
         case MODE_VPASS: kern = kernel_vpass(rad, aligned); break;
         case MODE_SINGLE: kern = kernel_single(rad, aligned, sym); break;
+        case MODE_SPLITF:
+            if (!aligned) return fail(SC_INVALID_ARGUMENT, "split-fused kernel needs 16-B aligned rows");
+            kern = kernel_splitf(rad);
+            break;
     }
     if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(j.width));
     const bool seg2 = j.out_hi2 > j.out_lo2;
@@ -422,7 +427,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
 
     // Kernel family: the TMA stage pipeline (default) or the register-streaming
     // direct kernel (SC_DIRECT=1), both bit-identical.
-    const bool direct = aligned && kn.direct != 0 && !j.above && !j.below;  // direct reads src only
+    const bool direct = aligned && kn.direct != 0 && !j.above && !j.below && j.mode != MODE_SPLITF;  // direct reads src only
     if (direct) {
         switch (j.mode) {
             case MODE_FUSED: kern = kernel_fused_direct(rad); break;
@@ -488,6 +493,57 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.nitems0 = pl.nitems0;
     p.work = work_slot(dev);
     if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
+    float* side = nullptr;
+    if (j.mode == MODE_SPLITF) {
+        // halo snapshot: stream-ordered scratch from the device's default pool
+        // (kept pooled: release threshold raised once), taken right before the launch
+        p.scr = j.scr;
+        p.scr_ps = j.scr_ps;
+        p.scr_rs = j.scr_rs;
+        const long long units = (long long)j.nplanes * pl.nstrips;
+        const int nb1 = (int)(pl.nitems0 / units);
+        const int nb = (int)(pl.nitems / units);
+        const size_t rows_f = (size_t)j.nplanes * nb * 2 * rad * j.C;
+        const size_t cols_f = (size_t)j.nplanes * (pl.nstrips - 1) * j.R * 8;
+        static std::once_flag pool_once[64];
+        if (dev >= 0 && dev < 64)
+            std::call_once(pool_once[dev], [dev]() {
+                cudaMemPool_t pool;
+                if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                    uint64_t thr = ~0ULL;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                }
+                cudaGetLastError();
+            });
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&side), (rows_f + cols_f + 4) * sizeof(float), s);
+        if (e != cudaSuccess) return cuda_fail(e, "split snapshot allocation");
+        p.side_rows = side;
+        p.side_cols = side + rows_f;
+        p.side_nb = nb;
+        SnapJob sj{};
+        sj.img = j.src;
+        sj.ps = j.sps;
+        sj.rs = j.srs;
+        sj.nplanes = j.nplanes;
+        sj.R = j.R;
+        sj.C = j.C;
+        sj.rad = rad;
+        sj.tw = pl.tw;
+        sj.nstrips = pl.nstrips;
+        sj.lo1 = pl.lo1;
+        sj.bh1 = pl.band_h;
+        sj.nb1 = nb1;
+        sj.lo2 = pl.lo2;
+        sj.bh2 = pl.band_h2;
+        sj.nb = nb;
+        sj.side_rows = side;
+        sj.side_cols = side + rows_f;
+        e = launch_split_snapshot(sj, s);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(side, s);
+            return cuda_fail(e, "split snapshot launch");
+        }
+    }
 #ifdef SC_TRACE
     p.trace = trace_buffer();
     if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * TRACE_SLOTS * kTraceCtas, s);
@@ -512,6 +568,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         cfg.numAttrs = 1;
     }
     cudaError_t e = cudaLaunchKernelExC(&cfg, kern, args);
+    if (side) cudaFreeAsync(side, s);  // after the kernel, in stream order
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     count_launch();
     if (kn.debug_plan)
@@ -933,6 +990,47 @@ int sc_two_pass_split_f32(float* image, float* scratch, int nplanes, int rows, i
     const int r = width / 2;
     const int h_lo = (flags & SC_EXTENDED) ? 0 : r;
     const int h_hi = (flags & SC_EXTENDED) ? rows : rows - r;
+    // One pass (image read once; scratch and image written once) when every row is
+    // 16-B aligned; otherwise (or SC_SPLIT_PASSES=1) the row pass + column pass pair.
+    const Knobs kn = read_knobs();
+    const bool aligned = cols % 4 == 0 && aligned16(image) && aligned16(scratch) && image_plane_stride % 4 == 0 &&
+                         scratch_plane_stride % 4 == 0 && image_row_stride % 4 == 0 && scratch_row_stride % 4 == 0 &&
+                         !kn.force_generic;
+    if (aligned && !kn.split_passes) {
+        SC_TRY(check_strides(nplanes, rows, cols, image_plane_stride, image_row_stride, "image"));
+        SC_TRY(check_strides(nplanes, rows, cols, scratch_plane_stride, scratch_row_stride, "scratch"));
+        SC_TRY(prepare(image));
+        SC_TRY(prepare(scratch));
+        if (overlaps(image, extent_bytes(nplanes, rows, cols, image_plane_stride, image_row_stride), scratch,
+                     extent_bytes(nplanes, rows, cols, scratch_plane_stride, scratch_row_stride)))
+            return fail(SC_INVALID_ARGUMENT, "source and destination must be distinct buffers");
+        if (!taps) return fail(SC_INVALID_ARGUMENT, "null taps");
+        RowsJob j{};
+        j.mode = MODE_SPLITF;
+        j.src = image;
+        j.dst = image;
+        j.sps = image_plane_stride;
+        j.dps = image_plane_stride;
+        j.srs = image_row_stride;
+        j.drs = image_row_stride;
+        j.nplanes = nplanes;
+        j.R = rows;
+        j.C = cols;
+        j.src_row0 = 0;
+        j.src_rows = rows;
+        j.dst_row0 = 0;
+        j.out_lo = 0;
+        j.out_hi = rows;
+        j.hrow_lo = h_lo;
+        j.hrow_hi = h_hi;
+        j.flags = (flags & SC_EXTENDED) | SC_NO_RING;
+        j.width = width;
+        j.taps = taps;
+        j.scr = scratch;
+        j.scr_ps = scratch_plane_stride;
+        j.scr_rs = scratch_row_stride;
+        return launch_rows(j, static_cast<cudaStream_t>(stream));
+    }
     SC_TRY(pass_common(MODE_HPASS, image, scratch, nplanes, rows, cols, image_plane_stride, scratch_plane_stride,
                        image_row_stride, scratch_row_stride, h_lo, h_hi, taps, nullptr, width, SC_ZERO_FILL,
                        stream));

@@ -74,6 +74,53 @@ static __global__ void fill_synthetic_kernel(float* __restrict__ dst, long long 
 }
 
 
+// Split-fused halo snapshot (S/conv.py:392-421 run in place needs the samples
+// other items read before their owners overwrite them): for every band boundary
+// b >= 1 the 2r image rows around it (one warp per row, float4 lanes, four
+// loads in flight), for every strip boundary s >= 1 the 8 columns around it in
+// every row (one thread per row: two float4s). Aligned rows only.
+static __global__ void __launch_bounds__(256) split_snapshot_kernel(const SnapJob j) {
+    const int lane = threadIdx.x & 31;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * blockDim.x;
+    const int c4 = j.C / 4, r2 = 2 * j.rad;
+    const long long ntask = (long long)j.nplanes * j.nb * r2;
+    for (long long task = tid >> 5; task < ntask; task += nthreads >> 5) {
+        const int t = (int)(task % r2);
+        const long long q = task / r2;
+        const int b = (int)(q % j.nb);
+        const int pl = (int)(q / j.nb);
+        if (b == 0) continue;
+        const int lo = b < j.nb1 ? j.lo1 + b * j.bh1 : j.lo2 + (b - j.nb1) * j.bh2;
+        const int y = lo - j.rad + t;
+        if (y < 0 || y >= j.R) continue;
+        const float4* src = reinterpret_cast<const float4*>(j.img + pl * j.ps + (long long)y * j.rs);
+        float4* dst = reinterpret_cast<float4*>(j.side_rows + (((long long)pl * j.nb + b) * r2 + t) * j.C);
+        int i = lane;
+        for (; i + 96 < c4; i += 128) {
+            const float4 v0 = src[i], v1 = src[i + 32], v2 = src[i + 64], v3 = src[i + 96];
+            dst[i] = v0;
+            dst[i + 32] = v1;
+            dst[i + 64] = v2;
+            dst[i + 96] = v3;
+        }
+        for (; i < c4; i += 32) dst[i] = src[i];
+    }
+    const int nsb = j.nstrips - 1;
+    const long long ncol = (long long)j.nplanes * nsb * j.R;
+    for (long long i = tid; i < ncol; i += nthreads) {
+        const int y = (int)(i % j.R);
+        const long long q = i / j.R;
+        const int s = (int)(q % nsb) + 1;
+        const int pl = (int)(q / nsb);
+        const float4* src = reinterpret_cast<const float4*>(j.img + pl * j.ps + (long long)y * j.rs + s * j.tw - 4);
+        float4* dst = reinterpret_cast<float4*>(j.side_cols + i * 8);  // i == ((pl * nsb + s - 1) * R + y)
+        const float4 a = src[0], c = src[1];
+        dst[0] = a;
+        dst[1] = c;
+    }
+}
+
 static int grid_for(long long total, int threads) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -93,6 +140,14 @@ cudaError_t launch_copy_region(const float* src, float* dst, long long sps, long
     // one warp per row: up to 8 warps x 8 CTAs per SM
     copy_region_kernel<<<grid_for((long long)nplanes * nrows * 32, 256), 256, 0, s>>>(
         src, dst, sps, dps, srs, drs, nplanes, row_lo, nrows, col_lo, ncols);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split_snapshot(const SnapJob& j, cudaStream_t s) {
+    const long long work = (long long)j.nplanes * j.nb * 2 * j.rad * 32 + (long long)j.nplanes * (j.nstrips - 1) * j.R;
+    if (work <= 0) return cudaSuccess;
+    split_snapshot_kernel<<<grid_for(work, 256), 256, 0, s>>>(j);
     count_launch();
     return cudaGetLastError();
 }

@@ -23,6 +23,18 @@ const void* kernel_fused(int rad, bool aligned) {
 #undef SC_K
 }
 
+// Split-fused (the reference's exact scratch end state in one pass; aligned rows only).
+const void* kernel_splitf(int rad) {
+    switch (rad) {
+        case 0: return (const void*)sepconv_rows_kernel<MODE_SPLITF, 0, true>;
+        case 1: return (const void*)sepconv_rows_kernel<MODE_SPLITF, 1, true>;
+        case 2: return (const void*)sepconv_rows_kernel<MODE_SPLITF, 2, true>;
+        case 3: return (const void*)sepconv_rows_kernel<MODE_SPLITF, 3, true>;
+        case 4: return (const void*)sepconv_rows_kernel<MODE_SPLITF, 4, true>;
+        default: return nullptr;
+    }
+}
+
 const void* kernel_fused_direct(int rad) {
     switch (rad) {
         case 0: return (const void*)sepconv_direct_kernel<MODE_FUSED, 0>;

@@ -200,7 +200,6 @@ __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, 
 template <int RAD>
 __global__ void __launch_bounds__(SC_U8_MAXT, SC_U8_MINB) sepconv_u8_kernel(const __grid_constant__ U8Params p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
     const int NS = p.ns;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* empty = full + NS;

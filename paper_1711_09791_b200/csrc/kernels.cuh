@@ -9,6 +9,12 @@
 //   MODE_HPASS  horizontal_rows_vec                       S/conv.py:215-240
 //   MODE_VPASS  vertical_rows_vec                         S/conv.py:269-293
 //   MODE_SINGLE single_pass_rows_vec / unrolled5_rows_vec S/conv.py:86-114, :146-175
+//   MODE_SPLITF conv_two_pass with the reference's buffer end state (scratch :=
+//               H0, image[valid] := V(H0) in place), fused: one read of the
+//               image, one write of scratch, one write of the image. Samples of
+//               OTHER items' regions (row and column halos) come from a
+//               snapshot taken before the launch (split_snapshot_kernel), since
+//               their owners overwrite them in place.
 //
 // Work decomposition: an "item" is (plane, column strip of TW = 4*GROUPS*NT
 // output columns, row band). A persistent grid claims items from an atomic
@@ -43,7 +49,9 @@
 
 namespace sc {
 
-enum Mode : int { MODE_FUSED = 0, MODE_HPASS = 1, MODE_VPASS = 2, MODE_SINGLE = 3 };
+enum Mode : int { MODE_FUSED = 0, MODE_HPASS = 1, MODE_VPASS = 2, MODE_SINGLE = 3, MODE_SPLITF = 4 };
+// modes that run the row pass on the staged input and fold it down the columns
+__host__ __device__ constexpr bool fused_like(int mode) { return mode == MODE_FUSED || mode == MODE_SPLITF; }
 
 // flags (mirrors include/sepconv_b200.h)
 constexpr int F_EXTENDED = 0x1;
@@ -92,6 +100,16 @@ struct Params {
     const float* below;
     long long above_ps, above_rs, below_ps, below_rs;
     int above_row0, below_row0;  // global row of row 0 of above / below
+    // MODE_SPLITF: the scratch planes (global rows, H0 written for every own row)
+    // and the halo snapshot: side_rows[((plane * side_nb + b) * 2r + t) * C + x] =
+    // image row lo_b - r + t of band boundary b (b = band ordinal >= 1, lo_b its
+    // first row); side_cols[((plane * (nstrips - 1) + s - 1) * R + y) * 8 + i] =
+    // image column s * tw - 4 + i of row y (strip boundary s >= 1)
+    float* scr;
+    long long scr_ps, scr_rs;
+    const float* side_rows;
+    const float* side_cols;
+    int side_nb;
     float w[MAX_W];
     float k[MAX_W * MAX_W];
 };
@@ -279,23 +297,27 @@ __device__ __forceinline__ int row_width(int tw) {
 
 struct Item {
     int plane, x0, ylo, yhi, in_lo, in_hi;
+    int strip, band;  // strip index, band ordinal over both segments
 };
 
 template <int MODE, int RAD>
 __device__ __forceinline__ Item decode_item(const Params& p, int item) {
     const int units = p.nplanes * p.nstrips;
-    int seg_lo = p.out_lo, seg_hi = p.out_hi, bh = p.band_h;
+    int seg_lo = p.out_lo, seg_hi = p.out_hi, bh = p.band_h, band0 = 0;
     if (item >= p.nitems0) {
         item -= p.nitems0;
         seg_lo = p.out_lo2;
         seg_hi = p.out_hi2;
         bh = p.band_h2;
+        band0 = p.nitems0 / units;
     }
     const int band = item / units;
     const int rem = item - band * units;
     Item it;
     it.plane = rem / p.nstrips;
     const int strip = rem - it.plane * p.nstrips;
+    it.strip = strip;
+    it.band = band0 + band;
     it.x0 = strip * p.tw;
     it.ylo = seg_lo + band * bh;
     it.yhi = min(it.ylo + bh, seg_hi);
@@ -314,7 +336,7 @@ __device__ __forceinline__ Item decode_item(const Params& p, int item) {
 template <int MODE, int RAD>
 __device__ __forceinline__ bool item_rows_edge(const Params& p, const Item& it) {
     if (MODE == MODE_HPASS) return it.ylo < p.hrow_lo || it.yhi > p.hrow_hi;
-    if (MODE == MODE_FUSED)
+    if (fused_like(MODE))
         return it.in_lo < p.hrow_lo || it.in_hi > p.hrow_hi || it.ylo < RAD || it.yhi > p.R - RAD;
     return false;
 }
@@ -399,7 +421,40 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
             const int nrows = min(SROWS, it.in_hi - r0);
             float* sbase = ring + slot * SROWS * SW + soff;
             sitem[slot] = item;
-            if (ALIGNED) {
+            if (MODE == MODE_SPLITF) {
+                // own rows: the item's own columns from the image (nobody else writes
+                // them), the 4-column halos from the column snapshot; halo rows (other
+                // bands' rows) wholly from the row snapshot
+                static_assert(MODE != MODE_SPLITF || ALIGNED, "split-fused runs aligned rows only");
+                const int xr = min(it.x0 + p.tw, p.C);
+                const bool lh = it.strip > 0, rh = it.strip + 1 < p.nstrips;
+                uint32_t total = 0;
+                for (int k = 0; k < nrows; ++k) {
+                    const int y = r0 + k;
+                    total += (y >= it.ylo && y < it.yhi) ? 4u * (uint32_t)(xr - it.x0) + (lh ? 16u : 0u) + (rh ? 16u : 0u)
+                                                         : (uint32_t)n * 4u;
+                }
+                mbar_arrive_expect_tx(&full[slot], total);
+                for (int k = 0; k < nrows; ++k) {
+                    const int y = r0 + k;
+                    float* srow = sbase + k * SW;  // column cx0
+                    if (y >= it.ylo && y < it.yhi) {
+                        float* mid = srow + (it.x0 - cx0);
+                        bulk_g2s(mid, src_row(p, it.plane, y) + it.x0, 4u * (uint32_t)(xr - it.x0), &full[slot], pol);
+                        const long long cb = ((long long)it.plane * (p.nstrips - 1) - 1) * p.R + y;
+                        if (lh) bulk_g2s(mid - 4, p.side_cols + (cb + (long long)it.strip * p.R) * 8, 16u, &full[slot], pol);
+                        if (rh)
+                            bulk_g2s(mid + (xr - it.x0), p.side_cols + (cb + (long long)(it.strip + 1) * p.R) * 8 + 4,
+                                     16u, &full[slot], pol);
+                    } else {
+                        const int b = y < it.ylo ? it.band : it.band + 1;  // boundary at this band's top / bottom
+                        const int t = y < it.ylo ? y - (it.ylo - RAD) : y - (it.yhi - RAD);
+                        const float* side =
+                            p.side_rows + (((long long)it.plane * p.side_nb + b) * (2 * RAD) + t) * (long long)p.C;
+                        bulk_g2s(srow, side + cx0, (uint32_t)n * 4u, &full[slot], pol);
+                    }
+                }
+            } else if (ALIGNED) {
                 const uint32_t bytes = (uint32_t)n * 4u;
                 mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
                 for (int k = 0; k < nrows; ++k)
@@ -794,7 +849,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
     constexpr int GROUPS = groups_of(MODE);
     const int tw2 = p.tw / GROUPS;  // column offset between a thread's groups
     const int R = p.R, C = p.C;
-    const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);
+    const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);  // SPLITF: image ring untouched
     const bool zero_fill = (MODE == MODE_HPASS) && (p.flags & F_ZERO_FILL);
     // unaligned kernels with 16-B aligned destination rows (only the source is
     // misaligned) store directly; staging pays only when the stores are unaligned
@@ -878,7 +933,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                             outv = dense_fold<RAD, NACC>(acc[g], win, p.k, p.one);
                     } else {
                         F4 v;
-                        if (MODE == MODE_FUSED) {
+                        if (fused_like(MODE)) {
                             if (live) {
 #ifdef SC_NOCOMPUTE
                                 v = own;
@@ -891,6 +946,22 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                             }
                         } else {
                             v = own;  // VPASS: src already holds the row-pass result
+                        }
+                        if constexpr (MODE == MODE_SPLITF) {
+                            // the reference's scratch row: H0 on the valid columns, 0 on the
+                            // column ring and on dead rows (the workspace is zeroed first,
+                            // S/conv.py:414); own rows only
+                            if (yi >= it.ylo && yi < it.yhi) {
+                                float* hrow = p.scr + (long long)it.plane * p.scr_ps + (long long)yi * p.scr_rs;
+                                if (fast[g]) {
+                                    st4(hrow + x4[g], v);
+                                } else {
+                                    F4 zero;
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) zero.v[i] = 0.0f;
+                                    store_edge<ALIGNED>(hrow, x4[g], C, RAD, v, zero, 2);
+                                }
+                            }
                         }
 #ifdef SC_NOCOMPUTE
                         outv = v;  // dev-only variant: pipeline cost without the arithmetic

@@ -15,6 +15,7 @@ const void* kernel_fused(int rad, bool aligned);
 const void* kernel_hpass(int rad, bool aligned);
 const void* kernel_vpass(int rad, bool aligned);
 const void* kernel_single(int rad, bool aligned, bool sym = false);
+const void* kernel_splitf(int rad);
 const void* kernel_fused_direct(int rad);
 const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);
@@ -29,6 +30,17 @@ cudaError_t launch_planes_to_hwc(const float* src, uint8_t* dst, long long sps, 
 cudaError_t launch_copy_region(const float* src, float* dst, long long sps, long long dps, long long srs,
                                long long drs, int nplanes, int row_lo, int nrows, int col_lo, int ncols,
                                cudaStream_t s);
+// Halo snapshot of the split-fused kernel (layout: Params::side_rows / side_cols).
+struct SnapJob {
+    const float* img;
+    long long ps, rs;
+    int nplanes, R, C, rad;
+    int tw, nstrips;
+    int lo1, bh1, nb1, lo2, bh2, nb;  // band b's first row: b < nb1 ? lo1 + b*bh1 : lo2 + (b-nb1)*bh2
+    float* side_rows;
+    float* side_cols;
+};
+cudaError_t launch_split_snapshot(const SnapJob& j, cudaStream_t s);
 cudaError_t launch_fill_synthetic(float* dst, long long count, uint64_t seed, uint64_t offset, int kind,
                                   cudaStream_t s);
 
@@ -52,6 +64,9 @@ struct RowsJob {
     const float* below = nullptr;
     long long above_ps = 0, above_rs = 0, below_ps = 0, below_rs = 0;
     int above_row0 = 0, above_rows = 0, below_row0 = 0, below_rows = 0;
+    // MODE_SPLITF: scratch planes (H0), same rows as the image
+    float* scr = nullptr;
+    long long scr_ps = 0, scr_rs = 0;
 };
 
 // Plans and launches one row-streaming kernel; returns an SC_* status and sets

@@ -6,7 +6,7 @@
 
 Every kernel family of the path runs on the same seeded image: fused two-pass
 (K1), row pass with zero fill and column pass (the split pair K2/K3), single
-pass (and its copy-back), and the PPM u8 payload kernel. For each the
+pass (and its copy-back), the one-pass split mode, and the PPM u8 payload kernel. For each the
 ALGORITHMIC bytes are the minimum one launch must move (a read of every input
 sample it needs once, a write of every output sample), so `alg GB/s` is what
 the roofline fraction uses; ncu's dram__bytes show the real traffic.
@@ -14,7 +14,7 @@ the roofline fraction uses; ncu's dram__bytes show the real traffic.
 import argparse, csv, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-OPS = ["fused", "hpass_zero", "vpass", "single", "single_copyback", "u8"]
+OPS = ["fused", "split", "hpass_zero", "vpass", "single", "single_copyback", "u8"]
 
 
 def build_ops(cfg):
@@ -37,6 +37,8 @@ def build_ops(cfg):
     ops = {
         # op: (callable, algorithmic bytes per launch, what)
         "fused": (lambda: dev.two_pass(x, w, y), 8 * n_px, "read image + write image"),
+        "split": (lambda: dev.two_pass_split(y, z, w), 12 * n_px,
+                  "read image + write scratch + write image (the reference's buffer end state)"),
         "hpass_zero": (lambda: dev.hpass(x, w, y, 0, R, zero_fill=True), 8 * n_px,
                        "read image + write scratch (all rows, ring zeroed)"),
         "vpass": (lambda: dev.vpass(y, w, z), 4 * n_px + 4 * valid, "read scratch + write valid region"),
