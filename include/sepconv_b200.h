@@ -114,9 +114,13 @@ int sc_vpass_f32(const float *src, float *dst, int nplanes, int rows, int cols,
                  int64_t src_row_stride, int64_t dst_row_stride,
                  int row_lo, int row_hi, const float *taps, int width, int flags, void *stream);
 
-/* The reference two-pass with its exact buffer semantics, two launches:
- * scratch := H0 (zero outside the row-pass region), then image[valid] := V(scratch).
- * image ring untouched. conv_two_pass(plane, kernel, scratch, extended), S/conv.py:392-421. */
+/* The reference two-pass with its exact buffer semantics: scratch := H0 (zero
+ * outside the row-pass region), image[valid] := V(H0), image ring untouched.
+ * conv_two_pass(plane, kernel, scratch, extended), S/conv.py:392-421.
+ * 16-B aligned rows: ONE pass (image read once, both buffers written once; a
+ * snapshot of the band/strip boundary samples is taken first, in a pooled
+ * stream-ordered allocation). Otherwise, or with SC_SPLIT_PASSES=1: the row pass
+ * with zero fill, then the column pass. */
 int sc_two_pass_split_f32(float *image, float *scratch, int nplanes, int rows, int cols,
                           int64_t image_plane_stride, int64_t scratch_plane_stride,
                           int64_t image_row_stride, int64_t scratch_row_stride,
