@@ -404,7 +404,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     // (measured: -17% at cfg5 size; the same reuse in the two-pass column fold
     // measured 0-3% slower, so the two-pass modes do not use it)
     bool sym = false;
-    if (!kn.no_sym && j.mode == MODE_SINGLE && j.dense) {
+    if (!kn.no_sym && (j.mode == MODE_SINGLE || j.mode == MODE_SINGLECB) && j.dense) {
         const int W = j.width;
         auto same = [](float a, float b) { return std::memcmp(&a, &b, sizeof(float)) == 0; };
         sym = true;
@@ -420,6 +420,10 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
             if (!aligned) return fail(SC_INVALID_ARGUMENT, "split-fused kernel needs 16-B aligned rows");
             kern = kernel_splitf(rad);
             break;
+        case MODE_SINGLECB:
+            if (!aligned) return fail(SC_INVALID_ARGUMENT, "in-place copy-back kernel needs 16-B aligned rows");
+            kern = kernel_single_cb(rad, sym);
+            break;
     }
     if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(j.width));
     const bool seg2 = j.out_hi2 > j.out_lo2;
@@ -427,7 +431,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
 
     // Kernel family: the TMA stage pipeline (default) or the register-streaming
     // direct kernel (SC_DIRECT=1), both bit-identical.
-    const bool direct = aligned && kn.direct != 0 && !j.above && !j.below && j.mode != MODE_SPLITF;  // direct reads src only
+    const bool direct = aligned && kn.direct != 0 && !j.above && !j.below && j.mode != MODE_SPLITF &&
+                        j.mode != MODE_SINGLECB;  // direct reads src only
     if (direct) {
         switch (j.mode) {
             case MODE_FUSED: kern = kernel_fused_direct(rad); break;
@@ -494,7 +499,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.work = work_slot(dev);
     if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
     float* side = nullptr;
-    if (j.mode == MODE_SPLITF) {
+    if (j.mode == MODE_SPLITF || j.mode == MODE_SINGLECB) {
         // halo snapshot: stream-ordered scratch from the device's default pool
         // (kept pooled: release threshold raised once), taken right before the launch
         p.scr = j.scr;
@@ -520,6 +525,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         p.side_rows = side;
         p.side_cols = side + rows_f;
         p.side_nb = nb;
+        p.snap_lo = pl.lo1;
+        p.snap_hi = pl.hi2 > pl.lo2 ? pl.hi2 : pl.hi1;
         SnapJob sj{};
         sj.img = j.src;
         sj.ps = j.sps;
@@ -916,7 +923,7 @@ static int pass_common(int mode, const float* src, float* dst, int nplanes, int 
                        const float* dense, int width, int flags, void* stream) {
     SC_TRY(check_width(width));
     SC_TRY(check_dims(nplanes, rows, cols, width));
-    if (mode == MODE_SINGLE ? !dense : !taps) return fail(SC_INVALID_ARGUMENT, "null taps");
+    if (single_like(mode) ? !dense : !taps) return fail(SC_INVALID_ARGUMENT, "null taps");
     SC_TRY(check_strides(nplanes, rows, cols, sps, srs, "src"));
     SC_TRY(check_strides(nplanes, rows, cols, dps, drs, "dst"));
     const int r = width / 2;
@@ -958,9 +965,14 @@ static int pass_common(int mode, const float* src, float* dst, int nplanes, int 
     j.width = width;
     j.taps = taps;
     j.dense = dense;
-    if (mode == MODE_SINGLE) {
+    if (single_like(mode)) {
         static float zeros[MAX_W] = {0};
         j.taps = zeros;
+    }
+    if (mode == MODE_SINGLECB) {  // second destination: the source image itself (copy-back, in place)
+        j.scr = const_cast<float*>(src);
+        j.scr_ps = sps;
+        j.scr_rs = srs;
     }
     return launch_rows(j, static_cast<cudaStream_t>(stream));
 }
@@ -1045,6 +1057,15 @@ int sc_single_pass_f32(float* src, float* dst, int nplanes, int rows, int cols, 
     SC_TRY(check_width(width));
     SC_TRY(check_dims(nplanes, rows, cols, width));
     const int r = width / 2;
+    const Knobs kn = read_knobs();
+    const bool aligned = cols % 4 == 0 && aligned16(src) && aligned16(dst) && src_plane_stride % 4 == 0 &&
+                         dst_plane_stride % 4 == 0 && src_row_stride % 4 == 0 && dst_row_stride % 4 == 0 &&
+                         !kn.force_generic && !kn.direct;
+    if ((flags & SC_COPY_BACK) && aligned && !kn.split_passes) {
+        // one pass: the valid region into the workspace and back into the image
+        return pass_common(MODE_SINGLECB, src, dst, nplanes, rows, cols, src_plane_stride, dst_plane_stride,
+                           src_row_stride, dst_row_stride, r, rows - r, nullptr, dense, width, flags, stream);
+    }
     SC_TRY(pass_common(MODE_SINGLE, src, dst, nplanes, rows, cols, src_plane_stride, dst_plane_stride,
                        src_row_stride, dst_row_stride, r, rows - r, nullptr, dense, width, flags, stream));
     if (flags & SC_COPY_BACK) {

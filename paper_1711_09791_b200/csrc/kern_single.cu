@@ -28,6 +28,25 @@ const void* kernel_single(int rad, bool aligned, bool sym) {
 #undef SC_K
 }
 
+// Single pass + in-place copy-back in one pass (aligned rows only).
+const void* kernel_single_cb(int rad, bool sym) {
+    sym = sym && rad >= 1;
+#define SC_K(R)                                                                                          \
+    case R:                                                                                              \
+        return sym ? (const void*)sepconv_rows_kernel<MODE_SINGLECB, R, true, (R >= 1)>                  \
+                   : (const void*)sepconv_rows_kernel<MODE_SINGLECB, R, true>;
+    switch (rad) {
+        SC_K(0)
+        SC_K(1)
+        SC_K(2)
+        SC_K(3)
+        SC_K(4)
+        default:
+            return nullptr;
+    }
+#undef SC_K
+}
+
 const void* kernel_single_direct(int rad) {
     switch (rad) {
         case 0: return (const void*)sepconv_direct_kernel<MODE_SINGLE, 0>;

@@ -15,6 +15,9 @@
 //               OTHER items' regions (row and column halos) come from a
 //               snapshot taken before the launch (split_snapshot_kernel), since
 //               their owners overwrite them in place.
+//   MODE_SINGLECB the single pass with copy-back (S/executors.py:330-331) in one
+//               pass: the valid region goes to the workspace AND back into the
+//               image in place, halos from the same snapshot.
 //
 // Work decomposition: an "item" is (plane, column strip of TW = 4*GROUPS*NT
 // output columns, row band). A persistent grid claims items from an atomic
@@ -49,9 +52,12 @@
 
 namespace sc {
 
-enum Mode : int { MODE_FUSED = 0, MODE_HPASS = 1, MODE_VPASS = 2, MODE_SINGLE = 3, MODE_SPLITF = 4 };
+enum Mode : int { MODE_FUSED = 0, MODE_HPASS = 1, MODE_VPASS = 2, MODE_SINGLE = 3, MODE_SPLITF = 4, MODE_SINGLECB = 5 };
 // modes that run the row pass on the staged input and fold it down the columns
 __host__ __device__ constexpr bool fused_like(int mode) { return mode == MODE_FUSED || mode == MODE_SPLITF; }
+__host__ __device__ constexpr bool single_like(int mode) { return mode == MODE_SINGLE || mode == MODE_SINGLECB; }
+// modes that overwrite their own source in place: other items' halos come from the snapshot
+__host__ __device__ constexpr bool snap_mode(int mode) { return mode == MODE_SPLITF || mode == MODE_SINGLECB; }
 
 // flags (mirrors include/sepconv_b200.h)
 constexpr int F_EXTENDED = 0x1;
@@ -100,8 +106,10 @@ struct Params {
     const float* below;
     long long above_ps, above_rs, below_ps, below_rs;
     int above_row0, below_row0;  // global row of row 0 of above / below
-    // MODE_SPLITF: the scratch planes (global rows, H0 written for every own row)
-    // and the halo snapshot: side_rows[((plane * side_nb + b) * 2r + t) * C + x] =
+    // MODE_SPLITF: the scratch planes (global rows, H0 written for every own row);
+    // MODE_SINGLECB: the image (second destination of the valid region). Both:
+    // rows [snap_lo, snap_hi) are written by some item (outside them the image is
+    // never written and is read directly), and the halo snapshot: side_rows[((plane * side_nb + b) * 2r + t) * C + x] =
     // image row lo_b - r + t of band boundary b (b = band ordinal >= 1, lo_b its
     // first row); side_cols[((plane * (nstrips - 1) + s - 1) * R + y) * 8 + i] =
     // image column s * tw - 4 + i of row y (strip boundary s >= 1)
@@ -110,6 +118,7 @@ struct Params {
     const float* side_rows;
     const float* side_cols;
     int side_nb;
+    int snap_lo, snap_hi;
     float w[MAX_W];
     float k[MAX_W * MAX_W];
 };
@@ -285,7 +294,7 @@ __device__ __forceinline__ void st4(float* p, const F4& a) {
 #define SC_SROWS 4
 #endif
 constexpr int SROWS = SC_SROWS;
-__host__ __device__ constexpr int groups_of(int mode) { return mode == MODE_SINGLE ? SC_GROUPS_SINGLE : SC_GROUPS; }
+__host__ __device__ constexpr int groups_of(int mode) { return single_like(mode) ? SC_GROUPS_SINGLE : SC_GROUPS; }
 
 // Shared-memory row width (floats): the segment [x0-4, x0+TW+4), plus room for
 // the 16-B realignment of unaligned rows (up to 3 floats before and after, and
@@ -421,18 +430,18 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
             const int nrows = min(SROWS, it.in_hi - r0);
             float* sbase = ring + slot * SROWS * SW + soff;
             sitem[slot] = item;
-            if (MODE == MODE_SPLITF) {
+            if (snap_mode(MODE)) {
                 // own rows: the item's own columns from the image (nobody else writes
                 // them), the 4-column halos from the column snapshot; halo rows (other
                 // bands' rows) wholly from the row snapshot
-                static_assert(MODE != MODE_SPLITF || ALIGNED, "split-fused runs aligned rows only");
+                static_assert(!snap_mode(MODE) || ALIGNED, "in-place modes run aligned rows only");
                 const int xr = min(it.x0 + p.tw, p.C);
                 const bool lh = it.strip > 0, rh = it.strip + 1 < p.nstrips;
                 uint32_t total = 0;
                 for (int k = 0; k < nrows; ++k) {
                     const int y = r0 + k;
                     total += (y >= it.ylo && y < it.yhi) ? 4u * (uint32_t)(xr - it.x0) + (lh ? 16u : 0u) + (rh ? 16u : 0u)
-                                                         : (uint32_t)n * 4u;
+                                                         : (uint32_t)n * 4u;  // halo rows: one full-width copy
                 }
                 mbar_arrive_expect_tx(&full[slot], total);
                 for (int k = 0; k < nrows; ++k) {
@@ -446,6 +455,9 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
                         if (rh)
                             bulk_g2s(mid + (xr - it.x0), p.side_cols + (cb + (long long)(it.strip + 1) * p.R) * 8 + 4,
                                      16u, &full[slot], pol);
+                    } else if (y < p.snap_lo || y >= p.snap_hi) {
+                        // a row no item writes (the single pass's ring rows): the image itself
+                        bulk_g2s(srow, src_row(p, it.plane, y) + cx0, (uint32_t)n * 4u, &full[slot], pol);
                     } else {
                         const int b = y < it.ylo ? it.band : it.band + 1;  // boundary at this band's top / bottom
                         const int t = y < it.ylo ? y - (it.ylo - RAD) : y - (it.yhi - RAD);
@@ -926,7 +938,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 #pragma unroll
                             for (int i = 0; i < 4; ++i) outv.v[i] = 0.0f;
                         }
-                    } else if (MODE == MODE_SINGLE) {
+                    } else if (single_like(MODE)) {
                         if constexpr (SYM && SC_F2 && RAD >= 1)
                             outv = dense_fold_sym<RAD, NACC>(acc[g], win, p.k, p.one);
                         else
@@ -982,6 +994,18 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                                 store_edge<ALIGNED>(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
                         }
                     } else if (emit) {
+                        if constexpr (MODE == MODE_SINGLECB) {
+                            // copy-back: the same valid samples into the image, in place
+                            float* irow = p.scr + (long long)it.plane * p.scr_ps + (long long)yo * p.scr_rs;
+                            if (fast[g]) {
+                                st4(irow + x4[g], outv);
+                            } else {
+                                F4 zero;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) zero.v[i] = 0.0f;
+                                store_edge<ALIGNED>(irow, x4[g], C, RAD, outv, zero, 0);
+                            }
+                        }
                         if (fast[g]) {
                             st4(dcur + x4[g], outv);
                         } else {

@@ -16,6 +16,7 @@ const void* kernel_hpass(int rad, bool aligned);
 const void* kernel_vpass(int rad, bool aligned);
 const void* kernel_single(int rad, bool aligned, bool sym = false);
 const void* kernel_splitf(int rad);
+const void* kernel_single_cb(int rad, bool sym);
 const void* kernel_fused_direct(int rad);
 const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);
@@ -64,7 +65,7 @@ struct RowsJob {
     const float* below = nullptr;
     long long above_ps = 0, above_rs = 0, below_ps = 0, below_rs = 0;
     int above_row0 = 0, above_rows = 0, below_row0 = 0, below_rows = 0;
-    // MODE_SPLITF: scratch planes (H0), same rows as the image
+    // MODE_SPLITF: scratch planes (H0); MODE_SINGLECB: the image (copy-back); same rows
     float* scr = nullptr;
     long long scr_ps = 0, scr_rs = 0;
 };
