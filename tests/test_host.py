@@ -265,3 +265,38 @@ def test_packed_math_keeps_two_roundings():
         sym = re.search(r"sepconv_rows_kernelILi\d+ELi\d+ELb[01]ELb1E", fn) is not None
         limit = 2 * fmul2 if sym else fmul2
         assert ffma2 <= limit, f"{fn}: {ffma2} FFMA2 vs {fmul2} FMUL2 -- contraction suspected"
+
+
+def test_two_pass_kernels_keep_four_ctas_per_sm():
+    """Regression guard on occupancy: the r = 2 two-pass kernels (fused, row pass,
+    column pass, one-pass split; aligned and unaligned) run 160-thread CTAs, 4 per
+    SM only while they need <= 96 registers (5 warps x 96 x 32 x 4 <= 64K). An
+    innocent-looking change (two int fields inserted before the taps in Params)
+    once moved the aligned fused kernel from 76 to 84 registers and the unaligned
+    one to 102 (3 CTAs/SM, 13-20% slower)."""
+    import shutil
+    import subprocess
+
+    from paper_1711_09791_b200 import _lib
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-res-usage", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    regs, current = {}, None
+    for line in out.splitlines():
+        m = re.search(r"Function (\S+):", line)
+        if m:
+            current = m.group(1)
+        elif current and "REG:" in line:
+            regs[current] = int(re.search(r"REG:(\d+)", line).group(1))
+    checked = 0
+    for fn, n in regs.items():
+        m = re.search(r"sepconv_rows_kernelILi([0124])ELi2ELb([01])E", fn)
+        if not m:
+            continue
+        checked += 1
+        assert n <= 96, f"{fn}: {n} registers (> 96: fewer than 4 CTAs/SM)"
+        if m.group(1) == "0" and m.group(2) == "1":
+            assert n <= 80, f"aligned fused kernel {fn}: {n} registers (was 76)"
+    assert checked >= 7
