@@ -364,6 +364,17 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     pl.nitems = (int)nitems;
     pl.nitems0 = (int)nitems0;
     pl.grid = (int)(ctas < (long long)di.sms * occ ? ctas : (long long)di.sms * occ);
+    // The FP32-bound single pass (8 columns per thread: a 4-stage ring of 1032-float
+    // rows is 66 KB, 3 CTAs/SM) runs better with one stage less and a 4th CTA once
+    // every CTA has several items (measured: 3x8192^2 -3.7%, 3x16384^2 -4.4%,
+    // 512 x 3x1080x1920 -5..7%); with ~1-2 items per CTA (3x4096^2) the shallower
+    // ring loses (+4-6%).
+    if (single_like(j.mode) && !direct && kn.ns == 0 && ns == 16 / SROWS && pl.nitems >= 4LL * pl.grid) {
+        Knobs k3 = kn;
+        k3.ns = 3;
+        Plan p3;
+        if (plan_rows(j, kern, aligned, direct, dev, k3, p3) == SC_OK && p3.occ > pl.occ) pl = p3;
+    }
     return SC_OK;
 }
 
