@@ -232,3 +232,37 @@ def test_random_larger_shapes(oracle, monkeypatch, P, R, C, width, seed, generic
     out = torch.zeros_like(xd)
     dev.single_pass(xd, dense, out)
     assert bits(out.cpu().numpy(), oracle.single_pass(x, dense))
+
+
+@settings(max_examples=25 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(P=st.integers(1, 3), R=st.integers(20, 1200), C4=st.integers(2, 700), width=widths,
+       seed=st.integers(0, 2**32 - 1), extended=st.booleans(), sym=st.booleans())
+def test_random_in_place_one_pass_modes(oracle, P, R, C4, width, seed, extended, sym):
+    """The in-place one-pass kernels on 16-B aligned rows (C % 4 == 0) with
+    planner-chosen strips and head/tail bands: the split two-pass (scratch H0 +
+    image V) and the single pass with copy-back (workspace + image), whose other
+    items' halos come from the pre-launch snapshot. Both buffers bit-exact."""
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    C = 4 * C4
+    if R < width or C < width:
+        return
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(-2, 2, size=width).astype(np.float32)
+    if sym:
+        w = ((w + w[::-1]) / np.float32(2)).astype(np.float32)
+    x = rng.uniform(-300, 300, size=(P, R, C)).astype(np.float32)
+    img, scr = torch.from_numpy(x).cuda(), torch.full((P, R, C), 5.0, device="cuda")
+    dev.two_pass_split(img, scr, w, extended=extended)
+    assert bits(img.cpu().numpy(), oracle.two_pass(x, w, extended=extended))
+    assert bits(scr.cpu().numpy(), oracle.two_pass_scratch(x, w, extended=extended))
+    dense = oracle.outer_product(w)
+    img, ws = torch.from_numpy(x).cuda(), torch.full((P, R, C), -5.0, device="cuda")
+    dev.single_pass(img, dense, ws, copy_back=True)
+    want = oracle.single_pass(x, dense, np.full((P, R, C), -5.0, np.float32))
+    r = width // 2
+    exp = x.copy()
+    exp[:, r:R - r, r:C - r] = want[:, r:R - r, r:C - r]
+    assert bits(ws.cpu().numpy(), want)
+    assert bits(img.cpu().numpy(), exp)
