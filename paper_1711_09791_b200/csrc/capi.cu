@@ -47,7 +47,7 @@ static int cuda_fail(cudaError_t e, const char* what) {
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
     int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
-    int no_sym = 0, no_pdl = 0, split_passes = 0;
+    int no_sym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0;
 };
 
 static Knobs read_knobs() {
@@ -75,6 +75,7 @@ static Knobs read_knobs() {
         else if (name == "NO_SYM") k.no_sym = v;
         else if (name == "NO_PDL") k.no_pdl = v;
         else if (name == "SPLIT_PASSES") k.split_passes = v;
+        else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;  // test hook: as if the allocation failed
     }
     return k;
 }
@@ -378,6 +379,10 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     return SC_OK;
 }
 
+// launch_rows status: the one-pass in-place modes could not get their snapshot
+// buffer; the entry point runs the equivalent two-launch path instead
+static constexpr int kNeedTwoLaunches = -100;
+
 static int cached_plan(const RowsJob& j, const void* kern, bool aligned, bool direct, int dev, const Knobs& kn,
                        Plan& pl) {
     static std::mutex mu;
@@ -531,8 +536,15 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
                 }
                 cudaGetLastError();
             });
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&side), (rows_f + cols_f + 4) * sizeof(float), s);
-        if (e != cudaSuccess) return cuda_fail(e, "split snapshot allocation");
+        cudaError_t e = kn.snapshot_fail ? cudaErrorMemoryAllocation
+                                         : cudaMallocAsync(reinterpret_cast<void**>(&side),
+                                                           (rows_f + cols_f + 4) * sizeof(float), s);
+        if (e != cudaSuccess) {
+            // no room (or no stream-ordered allocator): the caller falls back to two launches
+            cudaGetLastError();
+            set_error(std::string("split snapshot allocation: ") + cudaGetErrorString(e));
+            return kNeedTwoLaunches;
+        }
         p.side_rows = side;
         p.side_cols = side + rows_f;
         p.side_nb = nb;
@@ -1052,7 +1064,9 @@ int sc_two_pass_split_f32(float* image, float* scratch, int nplanes, int rows, i
         j.scr = scratch;
         j.scr_ps = scratch_plane_stride;
         j.scr_rs = scratch_row_stride;
-        return launch_rows(j, static_cast<cudaStream_t>(stream));
+        const int rc = launch_rows(j, static_cast<cudaStream_t>(stream));
+        if (rc != kNeedTwoLaunches) return rc;
+        set_error("");
     }
     SC_TRY(pass_common(MODE_HPASS, image, scratch, nplanes, rows, cols, image_plane_stride, scratch_plane_stride,
                        image_row_stride, scratch_row_stride, h_lo, h_hi, taps, nullptr, width, SC_ZERO_FILL,
@@ -1074,8 +1088,11 @@ int sc_single_pass_f32(float* src, float* dst, int nplanes, int rows, int cols, 
                          !kn.force_generic && !kn.direct;
     if ((flags & SC_COPY_BACK) && aligned && !kn.split_passes) {
         // one pass: the valid region into the workspace and back into the image
-        return pass_common(MODE_SINGLECB, src, dst, nplanes, rows, cols, src_plane_stride, dst_plane_stride,
-                           src_row_stride, dst_row_stride, r, rows - r, nullptr, dense, width, flags, stream);
+        const int rc = pass_common(MODE_SINGLECB, src, dst, nplanes, rows, cols, src_plane_stride,
+                                   dst_plane_stride, src_row_stride, dst_row_stride, r, rows - r, nullptr, dense,
+                                   width, flags, stream);
+        if (rc != kNeedTwoLaunches) return rc;
+        set_error("");
     }
     SC_TRY(pass_common(MODE_SINGLE, src, dst, nplanes, rows, cols, src_plane_stride, dst_plane_stride,
                        src_row_stride, dst_row_stride, r, rows - r, nullptr, dense, width, flags, stream));
