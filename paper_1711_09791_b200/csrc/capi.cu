@@ -47,7 +47,7 @@ static int cuda_fail(cudaError_t e, const char* what) {
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
     int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
-    int no_sym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0;
+    int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0;
 };
 
 static Knobs read_knobs() {
@@ -73,6 +73,7 @@ static Knobs read_knobs() {
         else if (name == "IPC") k.ipc = v;
         else if (name == "NO_STAGE") k.no_stage = v;
         else if (name == "NO_SYM") k.no_sym = v;
+        else if (name == "NO_COLSYM") k.no_colsym = v;
         else if (name == "NO_PDL") k.no_pdl = v;
         else if (name == "SPLIT_PASSES") k.split_passes = v;
         else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;  // test hook: as if the allocation failed
@@ -419,13 +420,17 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     // e.g. outer(w, w) of symmetric taps): the kernel that reuses mirrored products
     // (measured: -17% at cfg5 size; the same reuse in the two-pass column fold
     // measured 0-3% slower, so the two-pass modes do not use it)
-    bool sym = false;
+    int sym = 0;  // 1: mirror-symmetric rows, 2: rows and columns (outer product of symmetric taps)
     if (!kn.no_sym && (j.mode == MODE_SINGLE || j.mode == MODE_SINGLECB) && j.dense) {
         const int W = j.width;
         auto same = [](float a, float b) { return std::memcmp(&a, &b, sizeof(float)) == 0; };
-        sym = true;
-        for (int a = 0; a < W && sym; ++a)
-            for (int b = 0; b < W && sym; ++b) sym = same(j.dense[a * W + b], j.dense[(W - 1 - a) * W + b]);
+        bool rows = true, cols = true;
+        for (int a = 0; a < W; ++a)
+            for (int b = 0; b < W; ++b) {
+                rows = rows && same(j.dense[a * W + b], j.dense[(W - 1 - a) * W + b]);
+                cols = cols && same(j.dense[a * W + b], j.dense[a * W + (W - 1 - b)]);
+            }
+        sym = rows ? (cols && !kn.no_colsym ? 2 : 1) : 0;
     }
     switch (j.mode) {
         case MODE_FUSED: kern = kernel_fused(rad, aligned); break;

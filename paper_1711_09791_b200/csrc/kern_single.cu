@@ -6,16 +6,18 @@
 
 namespace sc {
 
-const void* kernel_single(int rad, bool aligned, bool sym) {
+// sym: 0 none, 1 mirror-symmetric rows (K[i][j] == K[2r-i][j]), 2 rows and columns
+const void* kernel_single(int rad, bool aligned, int sym) {
     // symmetric-tap variants exist for r >= 1 (r = 0 has a single tap)
-    sym = sym && rad >= 1;
-#define SC_K(R)                                                                                   \
-    case R:                                                                                       \
-        if (sym)                                                                                  \
-            return aligned ? (const void*)sepconv_rows_kernel<MODE_SINGLE, R, true, (R >= 1)>          \
-                           : (const void*)sepconv_rows_kernel<MODE_SINGLE, R, false, (R >= 1)>;        \
-        return aligned ? (const void*)sepconv_rows_kernel<MODE_SINGLE, R, true>                       \
-                       : (const void*)sepconv_rows_kernel<MODE_SINGLE, R, false>;
+    if (rad < 1) sym = 0;
+#define SC_KA(R, S)                                                                       \
+    return aligned ? (const void*)sepconv_rows_kernel<MODE_SINGLE, R, true, (R >= 1 ? S : 0)> \
+                   : (const void*)sepconv_rows_kernel<MODE_SINGLE, R, false, (R >= 1 ? S : 0)>;
+#define SC_K(R)                       \
+    case R:                           \
+        if (sym == 2) SC_KA(R, 2)     \
+        if (sym == 1) SC_KA(R, 1)     \
+        SC_KA(R, 0)
     switch (rad) {
         SC_K(0)
         SC_K(1)
@@ -26,15 +28,18 @@ const void* kernel_single(int rad, bool aligned, bool sym) {
             return nullptr;
     }
 #undef SC_K
+#undef SC_KA
 }
 
 // Single pass + in-place copy-back in one pass (aligned rows only).
-const void* kernel_single_cb(int rad, bool sym) {
-    sym = sym && rad >= 1;
-#define SC_K(R)                                                                                          \
-    case R:                                                                                              \
-        return sym ? (const void*)sepconv_rows_kernel<MODE_SINGLECB, R, true, (R >= 1)>                  \
-                   : (const void*)sepconv_rows_kernel<MODE_SINGLECB, R, true>;
+const void* kernel_single_cb(int rad, int sym) {
+    if (rad < 1) sym = 0;
+#define SC_KS(R, S) return (const void*)sepconv_rows_kernel<MODE_SINGLECB, R, true, (R >= 1 ? S : 0)>;
+#define SC_K(R)                   \
+    case R:                       \
+        if (sym == 2) SC_KS(R, 2) \
+        if (sym == 1) SC_KS(R, 1) \
+        SC_KS(R, 0)
     switch (rad) {
         SC_K(0)
         SC_K(1)
@@ -45,6 +50,7 @@ const void* kernel_single_cb(int rad, bool sym) {
             return nullptr;
     }
 #undef SC_K
+#undef SC_KS
 }
 
 const void* kernel_single_direct(int rad) {

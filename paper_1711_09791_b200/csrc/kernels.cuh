@@ -654,7 +654,13 @@ __device__ __forceinline__ float2 add2p(float2 acc, float2 prod, float2 one) {
     return __ffma2_rn(prod, one, acc);  // acc + prod, one rounding (see mad2)
 }
 
-template <int RAD, int NACC>
+// COLSYM: the matrix is also mirror-symmetric in its columns (K[i][j] == K[i][2r-j]:
+// outer(w, w) of symmetric taps). The products of column pair c with tap j and
+// of pair c+2 with tap j-2 then multiply the same window samples by equal taps
+// when j and j-2 mirror each other (j = 3, 1 at r = 2): writing both with the
+// same tap index makes them one expression (27 instead of 30 FMUL2 per 4
+// columns and row at r = 2).
+template <int RAD, int NACC, bool COLSYM = false>
 __device__ __forceinline__ F4 dense_fold_sym(F4 (&acc)[NACC], const float (&win)[12], const float* k, float one) {
     static_assert(RAD >= 1, "symmetric fold needs RAD >= 1");
     constexpr int W = 2 * RAD + 1;
@@ -668,7 +674,10 @@ __device__ __forceinline__ F4 dense_fold_sym(F4 (&acc)[NACC], const float (&win)
         for (int i = 0; i <= RAD; ++i)
 #pragma unroll
             for (int j = 0; j < W; ++j)
-                pr[i][j] = __fmul2_rn(make_float2(win[o + j], win[o + j + 1]), make_float2(k[i * W + j], k[i * W + j]));
+            {
+                const int kj = COLSYM ? (j < W - 1 - j ? j : W - 1 - j) : j;
+                pr[i][j] = __fmul2_rn(make_float2(win[o + j], win[o + j + 1]), make_float2(k[i * W + kj], k[i * W + kj]));
+            }
         float2 t = make_float2(acc[NACC - 1].v[c], acc[NACC - 1].v[c + 1]);
 #pragma unroll
         for (int j = 0; j < W; ++j) t = add2p(t, pr[0][j], one2);  // kernel row W-1 == row 0
@@ -851,7 +860,7 @@ __device__ __forceinline__ void publish_row(float* drow, const float* srow, int 
 // Consumer: one item (plane, strip, band). ROW_EDGE items contain ring rows or
 // rows with a dead row pass; all others run the lean loop.
 
-template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE, bool SYM>
+template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE, int SYM>
 __device__ __forceinline__ void consume_item(const Params& p, const Item& it, const float* ring, uint64_t* full,
                                              uint64_t* empty, const int* sshift, float* stage_out, int& slot,
                                              uint32_t& phase, int& gs) {
@@ -941,8 +950,8 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                             for (int i = 0; i < 4; ++i) outv.v[i] = 0.0f;
                         }
                     } else if (single_like(MODE)) {
-                        if constexpr (SYM && SC_F2 && RAD >= 1)
-                            outv = dense_fold_sym<RAD, NACC>(acc[g], win, p.k, p.one);
+                        if constexpr (SYM >= 1 && SC_F2 && RAD >= 1)
+                            outv = dense_fold_sym<RAD, NACC, (SYM >= 2)>(acc[g], win, p.k, p.one);
                         else
                             outv = dense_fold<RAD, NACC>(acc[g], win, p.k, p.one);
                     } else {
@@ -1103,7 +1112,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 // ---------------------------------------------------------------------------
 // The kernel
 
-template <int MODE, int RAD, bool ALIGNED, bool SYM = false>
+template <int MODE, int RAD, bool ALIGNED, int SYM = 0>
 #ifndef SC_MINB
 #define SC_MINB 1
 #endif

@@ -262,7 +262,7 @@ def test_packed_math_keeps_two_roundings():
         assert ffma == 0, f"scalar FFMA (contracted mul+add) in {fn}"
         # symmetric-matrix single-pass kernels (4th template argument true) reuse
         # mirrored products: fewer FMUL2 than adds by design, at most 2 adds per product
-        sym = re.search(r"sepconv_rows_kernelILi\d+ELi\d+ELb[01]ELb1E", fn) is not None
+        sym = re.search(r"sepconv_rows_kernelILi\d+ELi\d+ELb[01]ELi[12]E", fn) is not None
         limit = 2 * fmul2 if sym else fmul2
         assert ffma2 <= limit, f"{fn}: {ffma2} FFMA2 vs {fmul2} FMUL2 -- contraction suspected"
 
