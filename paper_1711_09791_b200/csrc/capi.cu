@@ -619,7 +619,9 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
 int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long drs, int R, int C, const float* taps,
                    int width, int flags, cudaStream_t s) {
     const int rad = width / 2;
-    const void* kern = kernel_u8(rad);
+    bool symw = !read_knobs().no_sym;  // mirror-symmetric taps: shared products (bit-identical)
+    for (int i = 0; i < width && symw; ++i) symw = std::memcmp(&taps[i], &taps[width - 1 - i], sizeof(float)) == 0;
+    const void* kern = kernel_u8(rad, symw);
     if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(width));
     U8Params p;
     std::memset(&p, 0, sizeof(p));

@@ -72,7 +72,7 @@ __device__ __forceinline__ void pack12(const F4 (&outv)[3], uint32_t (&w)[3]) {
 // One item (column strip x row band) of the fused u8 kernel. EDGE items contain
 // ring rows or rows whose row pass is dead (faithful zero H0 rows); the others
 // skip those per-row tests.
-template <int RAD, bool EDGE>
+template <int RAD, bool EDGE, bool SYMW>
 __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, uint64_t* full, uint64_t* empty,
                                         int SWB, int x0, int ylo, int yhi, int in_lo, int in_hi, int& slot,
                                         uint32_t& phase, int& gs) {
@@ -124,12 +124,12 @@ __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, 
                 }
                 F4 v;
                 if (live) {
-                    v = row_pass<RAD>(win, p.w, p.one);
+                    v = row_pass<RAD, SYMW>(win, p.w, p.one);
                 } else {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) v.v[c] = 0.0f;
                 }
-                outv[q] = col_fold<RAD, NACC>(acc[q], v, p.w, p.one);
+                outv[q] = col_fold<RAD, NACC, SYMW>(acc[q], v, p.w, p.one);
             }
             if (emit && x4 < C) {
                 uint32_t w3[3];
@@ -197,7 +197,7 @@ __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, 
 #ifndef SC_U8_MINB
 #define SC_U8_MINB 1
 #endif
-template <int RAD>
+template <int RAD, bool SYMW>
 __global__ void __launch_bounds__(SC_U8_MAXT, SC_U8_MINB) sepconv_u8_kernel(const __grid_constant__ U8Params p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = p.ns;
@@ -280,9 +280,9 @@ __global__ void __launch_bounds__(SC_U8_MAXT, SC_U8_MINB) sepconv_u8_kernel(cons
         // interior items (every input row live, no ring rows) run the lean loop
         const bool edge = in_lo < p.hrow_lo || in_hi > p.hrow_hi || ylo < RAD || yhi > p.R - RAD;
         if (edge)
-            u8_item<RAD, true>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
+            u8_item<RAD, true, SYMW>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
         else
-            u8_item<RAD, false>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
+            u8_item<RAD, false, SYMW>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
     }
 }
 
@@ -312,13 +312,14 @@ __global__ void planes_to_hwc_kernel(const float* __restrict__ src, uint8_t* __r
     }
 }
 
-const void* kernel_u8(int rad) {
+// symw: mirror-symmetric taps (w[j] == w[2r-j] bitwise): products shared by value
+const void* kernel_u8(int rad, bool symw) {
     switch (rad) {
-        case 0: return (const void*)sepconv_u8_kernel<0>;
-        case 1: return (const void*)sepconv_u8_kernel<1>;
-        case 2: return (const void*)sepconv_u8_kernel<2>;
-        case 3: return (const void*)sepconv_u8_kernel<3>;
-        case 4: return (const void*)sepconv_u8_kernel<4>;
+        case 0: return (const void*)sepconv_u8_kernel<0, false>;
+        case 1: return symw ? (const void*)sepconv_u8_kernel<1, true> : (const void*)sepconv_u8_kernel<1, false>;
+        case 2: return symw ? (const void*)sepconv_u8_kernel<2, true> : (const void*)sepconv_u8_kernel<2, false>;
+        case 3: return symw ? (const void*)sepconv_u8_kernel<3, true> : (const void*)sepconv_u8_kernel<3, false>;
+        case 4: return symw ? (const void*)sepconv_u8_kernel<4, true> : (const void*)sepconv_u8_kernel<4, false>;
         default: return nullptr;
     }
 }

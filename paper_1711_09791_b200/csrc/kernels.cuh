@@ -497,10 +497,20 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
     }
 }
 
+// Tap index used for the multiply by w[j]: with mirror-symmetric taps (SYMW:
+// w[j] == w[2r-j] bitwise, checked on the host) taps j and 2r-j are the same
+// value, so writing them with one index makes the products of the same operand
+// one expression (the column fold multiplies each row value by r+1 distinct taps
+// instead of 2r+1). Same IEEE products, same adds, same order: bit-identical.
+template <int RAD, bool SYMW>
+__host__ __device__ constexpr int tap_ix(int j) {
+    return SYMW && j > RAD ? 2 * RAD - j : j;
+}
+
 // ---------------------------------------------------------------------------
 // Per-row arithmetic for one 4-column group. win holds columns x4-4 .. x4+7.
 
-template <int RAD>
+template <int RAD, bool SYMW = false>
 __device__ __forceinline__ F4 row_pass(const float (&win)[12], const float* w, float one) {
     F4 h;
 #if SC_F2
@@ -513,7 +523,8 @@ __device__ __forceinline__ F4 row_pass(const float (&win)[12], const float* w, f
         float2 acc = __fmul2_rn(make_float2(win[o], win[o + 1]), make_float2(w[0], w[0]));
 #pragma unroll
         for (int m = 1; m <= 2 * RAD; ++m)
-            acc = mad2(acc, make_float2(win[o + m], win[o + m + 1]), make_float2(w[m], w[m]), one2);
+            acc = mad2(acc, make_float2(win[o + m], win[o + m + 1]),
+                       make_float2(w[tap_ix<RAD, SYMW>(m)], w[tap_ix<RAD, SYMW>(m)]), one2);
         h.v[c] = acc.x;
         h.v[c + 1] = acc.y;
     }
@@ -533,7 +544,7 @@ __device__ __forceinline__ F4 row_pass(const float (&win)[12], const float* w, f
 // Column fold: push row value v into the shift register, return the finished
 // output (row y-RAD). acc[j] holds the partial sum of output y-RAD+... started
 // j+1 rows ago; every update is acc + v*w[j], exactly the reference's order.
-template <int RAD, int NACC>
+template <int RAD, int NACC, bool SYMW = false>
 __device__ __forceinline__ F4 col_fold(F4 (&acc)[NACC], const F4& v, const float* w, float one) {
     F4 out;
     (void)one;
@@ -547,13 +558,14 @@ __device__ __forceinline__ F4 col_fold(F4 (&acc)[NACC], const F4& v, const float
     for (int c = 0; c < 4; c += 2) {
         const float2 one2 = make_float2(one, one);
         const float2 vv = make_float2(v.v[c], v.v[c + 1]);
-        float2 t = mad2(make_float2(acc[NACC - 1].v[c], acc[NACC - 1].v[c + 1]), vv,
-                        make_float2(w[2 * RAD], w[2 * RAD]), one2);
+        constexpr int jl = tap_ix<RAD, SYMW>(2 * RAD);
+        float2 t = mad2(make_float2(acc[NACC - 1].v[c], acc[NACC - 1].v[c + 1]), vv, make_float2(w[jl], w[jl]), one2);
         out.v[c] = t.x;
         out.v[c + 1] = t.y;
 #pragma unroll
         for (int j = NACC - 1; j >= 1; --j) {
-            t = mad2(make_float2(acc[j - 1].v[c], acc[j - 1].v[c + 1]), vv, make_float2(w[j], w[j]), one2);
+            const int jj = tap_ix<RAD, SYMW>(j);
+            t = mad2(make_float2(acc[j - 1].v[c], acc[j - 1].v[c + 1]), vv, make_float2(w[jj], w[jj]), one2);
             acc[j].v[c] = t.x;
             acc[j].v[c + 1] = t.y;
         }

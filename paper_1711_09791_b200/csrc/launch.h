@@ -22,7 +22,7 @@ const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);
 const void* kernel_single_direct(int rad);
 
-const void* kernel_u8(int rad);
+const void* kernel_u8(int rad, bool symw = false);
 cudaError_t launch_hwc_to_planes(const uint8_t* src, float* dst, long long srs, long long dps, long long drs, int R,
                                  int C, cudaStream_t s);
 cudaError_t launch_planes_to_hwc(const float* src, uint8_t* dst, long long sps, long long srs, long long drs, int R,
