@@ -14,3 +14,8 @@ python tools/prof_one.py --op single > gpurun_out/plain3.log 2>&1 && ncu --set f
 python tools/misalign_probe.py > gpurun_out/misalign.jsonl 2>&1; cat gpurun_out/misalign.jsonl
 python -m paper_1711_09791_b200.ladder --reps 200 --csv gpurun_out/ladder_gpu.csv > /dev/null 2>&1
 ls -la gpurun_out
+# per-kernel table (every kernel family: event time, DRAM bytes) and full captures of the in-place and u8 kernels
+bash tools/kernel_table.sh > gpurun_out/kt.log 2>&1
+python tools/kernel_table.py --cfg cfg5 --ncu-pass > gpurun_out/plain4.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:sepconv_u8 -s 3 -c 1 -o gpurun_out/prof_u8_cfg5 python tools/kernel_table.py --cfg cfg5 --ncu-pass > gpurun_out/ncu_u8.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sepconv_rows -s 3 -c 1 -o gpurun_out/prof_splitf_cfg5 python tools/kernel_table.py --cfg cfg5 --ncu-pass > gpurun_out/ncu_sf.log 2>&1
+ls -la gpurun_out
