@@ -179,6 +179,16 @@ int sc_two_pass_host_band_f32(const float *const *src_planes, float *const *dst_
                               int cols, int out_lo, int out_hi, const float *taps, int width, int flags,
                               int device);
 
+/* sc_two_pass_host_f32 over SEVERAL GPUs from one process (the reference's plans
+ * are single-process): ndev row bands by the reference's balanced split
+ * (partition_block, S/executors.py:121-139), each streamed through its own GPU
+ * and PCIe link by its own host thread, concurrently. The 2r rows around every
+ * band boundary are copied aside first, so in-place use stays exact. Same bits
+ * as one device. A device may be listed more than once (its bands then run one
+ * after the other). Blocks until done. */
+int sc_two_pass_host_multi_f32(const float *const *src_planes, float *const *dst_planes, int nplanes, int rows,
+                               int cols, const float *taps, int width, int flags, const int *devices, int ndev);
+
 #ifdef __cplusplus
 }
 #endif

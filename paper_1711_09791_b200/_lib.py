@@ -53,6 +53,7 @@ EXPORTS = (
     "sc_fill_synthetic_f32",
     "sc_two_pass_host_f32",
     "sc_two_pass_host_band_f32",
+    "sc_two_pass_host_multi_f32",
     "sc_two_pass_u8hwc",
     "sc_hwc_u8_to_planes_f32",
     "sc_planes_f32_to_hwc_u8",
@@ -94,6 +95,7 @@ _SIGNATURES = {
     "sc_fill_synthetic_f32": ([_vp, _i64, _u64, _u64, _i32, _vp], _i32),
     "sc_two_pass_host_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_two_pass_host_band_f32": ([_vp, _vp, _i32, _i32, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
+    "sc_two_pass_host_multi_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _i32], _i32),
     "sc_two_pass_u8hwc": ([_vp, _vp, _i32, _i32, _i64, _i64, _fp, _i32, _i32, _vp], _i32),
     "sc_hwc_u8_to_planes_f32": ([_vp, _vp, _i32, _i32, _i64, _i64, _i64, _vp], _i32),
     "sc_planes_f32_to_hwc_u8": ([_vp, _vp, _i32, _i32, _i64, _i64, _i64, _vp], _i32),

@@ -319,7 +319,8 @@ const void* kernel_u8(int rad, bool symw) {
         case 1: return symw ? (const void*)sepconv_u8_kernel<1, true> : (const void*)sepconv_u8_kernel<1, false>;
         case 2: return symw ? (const void*)sepconv_u8_kernel<2, true> : (const void*)sepconv_u8_kernel<2, false>;
         case 3: return symw ? (const void*)sepconv_u8_kernel<3, true> : (const void*)sepconv_u8_kernel<3, false>;
-        case 4: return symw ? (const void*)sepconv_u8_kernel<4, true> : (const void*)sepconv_u8_kernel<4, false>;
+        // r = 4 with shared products spills (the products of 5 distinct taps stay live)
+        case 4: return (const void*)sepconv_u8_kernel<4, false>;
         default: return nullptr;
     }
 }

@@ -12,7 +12,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <map>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -87,8 +89,12 @@ static int ensure(HostCtx* c, size_t in_floats, size_t out_floats, std::string& 
 
 using namespace sc;
 
+// halo_top / halo_bot (optional, per plane): r rows holding global rows
+// [out_lo - r, out_lo) / [out_hi, out_hi + r), read instead of the source planes
+// (the multi-device path: neighbouring bands overwrite those rows in place)
 static int host_band(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows, int cols,
-                     int out_lo, int out_hi, const float* taps, int width, int flags, int device);
+                     int out_lo, int out_hi, const float* taps, int width, int flags, int device,
+                     const float* const* halo_top = nullptr, const float* const* halo_bot = nullptr);
 
 extern "C" int sc_two_pass_host_f32(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows,
                                     int cols, const float* taps, int width, int flags, int device) {
@@ -106,11 +112,76 @@ extern "C" int sc_two_pass_host_band_f32(const float* const* src_planes, float* 
     return host_band(src_planes, dst_planes, nplanes, rows, cols, out_lo, out_hi, taps, width, flags, device);
 }
 
+// One process, several GPUs (the reference's single-process plan model): the
+// image is split into ndev row bands by the reference's balanced block split
+// (S/executors.py:121-139); every band streams through its own GPU (and PCIe
+// link) concurrently, one host thread per device. Before any device starts, the
+// 2r rows around every band boundary are copied aside on the host, so that in
+// place (dst == src) a band never reads halo rows its neighbour has already
+// overwritten. A device listed twice runs its bands one after the other.
+extern "C" int sc_two_pass_host_multi_f32(const float* const* src_planes, float* const* dst_planes, int nplanes,
+                                          int rows, int cols, const float* taps, int width, int flags,
+                                          const int* devices, int ndev) {
+    set_error("");
+    if (!devices || ndev < 1) {
+        set_error("need at least one device");
+        return SC_INVALID_ARGUMENT;
+    }
+    if (!src_planes || !dst_planes || !taps || nplanes < 1 || rows < 1 || cols < 1) {
+        set_error("null pointer or non-positive dimension");
+        return SC_INVALID_ARGUMENT;
+    }
+    const int r = width / 2;
+    // bands no shorter than r rows, so that a halo comes from the adjacent band only
+    int nb = ndev;
+    while (nb > 1 && rows / nb < (r > 1 ? r : 1)) --nb;
+    if (nb == 1) return host_band(src_planes, dst_planes, nplanes, rows, cols, 0, rows, taps, width, flags, devices[0]);
+    std::vector<int> lo(nb + 1);
+    const int q = rows / nb, rem = rows % nb;
+    for (int g = 0; g <= nb; ++g) lo[g] = g * q + (g < rem ? g : rem);
+    // halo copies: boundary g (1..nb-1) keeps rows [lo[g] - r, lo[g] + r) of every plane
+    std::vector<float> side((size_t)(nb - 1) * nplanes * 2 * r * cols);
+    auto side_rows = [&](int g, int p) { return side.data() + (((size_t)(g - 1) * nplanes + p) * 2 * r) * cols; };
+    for (int g = 1; g < nb && r > 0; ++g)
+        for (int p = 0; p < nplanes; ++p) {
+            if (!src_planes[p]) {
+                set_error("null plane pointer");
+                return SC_INVALID_ARGUMENT;
+            }
+            std::memcpy(side_rows(g, p), src_planes[p] + (size_t)(lo[g] - r) * cols, sizeof(float) * 2 * r * cols);
+        }
+    std::vector<int> rcs(nb, SC_OK);
+    std::vector<std::string> errs(nb);
+    auto run = [&](int g) {
+        std::vector<const float*> top(nplanes), bot(nplanes);
+        for (int p = 0; p < nplanes; ++p) {
+            top[p] = g > 0 ? side_rows(g, p) : nullptr;                                // rows [lo-r, lo)
+            bot[p] = g + 1 < nb ? side_rows(g + 1, p) + (size_t)r * cols : nullptr;  // rows [hi, hi+r)
+        }
+        rcs[g] = host_band(src_planes, dst_planes, nplanes, rows, cols, lo[g], lo[g + 1], taps, width, flags,
+                           devices[g % ndev], g > 0 && r > 0 ? top.data() : nullptr,
+                           g + 1 < nb && r > 0 ? bot.data() : nullptr);
+        errs[g] = sc_last_error();
+    };
+    std::vector<std::thread> threads;
+    for (int g = 1; g < nb; ++g) threads.emplace_back(run, g);
+    run(0);
+    for (auto& t : threads) t.join();
+    for (int g = 0; g < nb; ++g)
+        if (rcs[g] != SC_OK) {
+            set_error("band " + std::to_string(g) + ": " + errs[g]);
+            return rcs[g];
+        }
+    set_error("");
+    return SC_OK;
+}
+
 // Rows [out_lo, out_hi) of a rows x cols image (global-row rules), reading host
 // rows [out_lo - r, out_hi + r) clipped to the image and writing host rows
 // [out_lo, out_hi); plane pointers address row 0 (the rows outside are not touched).
 static int host_band(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows, int cols,
-                     int out_lo, int out_hi, const float* taps, int width, int flags, int device) {
+                     int out_lo, int out_hi, const float* taps, int width, int flags, int device,
+                     const float* const* halo_top, const float* const* halo_bot) {
     set_error("");
     if (!src_planes || !dst_planes || !taps || nplanes < 1 || rows < 1 || cols < 1) {
         set_error("null pointer or non-positive dimension");
@@ -188,8 +259,27 @@ static int host_band(const float* const* src_planes, float* const* dst_planes, i
         const Chunk& q = chunks[k];
         const int s = (int)(k % NSLOT);
         if (k >= NSLOT) cudaStreamWaitEvent(c->h2d, c->ev_cmp[s], 0);  // slot's previous kernel done
-        cudaError_t e2 = cudaMemcpyAsync(c->in_buf[s], src_planes[q.plane] + (size_t)q.in_lo * cols,
-                                         (size_t)(q.in_hi - q.in_lo) * row_bytes, cudaMemcpyHostToDevice, c->h2d);
+        // rows [in_lo, in_hi): own rows from the source planes, halo rows outside
+        // [out_lo, out_hi) from the halo copies when given
+        cudaError_t e2 = cudaSuccess;
+        int y = q.in_lo;
+        float* d = c->in_buf[s];
+        if (halo_top && y < out_lo) {
+            const int n_top = out_lo - y;
+            e2 = cudaMemcpyAsync(d, halo_top[q.plane] + (size_t)(r - n_top) * cols, (size_t)n_top * row_bytes,
+                                 cudaMemcpyHostToDevice, c->h2d);
+            d += (size_t)n_top * cols;
+            y = out_lo;
+        }
+        const int own_hi = (halo_bot && q.in_hi > out_hi) ? out_hi : q.in_hi;
+        if (e2 == cudaSuccess && own_hi > y) {
+            e2 = cudaMemcpyAsync(d, src_planes[q.plane] + (size_t)y * cols, (size_t)(own_hi - y) * row_bytes,
+                                 cudaMemcpyHostToDevice, c->h2d);
+            d += (size_t)(own_hi - y) * cols;
+        }
+        if (e2 == cudaSuccess && own_hi < q.in_hi)
+            e2 = cudaMemcpyAsync(d, halo_bot[q.plane], (size_t)(q.in_hi - own_hi) * row_bytes, cudaMemcpyHostToDevice,
+                                 c->h2d);
         cudaEventRecord(c->ev_h2d[s], c->h2d);
         return e2;
     };

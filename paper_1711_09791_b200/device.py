@@ -281,10 +281,12 @@ def synthetic(shape, seed: int, kind: int, device="cuda", offset: int = 0) -> to
 
 
 def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring: bool = True,
-                  device: int = 0) -> None:
+                  device: int = 0, devices=None) -> None:
     """End-to-end two-pass on HOST planes (numpy arrays or CPU tensors, ideally pinned):
     streamed H2D -> fused kernel -> D2H inside the library; blocks until done.
-    dst_planes may be src_planes (in place, as conv_two_pass)."""
+    dst_planes may be src_planes (in place, as conv_two_pass). devices (a list of
+    device indices, one process): row bands streamed through every listed GPU
+    concurrently (sc_two_pass_host_multi_f32), same bits."""
     w = _taps(taps)
     ptrs_in, ptrs_out = [], []
     shape = None
@@ -310,6 +312,15 @@ def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring:
     arr_out = (ctypes.c_void_p * n)(*ptrs_out)
     flags = (_lib.SC_EXTENDED if extended else 0) | (0 if ring else _lib.SC_NO_RING)
     L = _lib.load()
+    if devices is not None and len(list(devices)) > 1:
+        devs = [int(d) for d in devices]
+        arr_dev = (ctypes.c_int * len(devs))(*devs)
+        _lib.check(L.sc_two_pass_host_multi_f32(ctypes.cast(arr_in, ctypes.c_void_p),
+                                                ctypes.cast(arr_out, ctypes.c_void_p), n, shape[0], shape[1], _fp(w),
+                                                w.size, flags, ctypes.cast(arr_dev, ctypes.c_void_p), len(devs)))
+        return
+    if devices is not None and len(list(devices)) == 1:
+        device = int(list(devices)[0])
     _lib.check(L.sc_two_pass_host_f32(ctypes.cast(arr_in, ctypes.c_void_p), ctypes.cast(arr_out, ctypes.c_void_p),
                                       n, shape[0], shape[1], _fp(w), w.size, flags, int(device)))
 

@@ -29,22 +29,33 @@ from .multi import partition_block  # noqa: F401  (re-exported like the referenc
 
 @dataclass(frozen=True)
 class Cuda:
-    """Run on one CUDA device. device=None: the image's device (or the current one
-    for host images). fused: stream host images through the fused kernel."""
+    """Run on CUDA devices. device=None: the image's device (or the current one
+    for host images). fused: stream host images through the fused kernel.
+    devices: several GPUs from this one process (host images, fused two-pass):
+    the image is split into row bands (the reference's partition_block), each
+    streamed through its own GPU and PCIe link concurrently; same bits."""
 
     device: int | None = None
     fused: bool = True
+    devices: tuple[int, ...] | None = None
 
     def __post_init__(self):
         if self.device is not None and self.device < 0:
             raise InvalidArgumentError(f"device must be >= 0, got {self.device}")
+        if self.devices is not None:
+            devs = tuple(int(d) for d in self.devices)
+            if not devs or any(d < 0 for d in devs):
+                raise InvalidArgumentError(f"devices must be a non-empty list of indices >= 0, got {self.devices}")
+            if self.device is not None:
+                raise InvalidArgumentError("give either device or devices, not both")
+            object.__setattr__(self, "devices", devs)
 
 
 ExecPlan = Cuda
 
 
 def make_plan(mode: str, workers: int | None = None, cutoff: int = 100, agglomerate: bool = False,
-              *, device: int | None = None, fused: bool = True) -> ExecPlan:
+              *, device: int | None = None, fused: bool = True, devices=None) -> ExecPlan:
     """Plan from loose configuration (CLI flags, request bodies), S/executors.py:88-109.
 
     mode "cuda" is the B200 plan. The reference's CPU thread modes are not part of
@@ -54,7 +65,7 @@ def make_plan(mode: str, workers: int | None = None, cutoff: int = 100, agglomer
         if agglomerate:
             # every launch already covers all planes; accepted for compatibility
             pass
-        return Cuda(device=device, fused=fused)
+        return Cuda(device=device, fused=fused, devices=tuple(devices) if devices is not None else None)
     if mode in ("sequential", "static", "taskpool"):
         raise UnsupportedCombinationError(
             f"plan mode {mode!r} schedules CPU threads; the B200 build runs mode 'cuda'"
@@ -159,10 +170,11 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
                     dev.single_pass(ig, outer_product(kernel).matrix, wg, copy_back=variant.copy_back)
             torch.cuda.current_stream().synchronize()
     else:
-        device_index = plan.device if plan.device is not None else torch.cuda.current_device()
+        device_index = plan.device if plan.device is not None else (
+            plan.devices[0] if plan.devices else torch.cuda.current_device())
         if two_pass and plan.fused:
             planes = [p.data for p in image.planes]
-            dev.two_pass_host(planes, planes, kernel.weights, device=device_index)
+            dev.two_pass_host(planes, planes, kernel.weights, device=device_index, devices=plan.devices)
         else:
             with torch.cuda.device(device_index):
                 src = torch.stack([torch.from_numpy(p.data) for p in image.planes]).cuda()

@@ -199,3 +199,18 @@ def test_reference_errors(sc):
     dsrc = sc.Plane(torch.zeros((8, 8), device="cuda"))
     with pytest.raises(sc.InvalidArgumentError):
         sc.conv_two_pass(dsrc, sc.gaussian5(), sc.Plane(dsrc.data[:, :]))
+
+
+def test_convolve_image_multi_device_plan(sc):
+    """convolve_image with Cuda(devices=[...]) on a host image (the reference's
+    single-process plan model, several GPUs): same bits as Cuda()."""
+    rng = np.random.default_rng(12)
+    data = rng.random((3, 300, 517), dtype=np.float32)
+    k = sc.SeparableKernel(np.array([1, 4, 6, 4, 1], np.float32) / 16)
+    variant = sc.ConvVariant(sc.Algorithm.TWO_PASS)
+    a = sc.Image([sc.Plane(p.copy()) for p in data])
+    b = sc.Image([sc.Plane(p.copy()) for p in data])
+    sc.convolve_image(a, k, variant, sc.Cuda())
+    sc.convolve_image(b, k, variant, sc.Cuda(devices=[0, 0, 0, 0]))
+    for pa, pb in zip(a.planes, b.planes):
+        assert np.array_equal(pa.data.view(np.uint32), pb.data.view(np.uint32))

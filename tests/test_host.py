@@ -260,9 +260,11 @@ def test_packed_math_keeps_two_roundings():
         if "sepconv_" not in fn:
             continue
         assert ffma == 0, f"scalar FFMA (contracted mul+add) in {fn}"
-        # symmetric-matrix single-pass kernels (4th template argument true) reuse
-        # mirrored products: fewer FMUL2 than adds by design, at most 2 adds per product
-        sym = re.search(r"sepconv_rows_kernelILi\d+ELi\d+ELb[01]ELi[12]E", fn) is not None
+        # symmetric-matrix single-pass kernels (4th template argument 1 or 2) and the
+        # symmetric-tap u8 kernels reuse mirrored products: fewer FMUL2 than adds by
+        # design, at most 2 adds per product
+        sym = (re.search(r"sepconv_rows_kernelILi\d+ELi\d+ELb[01]ELi[12]E", fn) is not None
+               or re.search(r"sepconv_u8_kernelILi\d+ELb1E", fn) is not None)  # u8 with symmetric taps
         limit = 2 * fmul2 if sym else fmul2
         assert ffma2 <= limit, f"{fn}: {ffma2} FFMA2 vs {fmul2} FMUL2 -- contraction suspected"
 
@@ -300,3 +302,18 @@ def test_two_pass_kernels_keep_four_ctas_per_sm():
         if m.group(1) == "0" and m.group(2) == "1":
             assert n <= 80, f"aligned fused kernel {fn}: {n} registers (was 76)"
     assert checked >= 7
+
+
+def test_cuda_plan_devices_validation():
+    """Cuda(devices=...) (several GPUs from one process) validates like the
+    reference's plan constructors: non-empty, non-negative, not with device=."""
+    from paper_1711_09791_b200.errors import InvalidArgumentError
+    from paper_1711_09791_b200.executors import Cuda, make_plan
+
+    assert Cuda(devices=[0, 1]).devices == (0, 1)
+    assert make_plan("cuda", devices=[3]).devices == (3,)
+    for bad in ([], [-1], [0, -2]):
+        with pytest.raises(InvalidArgumentError):
+            Cuda(devices=bad)
+    with pytest.raises(InvalidArgumentError):
+        Cuda(device=0, devices=[1])
