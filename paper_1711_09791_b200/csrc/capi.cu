@@ -408,6 +408,7 @@ static int cached_plan(const RowsJob& j, const void* kern, bool aligned, bool di
 }
 
 int launch_rows(const RowsJob& j, cudaStream_t s) {
+    if (j.width > MAX_W) return launch_wide(j, s);
     const int rad = j.width / 2;
     const Knobs kn = read_knobs();
     const void* kern = nullptr;
@@ -681,8 +682,9 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
 static int check_width(int width) {
     if (width < 1 || width % 2 == 0)
         return fail(SC_INVALID_ARGUMENT, "kernel width must be odd and >= 1, got " + std::to_string(width));
-    if (width > MAX_W)
-        return fail(SC_UNSUPPORTED_WIDTH, "kernel width " + std::to_string(width) + " > 9 not supported");
+    if (width > MAX_W_WIDE)
+        return fail(SC_UNSUPPORTED_WIDTH,
+                    "kernel width " + std::to_string(width) + " > " + std::to_string(MAX_W_WIDE) + " not supported");
     return SC_OK;
 }
 
@@ -1038,7 +1040,7 @@ int sc_two_pass_split_f32(float* image, float* scratch, int nplanes, int rows, i
     const bool aligned = cols % 4 == 0 && aligned16(image) && aligned16(scratch) && image_plane_stride % 4 == 0 &&
                          scratch_plane_stride % 4 == 0 && image_row_stride % 4 == 0 && scratch_row_stride % 4 == 0 &&
                          !kn.force_generic;
-    if (aligned && !kn.split_passes) {
+    if (aligned && !kn.split_passes && width <= MAX_W) {
         SC_TRY(check_strides(nplanes, rows, cols, image_plane_stride, image_row_stride, "image"));
         SC_TRY(check_strides(nplanes, rows, cols, scratch_plane_stride, scratch_row_stride, "scratch"));
         SC_TRY(prepare(image));
@@ -1093,7 +1095,7 @@ int sc_single_pass_f32(float* src, float* dst, int nplanes, int rows, int cols, 
     const bool aligned = cols % 4 == 0 && aligned16(src) && aligned16(dst) && src_plane_stride % 4 == 0 &&
                          dst_plane_stride % 4 == 0 && src_row_stride % 4 == 0 && dst_row_stride % 4 == 0 &&
                          !kn.force_generic && !kn.direct;
-    if ((flags & SC_COPY_BACK) && aligned && !kn.split_passes) {
+    if ((flags & SC_COPY_BACK) && aligned && !kn.split_passes && width <= MAX_W) {
         // one pass: the valid region into the workspace and back into the image
         const int rc = pass_common(MODE_SINGLECB, src, dst, nplanes, rows, cols, src_plane_stride,
                                    dst_plane_stride, src_row_stride, dst_row_stride, r, rows - r, nullptr, dense,

@@ -71,6 +71,7 @@ constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (d
 constexpr int HALO = 4;       // smem columns kept either side of a strip (supports r <= 4)
 constexpr int MAX_RAD = 4;
 constexpr int MAX_W = 2 * MAX_RAD + 1;
+constexpr int MAX_W_WIDE = 255;  // widths 11..255 run the plain kernels of kern_wide.cu
 constexpr int MAX_THREADS = 32 + 256;  // producer warp + up to 8 consumer warps
 #ifndef SC_MAXT
 #define SC_MAXT MAX_THREADS

@@ -73,6 +73,8 @@ struct RowsJob {
 // Plans and launches one row-streaming kernel; returns an SC_* status and sets
 // the thread's last error on failure.
 int launch_rows(const RowsJob& job, cudaStream_t s);
+// widths above MAX_W (kern_wide.cu); called by launch_rows
+int launch_wide(const RowsJob& job, cudaStream_t s);
 
 void set_error(const std::string& msg);
 void count_launch(uint64_t n = 1);

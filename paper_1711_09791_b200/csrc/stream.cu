@@ -191,8 +191,8 @@ static int host_band(const float* const* src_planes, float* const* dst_planes, i
         set_error("kernel width must be odd and >= 1");
         return SC_INVALID_ARGUMENT;
     }
-    if (width > MAX_W) {
-        set_error("kernel width > 9 not supported");
+    if (width > MAX_W_WIDE) {
+        set_error("kernel width > 255 not supported");
         return SC_UNSUPPORTED_WIDTH;
     }
     if (rows < width || cols < width) {

@@ -416,7 +416,8 @@ def two_pass_u8hwc(src: torch.Tensor, taps, out: torch.Tensor | None = None, *,
         raise InvalidArgumentError("source and destination dimensions differ")
     flags = _lib.SC_EXTENDED if extended else 0
     L = _lib.load()
-    if C % 16 == 0 and srs % 16 == 0 and drs % 16 == 0 and src.data_ptr() % 16 == 0 and out.data_ptr() % 4 == 0:
+    if C % 16 == 0 and srs % 16 == 0 and drs % 16 == 0 and src.data_ptr() % 16 == 0 and out.data_ptr() % 4 == 0 \
+            and w.size <= 9:  # the fused u8 kernel covers widths 1..9; wider taps take the planes path
         _lib.check(L.sc_two_pass_u8hwc(src.data_ptr(), out.data_ptr(), R, C, srs, drs, _fp(w), w.size, flags,
                                        _stream(src)))
         return out

@@ -129,7 +129,22 @@ def plane_case(name, planes_data: np.ndarray, taps: np.ndarray):
     return path
 
 
+def wide_cases():
+    """Widths above 9 (the reference takes any odd width, S/kernels.py:17-20)."""
+    out = []
+    img = ref.make_synthetic(30, 34, 2, 17)
+    data = np.stack([p.data for p in img.planes])
+    rng = np.random.default_rng(1711)
+    for W in (11, 13):
+        taps = rng.uniform(-1, 1, size=W).astype(np.float32)
+        out.append(plane_case(f"syn_30x34_s17_w{W}", data, taps))
+    return out
+
+
 def main():
+    if "--only-wide" in sys.argv:  # add the wide fixtures without rewriting the others
+        print(wide_cases())
+        return
     written = []
     # 1. reference-test shapes on make_synthetic inputs (values in [0, 256))
     shapes = [
@@ -156,6 +171,7 @@ def main():
     data = np.stack([p.data for p in img.planes])
     written.append(plane_case("syn_12x16_s4_delta5", data, ref.delta(5).weights))
     written.append(plane_case("syn_12x16_s4_w3", data, np.array([0.1, 0.7, 0.3], dtype=np.float32)))
+    written.extend(wide_cases())
     # 3. special values: negative, zero rows, large magnitudes (FMA-sensitive)
     rng = np.random.default_rng(1234)
     spec = rng.uniform(-1e4, 1e4, size=(2, 20, 28)).astype(np.float32)

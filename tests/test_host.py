@@ -48,7 +48,8 @@ def test_abi_validates_before_launch():
     buf = (ctypes.c_float * 64)()
     p = ctypes.cast(buf, ctypes.c_void_p)
     assert _fused(L, p, p, 1, 8, 8, 4) == _lib.SC_INVALID_ARGUMENT          # even width
-    assert _fused(L, p, p, 1, 8, 8, 11) == _lib.SC_UNSUPPORTED_WIDTH        # > 9
+    assert _fused(L, p, p, 1, 8, 8, 257) == _lib.SC_UNSUPPORTED_WIDTH       # > 255
+    assert _fused(L, p, p, 1, 8, 8, 11) == _lib.SC_INVALID_DIMENSION        # widths 11..255 run; 8 rows < 11
     assert _fused(L, p, p, 1, 4, 8, 5) == _lib.SC_INVALID_DIMENSION         # rows < width
     assert b"smaller than kernel width" in L.sc_last_error()
     assert _fused(L, p, p, 0, 8, 8, 5) == _lib.SC_INVALID_ARGUMENT          # no planes
