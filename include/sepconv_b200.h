@@ -31,7 +31,7 @@ extern "C" {
 #define SC_OK 0
 #define SC_INVALID_ARGUMENT 1  /* InvalidArgumentError: shapes, ranges, aliasing (S/conv.py:68-75) */
 #define SC_INVALID_DIMENSION 2 /* InvalidDimensionError: plane smaller than the kernel (S/conv.py:76-79) */
-#define SC_UNSUPPORTED_WIDTH 3 /* UnsupportedWidthError: width outside 1..9 (odd) */
+#define SC_UNSUPPORTED_WIDTH 3 /* UnsupportedWidthError: width above 255 (or above 9 on the peer-band and fused-u8 entry points) */
 #define SC_CUDA_ERROR 4        /* ExecutionError: a launch or copy failed (S/errors.py:36-42) */
 
 /* Flags */
