@@ -433,14 +433,17 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
             }
         sym = rows ? (cols && !kn.no_colsym ? 2 : 1) : 0;
     }
+    // two-pass modes: mirror-symmetric taps (bitwise) share their products
+    bool symw = !kn.no_sym && (j.mode == MODE_FUSED || j.mode == MODE_SPLITF) && j.taps;
+    for (int i = 0; i < j.width && symw; ++i) symw = std::memcmp(&j.taps[i], &j.taps[j.width - 1 - i], sizeof(float)) == 0;
     switch (j.mode) {
-        case MODE_FUSED: kern = kernel_fused(rad, aligned); break;
+        case MODE_FUSED: kern = kernel_fused(rad, aligned, symw); break;
         case MODE_HPASS: kern = kernel_hpass(rad, aligned); break;
         case MODE_VPASS: kern = kernel_vpass(rad, aligned); break;
         case MODE_SINGLE: kern = kernel_single(rad, aligned, sym); break;
         case MODE_SPLITF:
             if (!aligned) return fail(SC_INVALID_ARGUMENT, "split-fused kernel needs 16-B aligned rows");
-            kern = kernel_splitf(rad);
+            kern = kernel_splitf(rad, symw);
             break;
         case MODE_SINGLECB:
             if (!aligned) return fail(SC_INVALID_ARGUMENT, "in-place copy-back kernel needs 16-B aligned rows");
