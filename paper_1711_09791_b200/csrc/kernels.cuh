@@ -873,7 +873,12 @@ __device__ __forceinline__ void publish_row(float* drow, const float* srow, int 
 // Consumer: one item (plane, strip, band). ROW_EDGE items contain ring rows or
 // rows with a dead row pass; all others run the lean loop.
 
-template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE, int SYM>
+// COL_EDGE: the item's strip touches the image's column ring or its right edge
+// (first and last strips, unaligned rows); interior strips (COL_EDGE false) store
+// every group with one STG.128 and need no per-row column tests (measured: -2% at
+// cfg5 under the bench's sustained power cap, where issue slots are scarce; not
+// used by the single pass, whose register allocation it upset: cfg2 +13%).
+template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE, int SYM, bool COL_EDGE = true>
 __device__ __forceinline__ void consume_item(const Params& p, const Item& it, const float* ring, uint64_t* full,
                                              uint64_t* empty, const int* sshift, float* stage_out, int& slot,
                                              uint32_t& phase, int& gs) {
@@ -900,7 +905,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 #pragma unroll
     for (int g = 0; g < GROUPS; ++g) {
         x4[g] = it.x0 + 4 * ct + g * tw2;
-        fast[g] = ALIGNED && x4[g] >= RAD && x4[g] + 4 <= C - RAD;
+        fast[g] = ALIGNED && (!COL_EDGE || (x4[g] >= RAD && x4[g] + 4 <= C - RAD));
     }
     float* dplane = p.dst + (long long)it.plane * p.dst_plane_stride;
 
@@ -948,7 +953,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                     // a warp whose group lies wholly right of the image (the padding of a
                     // partial last strip) has nothing to store: skip its arithmetic. The
                     // test is warp-uniform (lane 0's columns), as store_shift shuffles.
-                    if (x4[g] - 4 * lane >= C) continue;
+                    if (COL_EDGE && x4[g] - 4 * lane >= C) continue;
                     float win[12];
                     if (ALIGNED) {
                         load_win(win, sstage + k * SW + g * tw2);
@@ -1188,8 +1193,11 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
         const Item it = decode_item<MODE, RAD>(p, item);
         if (item_rows_edge<MODE, RAD>(p, it))
             consume_item<MODE, RAD, ALIGNED, true, SYM>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
-        else
+        else if (single_like(MODE) || !ALIGNED || it.x0 < RAD || it.x0 + p.tw > p.C - RAD)
             consume_item<MODE, RAD, ALIGNED, false, SYM>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
+        else
+            consume_item<MODE, RAD, ALIGNED, false, SYM, false>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
+                                                                gs);
 #ifdef SC_TRACE
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 30 + ntr, clock64());
         ++ntr;
