@@ -50,6 +50,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace sc {
 
 enum Mode : int { MODE_FUSED = 0, MODE_HPASS = 1, MODE_VPASS = 2, MODE_SINGLE = 3, MODE_SPLITF = 4, MODE_SINGLECB = 5 };
@@ -935,148 +937,158 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 #endif
         // stages are contiguous in smem: the ring is one circular buffer of NS*SROWS rows
         const float* sstage = ring + slot * SROWS * SW + 4 * ct;
-#pragma unroll
-        for (int k = 0; k < SROWS; ++k) {
-            const int yi = r0 + k;
-            if (yi < it.in_hi) {
-                const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
-                const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
-                const bool emit = yo >= emit_lo && yo < emit_hi;
-                const int shift = ALIGNED ? 0 : sshift[slot * SROWS + k];
-                // unaligned: this row's staging row, indexed so that srow[x - x0] has the
-                // global column's 16-B alignment
-                float* srow = nullptr;
-                if (staged)
-                    srow = stage_out + ((gs & 1) * SROWS + k) * (p.tw + 8) + row_shift(dcur, it.x0);
-#pragma unroll
-                for (int g = 0; g < GROUPS; ++g) {
-                    // a warp whose group lies wholly right of the image (the padding of a
-                    // partial last strip) has nothing to store: skip its arithmetic. The
-                    // test is warp-uniform (lane 0's columns), as store_shift shuffles.
-                    if (COL_EDGE && x4[g] - 4 * lane >= C) continue;
-                    float win[12];
-                    if (ALIGNED) {
-                        load_win(win, sstage + k * SW + g * tw2);
-                    } else {
-                        load_win_shift(win, sstage + k * SW + g * tw2 + 4, shift);
-                    }
-                    F4 own;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) own.v[i] = win[4 + i];
-                    F4 outv;
-                    if (MODE == MODE_HPASS) {
-                        if (live) {
-                            outv = row_pass<RAD, SYMW>(win, p.w, p.one);
+        // A stage whose rows all exist and all emit (every stage of an interior item
+        // but its first and last) runs without per-row range tests.
+        auto stage_rows = [&](auto fast_stage) {
+            constexpr bool FAST = decltype(fast_stage)::value;
+    #pragma unroll
+            for (int k = 0; k < SROWS; ++k) {
+                const int yi = r0 + k;
+                if (FAST || yi < it.in_hi) {
+                    const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
+                    const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
+                    const bool emit = FAST || (yo >= emit_lo && yo < emit_hi);
+                    const int shift = ALIGNED ? 0 : sshift[slot * SROWS + k];
+                    // unaligned: this row's staging row, indexed so that srow[x - x0] has the
+                    // global column's 16-B alignment
+                    float* srow = nullptr;
+                    if (staged)
+                        srow = stage_out + ((gs & 1) * SROWS + k) * (p.tw + 8) + row_shift(dcur, it.x0);
+    #pragma unroll
+                    for (int g = 0; g < GROUPS; ++g) {
+                        // a warp whose group lies wholly right of the image (the padding of a
+                        // partial last strip) has nothing to store: skip its arithmetic. The
+                        // test is warp-uniform (lane 0's columns), as store_shift shuffles.
+                        if (COL_EDGE && x4[g] - 4 * lane >= C) continue;
+                        float win[12];
+                        if (ALIGNED) {
+                            load_win(win, sstage + k * SW + g * tw2);
                         } else {
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) outv.v[i] = 0.0f;
+                            load_win_shift(win, sstage + k * SW + g * tw2 + 4, shift);
                         }
-                    } else if (single_like(MODE)) {
-                        if constexpr (SYM >= 1 && SC_F2 && RAD >= 1)
-                            outv = dense_fold_sym<RAD, NACC, (SYM >= 2)>(acc[g], win, p.k, p.one);
-                        else
-                            outv = dense_fold<RAD, NACC>(acc[g], win, p.k, p.one);
-                    } else {
-                        F4 v;
-                        if (fused_like(MODE)) {
+                        F4 own;
+    #pragma unroll
+                        for (int i = 0; i < 4; ++i) own.v[i] = win[4 + i];
+                        F4 outv;
+                        if (MODE == MODE_HPASS) {
                             if (live) {
-#ifdef SC_NOCOMPUTE
-                                v = own;
-#else
-                                v = row_pass<RAD, SYMW>(win, p.w, p.one);
-#endif
+                                outv = row_pass<RAD, SYMW>(win, p.w, p.one);
                             } else {
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) v.v[i] = 0.0f;  // faithful: scratch row stays 0
+    #pragma unroll
+                                for (int i = 0; i < 4; ++i) outv.v[i] = 0.0f;
                             }
+                        } else if (single_like(MODE)) {
+                            if constexpr (SYM >= 1 && SC_F2 && RAD >= 1)
+                                outv = dense_fold_sym<RAD, NACC, (SYM >= 2)>(acc[g], win, p.k, p.one);
+                            else
+                                outv = dense_fold<RAD, NACC>(acc[g], win, p.k, p.one);
                         } else {
-                            v = own;  // VPASS: src already holds the row-pass result
+                            F4 v;
+                            if (fused_like(MODE)) {
+                                if (live) {
+    #ifdef SC_NOCOMPUTE
+                                    v = own;
+    #else
+                                    v = row_pass<RAD, SYMW>(win, p.w, p.one);
+    #endif
+                                } else {
+    #pragma unroll
+                                    for (int i = 0; i < 4; ++i) v.v[i] = 0.0f;  // faithful: scratch row stays 0
+                                }
+                            } else {
+                                v = own;  // VPASS: src already holds the row-pass result
+                            }
+                            if constexpr (MODE == MODE_SPLITF) {
+                                // the reference's scratch row: H0 on the valid columns, 0 on the
+                                // column ring and on dead rows (the workspace is zeroed first,
+                                // S/conv.py:414); own rows only
+                                if (yi >= it.ylo && yi < it.yhi) {
+                                    float* hrow = p.scr + (long long)it.plane * p.scr_ps + (long long)yi * p.scr_rs;
+                                    if (fast[g]) {
+                                        st4(hrow + x4[g], v);
+                                    } else {
+                                        F4 zero;
+    #pragma unroll
+                                        for (int i = 0; i < 4; ++i) zero.v[i] = 0.0f;
+                                        store_edge<ALIGNED>(hrow, x4[g], C, RAD, v, zero, 2);
+                                    }
+                                }
+                            }
+    #ifdef SC_NOCOMPUTE
+                            outv = v;  // dev-only variant: pipeline cost without the arithmetic
+    #else
+                            outv = col_fold<RAD, NACC, SYMW>(acc[g], v, p.w, p.one);
+    #endif
                         }
-                        if constexpr (MODE == MODE_SPLITF) {
-                            // the reference's scratch row: H0 on the valid columns, 0 on the
-                            // column ring and on dead rows (the workspace is zeroed first,
-                            // S/conv.py:414); own rows only
-                            if (yi >= it.ylo && yi < it.yhi) {
-                                float* hrow = p.scr + (long long)it.plane * p.scr_ps + (long long)yi * p.scr_rs;
+                        if (MODE == MODE_HPASS) {
+                            // dead rows are written only under zero fill
+                            if (emit && (live || zero_fill)) {
+                                if (fast[g] && live)
+                                    st4(dcur + 4 * ct + g * tw2 + (it.x0), outv);
+                                else if (staged)
+                                    stage_cols(srow, x4[g], it.x0, C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
+                                else if (!ALIGNED)
+                                    store_shift(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0, lane);
+                                else
+                                    store_edge<ALIGNED>(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
+                            }
+                        } else if (emit) {
+                            if constexpr (MODE == MODE_SINGLECB) {
+                                // copy-back: the same valid samples into the image, in place
+                                float* irow = p.scr + (long long)it.plane * p.scr_ps + (long long)yo * p.scr_rs;
                                 if (fast[g]) {
-                                    st4(hrow + x4[g], v);
+                                    st4(irow + x4[g], outv);
                                 } else {
                                     F4 zero;
-#pragma unroll
+    #pragma unroll
                                     for (int i = 0; i < 4; ++i) zero.v[i] = 0.0f;
-                                    store_edge<ALIGNED>(hrow, x4[g], C, RAD, v, zero, 2);
+                                    store_edge<ALIGNED>(irow, x4[g], C, RAD, outv, zero, 0);
                                 }
                             }
-                        }
-#ifdef SC_NOCOMPUTE
-                        outv = v;  // dev-only variant: pipeline cost without the arithmetic
-#else
-                        outv = col_fold<RAD, NACC, SYMW>(acc[g], v, p.w, p.one);
-#endif
-                    }
-                    if (MODE == MODE_HPASS) {
-                        // dead rows are written only under zero fill
-                        if (emit && (live || zero_fill)) {
-                            if (fast[g] && live)
-                                st4(dcur + 4 * ct + g * tw2 + (it.x0), outv);
-                            else if (staged)
-                                stage_cols(srow, x4[g], it.x0, C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
-                            else if (!ALIGNED)
-                                store_shift(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0, lane);
-                            else
-                                store_edge<ALIGNED>(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
-                        }
-                    } else if (emit) {
-                        if constexpr (MODE == MODE_SINGLECB) {
-                            // copy-back: the same valid samples into the image, in place
-                            float* irow = p.scr + (long long)it.plane * p.scr_ps + (long long)yo * p.scr_rs;
                             if (fast[g]) {
-                                st4(irow + x4[g], outv);
+                                st4(dcur + x4[g], outv);
                             } else {
-                                F4 zero;
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) zero.v[i] = 0.0f;
-                                store_edge<ALIGNED>(irow, x4[g], C, RAD, outv, zero, 0);
-                            }
-                        }
-                        if (fast[g]) {
-                            st4(dcur + x4[g], outv);
-                        } else {
-                            F4 ringv;
-                            if (ring_copy) {
-                                int rr = slot * SROWS + k - RAD;  // ring row of input row yo
-                                if (rr < 0) rr += NS * SROWS;
-                                const float* rrow = ring + rr * SW + 4 * ct + g * tw2;
-                                if (ALIGNED) {
-                                    ringv = ld4(rrow + 4);
+                                F4 ringv;
+                                if (ring_copy) {
+                                    int rr = slot * SROWS + k - RAD;  // ring row of input row yo
+                                    if (rr < 0) rr += NS * SROWS;
+                                    const float* rrow = ring + rr * SW + 4 * ct + g * tw2;
+                                    if (ALIGNED) {
+                                        ringv = ld4(rrow + 4);
+                                    } else {
+                                        const float* q = rrow + 8 + sshift[rr];
+    #pragma unroll
+                                        for (int i = 0; i < 4; ++i) ringv.v[i] = q[i];
+                                    }
                                 } else {
-                                    const float* q = rrow + 8 + sshift[rr];
-#pragma unroll
-                                    for (int i = 0; i < 4; ++i) ringv.v[i] = q[i];
+    #pragma unroll
+                                    for (int i = 0; i < 4; ++i) ringv.v[i] = 0.0f;
                                 }
-                            } else {
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) ringv.v[i] = 0.0f;
+                                if (ALIGNED)
+                                    store_edge<ALIGNED>(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                                else if (staged)
+                                    stage_cols(srow, x4[g], it.x0, C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                                else
+                                    store_shift(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0, lane);
                             }
+                        }
+                        if (ROW_EDGE && ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD)) {
+                            float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
                             if (ALIGNED)
-                                store_edge<ALIGNED>(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0);
-                            else if (staged)
-                                stage_cols(srow, x4[g], it.x0, C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                                store_edge<ALIGNED>(drow, x4[g], C, 0, own, own, 1);
                             else
-                                store_shift(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0, lane);
+                                store_shift(drow, x4[g], C, 0, own, own, 1, lane);
                         }
                     }
-                    if (ROW_EDGE && ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD)) {
-                        float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
-                        if (ALIGNED)
-                            store_edge<ALIGNED>(drow, x4[g], C, 0, own, own, 1);
-                        else
-                            store_shift(drow, x4[g], C, 0, own, own, 1, lane);
-                    }
+                    if (emit) dcur += p.dst_row_stride;
                 }
-                if (emit) dcur += p.dst_row_stride;
             }
-        }
+        };
+        const int yo0 = (MODE == MODE_HPASS) ? r0 : r0 - RAD;
+        if (!ROW_EDGE && !COL_EDGE && r0 + SROWS <= it.in_hi && yo0 >= emit_lo && yo0 + SROWS <= emit_hi)
+            stage_rows(std::true_type{});
+        else
+            stage_rows(std::false_type{});
         if (staged) {
             // publish the stage's staged output rows: fence the generic-proxy smem
             // writes for the TMA engine, make sure the bulk stores of the previous
