@@ -261,6 +261,31 @@ __device__ __forceinline__ float2 mad2(float2 acc, float2 x, float2 w, float2 on
     return __ffma2_rn(__fmul2_rn(x, w), one, acc);
 }
 
+// acc + prod with one rounding (see mad2)
+__device__ __forceinline__ float2 add2p(float2 acc, float2 prod, float2 one) {
+    return __ffma2_rn(prod, one, acc);  // acc + prod, one rounding (see mad2)
+}
+
+// Product of the window pair (win[idx], win[idx+1]) with one tap. A pair that
+// starts at an odd index straddles two register pairs, and forming it costs a
+// MOV pair; two scalar multiplies writing an aligned product pair use the same
+// FMA-pipe slots as one FMUL2 and one instruction less (SC_ODD_SCALAR=0: always
+// FMUL2). Bits are identical either way.
+#ifndef SC_ODD_SCALAR
+#define SC_ODD_SCALAR 1
+#endif
+// the packed form always (the single pass's dense folds: scalar products there
+// raised its registers from 88-94 to 118-157)
+__device__ __forceinline__ float2 prod2p(const float (&win)[12], int idx, float kv) {
+    return __fmul2_rn(make_float2(win[idx], win[idx + 1]), make_float2(kv, kv));
+}
+__device__ __forceinline__ float2 prod2(const float (&win)[12], int idx, float kv) {
+#if SC_ODD_SCALAR
+    if (idx & 1) return make_float2(__fmul_rn(win[idx], kv), __fmul_rn(win[idx + 1], kv));
+#endif
+    return __fmul2_rn(make_float2(win[idx], win[idx + 1]), make_float2(kv, kv));
+}
+
 struct F4 {
     float v[4];
 };
@@ -525,9 +550,7 @@ __device__ __forceinline__ F4 row_pass(const float (&win)[12], const float* w, f
         const int o = HALO - RAD + c;
         float2 acc = __fmul2_rn(make_float2(win[o], win[o + 1]), make_float2(w[0], w[0]));
 #pragma unroll
-        for (int m = 1; m <= 2 * RAD; ++m)
-            acc = mad2(acc, make_float2(win[o + m], win[o + m + 1]),
-                       make_float2(w[tap_ix<RAD, SYMW>(m)], w[tap_ix<RAD, SYMW>(m)]), one2);
+        for (int m = 1; m <= 2 * RAD; ++m) acc = add2p(acc, prod2(win, o + m, w[tap_ix<RAD, SYMW>(m)]), one2);
         h.v[c] = acc.x;
         h.v[c + 1] = acc.y;
     }
@@ -607,25 +630,20 @@ __device__ __forceinline__ F4 dense_fold(F4 (&acc)[NACC], const float (&win)[12]
         const int o = HALO - RAD + c;
         float2 t = make_float2(acc[NACC - 1].v[c], acc[NACC - 1].v[c + 1]);
 #pragma unroll
-        for (int j = 0; j < W; ++j)
-            t = mad2(t, make_float2(win[o + j], win[o + j + 1]),
-                     make_float2(k[(W - 1) * W + j], k[(W - 1) * W + j]), one2);
+        for (int j = 0; j < W; ++j) t = add2p(t, prod2p(win, o + j, k[(W - 1) * W + j]), one2);
         out.v[c] = t.x;
         out.v[c + 1] = t.y;
 #pragma unroll
         for (int i = NACC - 1; i >= 1; --i) {
             t = make_float2(acc[i - 1].v[c], acc[i - 1].v[c + 1]);
 #pragma unroll
-            for (int j = 0; j < W; ++j)
-                t = mad2(t, make_float2(win[o + j], win[o + j + 1]), make_float2(k[i * W + j], k[i * W + j]),
-                         one2);
+            for (int j = 0; j < W; ++j) t = add2p(t, prod2p(win, o + j, k[i * W + j]), one2);
             acc[i].v[c] = t.x;
             acc[i].v[c + 1] = t.y;
         }
-        t = __fmul2_rn(make_float2(win[o], win[o + 1]), make_float2(k[0], k[0]));
+        t = prod2p(win, o, k[0]);
 #pragma unroll
-        for (int j = 1; j < W; ++j)
-            t = mad2(t, make_float2(win[o + j], win[o + j + 1]), make_float2(k[j], k[j]), one2);
+        for (int j = 1; j < W; ++j) t = add2p(t, prod2p(win, o + j, k[j]), one2);
         acc[0].v[c] = t.x;
         acc[0].v[c + 1] = t.y;
     }
@@ -665,9 +683,6 @@ __device__ __forceinline__ F4 dense_fold(F4 (&acc)[NACC], const float (&win)[12]
 // used twice. Fold order and every rounding are unchanged (bit-identical);
 // (2r+1)*r fewer multiplies per input row (25 -> 15 at r = 2) in an FP32-bound
 // kernel.
-__device__ __forceinline__ float2 add2p(float2 acc, float2 prod, float2 one) {
-    return __ffma2_rn(prod, one, acc);  // acc + prod, one rounding (see mad2)
-}
 
 // COLSYM: the matrix is also mirror-symmetric in its columns (K[i][j] == K[i][2r-j]:
 // outer(w, w) of symmetric taps). The products of column pair c with tap j and
@@ -691,7 +706,7 @@ __device__ __forceinline__ F4 dense_fold_sym(F4 (&acc)[NACC], const float (&win)
             for (int j = 0; j < W; ++j)
             {
                 const int kj = COLSYM ? (j < W - 1 - j ? j : W - 1 - j) : j;
-                pr[i][j] = __fmul2_rn(make_float2(win[o + j], win[o + j + 1]), make_float2(k[i * W + kj], k[i * W + kj]));
+                pr[i][j] = prod2p(win, o + j, k[i * W + kj]);
             }
         float2 t = make_float2(acc[NACC - 1].v[c], acc[NACC - 1].v[c + 1]);
 #pragma unroll
