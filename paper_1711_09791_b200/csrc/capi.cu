@@ -638,6 +638,7 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
     p.hrow_lo = (flags & SC_EXTENDED) ? 0 : rad;
     p.hrow_hi = (flags & SC_EXTENDED) ? R : R - rad;
     p.flags = flags;
+    if ((long long)R * C >= (1LL << 25)) p.flags |= F_U8_LEAN;  // >= 32 Mpixel: the lean loops pay
     p.one = 1.0f;
     for (int i = 0; i < width; ++i) p.w[i] = taps[i];
     // 4 columns per consumer thread; strips of TW = 4*nt columns, nt minimising padding

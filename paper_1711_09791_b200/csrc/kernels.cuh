@@ -67,6 +67,7 @@ constexpr int F_NO_RING = 0x2;
 constexpr int F_ZERO_FILL = 0x4;
 // tuning flags (set by the planner from SC_* environment variables)
 constexpr int F_STAGED_STORE = 0x200;  // unaligned kernels: dst rows not all 16-B aligned -> staged TMA stores
+constexpr int F_U8_LEAN = 0x400;  // u8 kernel: interior strips take the lean loops (large payloads)
 constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (default: evict_normal,
                                          // which lets neighbouring bands' halo rows hit in L2)
 

@@ -92,3 +92,25 @@ def test_fused_u8_large_against_float_path():
         fused = dev.two_pass_u8hwc(src, np.asarray(taps, np.float32))
         ref = dev.planes_to_hwc(dev.two_pass(dev.hwc_to_planes(src), np.asarray(taps, np.float32)))
         assert torch.equal(fused, ref)
+
+
+@pytest.mark.gpu
+def test_fused_u8_large_payload_lean_loops():
+    """Payloads of >= 32 Mpixel take the u8 kernel's lean loops (interior strips,
+    full stages without per-row tests): same bytes as unpack -> fused f32 -> pack."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_09791_b200 import device as dev
+
+    R, C = 4100, 8192  # 33.6 Mpixel; 4100 rows: the last band is short
+    g = torch.Generator(device="cuda").manual_seed(11)
+    src = torch.randint(0, 256, (R, C, 3), dtype=torch.uint8, device="cuda", generator=g)
+    for taps in ([1 / 16, 4 / 16, 6 / 16, 4 / 16, 1 / 16], [-1, -2, 7, -2, -1], [0.1, -0.3, 0.9, 0.2, 0.1]):
+        w = np.asarray(taps, np.float32)
+        fused = dev.two_pass_u8hwc(src, w)
+        ref = dev.planes_to_hwc(dev.two_pass(dev.hwc_to_planes(src), w))
+        assert torch.equal(fused, ref)
+        fused_ext = dev.two_pass_u8hwc(src, w, extended=True)
+        ref_ext = dev.planes_to_hwc(dev.two_pass(dev.hwc_to_planes(src), w, extended=True))
+        assert torch.equal(fused_ext, ref_ext)
