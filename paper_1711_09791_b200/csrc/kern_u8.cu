@@ -300,9 +300,9 @@ __global__ void __launch_bounds__(SC_U8_MAXT, SC_U8_MINB) sepconv_u8_kernel(cons
         const bool edge = in_lo < p.hrow_lo || in_hi > p.hrow_hi || ylo < RAD || yhi > p.R - RAD;
         if (edge)
             u8_item<RAD, true, SYMW>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
-        else if (!(p.flags & F_U8_LEAN) || x0 < RAD || x0 + p.tw > p.C - RAD)
+        else if (RAD >= 4 || !(p.flags & F_U8_LEAN) || x0 < RAD || x0 + p.tw > p.C - RAD)
             u8_item<RAD, false, SYMW>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
-        else
+        else if constexpr (RAD < 4)  // r = 4 with the lean variant spills
             u8_item<RAD, false, SYMW, false>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
     }
 }
