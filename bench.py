@@ -399,6 +399,24 @@ def main():
                                   "10 back-to-back kernel-only launches after the timed region"),
                 "kernel_ms_back_to_back": round(kms_b2b, 4),
                 "alg_bytes_per_launch": kernel_bytes}
+    if flush is not None and world == 1:
+        # small inputs: a plain copy of the same image under the same protocol (L2
+        # flushed before every step) -- the floor launch latency and DRAM ramp set
+        # at this size, next to the big-transfer peak above
+        dst_copy = torch.empty_like(src)
+        cpairs = []
+        for _ in range(min(args.steps, 100)):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dst_copy.copy_(src)
+            b.record(stream)
+            cpairs.append((a, b))
+        torch.cuda.synchronize()
+        copy_ms = statistics.median(a.elapsed_time(b) for a, b in cpairs)
+        roofline["same_size_copy_ms"] = round(copy_ms, 4)
+        roofline["frac_of_same_size_copy"] = round(copy_ms / ms, 4)
+        del dst_copy
 
     # ---- end to end through the C-ABI host entry point (pinned host planes)
     e2e = None
