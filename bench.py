@@ -15,8 +15,9 @@ e2e: the same metric through the C-ABI host entry point (sc_two_pass_host_f32):
 pinned host planes in, H2D + kernel + D2H inside the timed region.
 
 Inputs are 3.2 GB, far larger than the 126 MB L2, so no flush is needed between
-timed steps. --impl reference times the reference algorithm on the host CPU
-(the oracle's numpy port of sepconv_lab's StaticChunked two-pass).
+timed steps. --impl reference times the reference's own CPU path on the host
+cores: the real sepconv_lab package (baseline/_ref),
+convolve_image(TWO_PASS, StaticChunked(os.cpu_count())) on the full workload.
 """
 
 from __future__ import annotations
@@ -126,42 +127,122 @@ def dist_env():
     return world, rank, local
 
 
-def reference_arm(args, wl):
-    """The reference algorithm on host cores (numpy port of the reference's
-    vectorised StaticChunked two-pass; oracle/oracle.py) -- rank 0 only."""
-    world, rank, _ = dist_env()
-    if rank != 0:
-        return 0
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_reference():
+    """The real reference package, sepconv_lab, from baseline/_ref (the pip install
+    of /root/reference/pkg that travels with the repo), or None."""
+    if os.path.isdir(REF_INSTALL) and REF_INSTALL not in sys.path:
+        sys.path.append(REF_INSTALL)
+    try:
+        import sepconv_lab
+    except ImportError:
+        return None
+    return sepconv_lab
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ReferenceRun:
+    """One step of the workload through the reference's own CPU path:
+    sepconv_lab.convolve_image(image, kernel, TWO_PASS, StaticChunked(cores),
+    workspace=..., pool=...) (S/executors.py:269-405) on the FULL image of the
+    configuration (every frame for a batch), vectorised, with one worker pool
+    reused across steps as the reference's time_variant does (S/bench.py:134-179).
+    The input samples are the bench's own (the same seeded splitmix64 stream,
+    generated by the oracle's C generator so the two arms convolve identical data)."""
+
+    def __init__(self, sl, wl, cores):
+        from oracle import oracle as orc
+
+        self.sl, self.wl = sl, wl
+        P, R, C = wl.planes, wl.rows, wl.cols
+        self.buf = orc.synthetic(wl.frames * P * R * C, wl.seed, wl.kind).reshape(wl.frames, P, R, C)
+        # zero-copy Images over the (F, P, R, C) buffer (Plane keeps float32 C-contiguous views, S/image.py:37-39)
+        self.images = [sl.Image([sl.Plane(self.buf[f, p]) for p in range(P)]) for f in range(wl.frames)]
+        self.workspace = sl.Image.zeros(R, C, P)
+        self.kernel = sl.SeparableKernel(wl.tap_vector())
+        self.variant = sl.ConvVariant(sl.Algorithm.TWO_PASS)
+        self.plan = sl.StaticChunked(workers=cores)
+        self.pool = sl.WorkerPool(cores)
+
+    def __call__(self):
+        for img in self.images:
+            self.sl.convolve_image(img, self.kernel, self.variant, self.plan, workspace=self.workspace,
+                                   pool=self.pool)
+
+    def close(self):
+        self.pool.close()
+
+
+def _port_run(wl, cores, rows):
+    """Fallback when sepconv_lab is not installed: the oracle's numpy port of the
+    same StaticChunked two-pass on a row slice (kind "port")."""
     from oracle import oracle as orc
 
-    cores = os.cpu_count() or 1
-    rows = max(64, min(wl.rows, args.ref_rows))
-    sample_px = rows * wl.cols
     w = wl.tap_vector()
     planes = [orc.synthetic(rows * wl.cols, wl.seed, wl.kind, offset=p * wl.rows * wl.cols).reshape(rows, wl.cols)
               for p in range(wl.planes)]
     scratch = [np.zeros_like(p) for p in planes]
     run = orc.NumpyTwoPass(cores)
+    return (lambda: run(planes, scratch, w)), run.close
+
+
+def reference_arm(args, wl):
+    """The reference's own CPU implementation of the path on the host cores (rank 0
+    only; other ranks exit without work): the real sepconv_lab package on the FULL
+    configured workload, same steps and warm-up as our arm."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    sl = import_reference()
+    if sl is not None:
+        run = ReferenceRun(sl, wl, cores)
+        fn, close = run, run.close
+        px = wl.pixels
+        kind = "reference"
+        sample = (f"the full workload per step ({wl.frames} x {wl.planes}x{wl.rows}x{wl.cols}): sepconv_lab "
+                  f"{sl.__version__} (baseline/_ref) convolve_image(TWO_PASS, StaticChunked({cores})), vectorised, "
+                  f"one WorkerPool reused (S/executors.py:269-405, S/bench.py:134-179)")
+    else:
+        rows = max(64, min(wl.rows, args.ref_rows))
+        fn, close = _port_run(wl, cores, rows)
+        px = rows * wl.cols
+        kind = "port"
+        sample = (f"{wl.planes}x{rows}x{wl.cols} slice of {wl.name} per step (sepconv_lab not installed: numpy "
+                  f"port of the reference's vectorised two-pass, StaticChunked({cores}) threads)")
+    times = []
     try:
         for _ in range(args.warmup):
-            run(planes, scratch, w)
-        t0 = time.perf_counter()
+            fn()
         for _ in range(args.steps):
-            run(planes, scratch, w)
-        dt = (time.perf_counter() - t0) / args.steps
+            t0 = time.perf_counter()
+            fn()
+            times.append(time.perf_counter() - t0)
     finally:
-        run.close()
-    value = sample_px / dt / 1e9
-    sample = (f"{wl.planes}x{rows}x{wl.cols} slice of {wl.name} per step (numpy port of the reference's "
-              f"vectorised two-pass, StaticChunked({cores}) threads, S/executors.py:366-380)")
+        close()
+    dt = sum(times) / len(times)
+    value = px / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gpix/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "weak" if wl.frames > 1 else "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{wl.name}: {wl.note}", "sample_rows": rows},
-        "cpu_baseline": {"value": round(value, 6), "unit": "Gpix/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "config": {"workload": f"{wl.name}: {wl.note}", "frames": wl.frames, "planes": wl.planes, "rows": wl.rows,
+                   "cols": wl.cols, "taps": [float(v) for v in wl.tap_vector()]},
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gpix/s", "cores": cores, "kind": kind,
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 6), "unit": "Gpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -169,32 +250,34 @@ def reference_arm(args, wl):
 
 
 def cpu_baseline(wl):
-    """Bounded CPU sample of the same workload (reported baseline, not the target)."""
-    from oracle import oracle as orc
-
+    """Bounded sample of the same workload on the reference's own CPU path (the
+    real sepconv_lab when installed): 1 warm-up, then steps until ~10 s of CPU
+    work (at least 2). Reported baseline, not the target."""
     cores = os.cpu_count() or 1
-    rows = min(wl.rows, 2048)
-    w = wl.tap_vector()
-    planes = [orc.synthetic(rows * wl.cols, wl.seed, wl.kind, offset=p * wl.rows * wl.cols).reshape(rows, wl.cols)
-              for p in range(wl.planes)]
-    scratch = [np.zeros_like(p) for p in planes]
-    run = orc.NumpyTwoPass(cores)
+    sl = import_reference()
+    if sl is not None:
+        run = ReferenceRun(sl, wl, cores)
+        fn, close, px, kind = run, run.close, wl.pixels, "reference"
+        what = (f"full {wl.name} workload per step, sepconv_lab {sl.__version__} convolve_image(TWO_PASS, "
+                f"StaticChunked({cores}))")
+    else:
+        rows = min(wl.rows, 2048)
+        fn, close = _port_run(wl, cores, rows)
+        px, kind = rows * wl.cols, "port"
+        what = f"{wl.planes}x{rows}x{wl.cols} slice of {wl.name}, numpy port, StaticChunked({cores})"
     try:
-        run(planes, scratch, w)  # warm-up (S/bench.py:158-159)
-        # ~10 s of CPU work (a bounded sample; at least 3 reps)
+        fn()  # warm-up (S/bench.py:158-159)
         reps, t0 = 0, time.perf_counter()
         while True:
-            run(planes, scratch, w)
+            fn()
             reps += 1
             el = time.perf_counter() - t0
-            if (el > 10.0 and reps >= 3) or reps >= 200:
+            if (el > 10.0 and reps >= 2) or reps >= 200:
                 break
     finally:
-        run.close()
-    return {"value": round(rows * wl.cols * reps / el / 1e9, 6), "unit": "Gpix/s", "cores": cores,
-            "kind": "port",
-            "sample": f"{wl.planes}x{rows}x{wl.cols} slice of {wl.name}, {reps} reps after 1 warm-up, numpy port "
-                      f"of the reference two-pass with StaticChunked({cores}) threads"}
+        close()
+    return {"value": round(px * reps / el / 1e9, 6), "unit": "Gpix/s", "cores": cores, "kind": kind,
+            "cpu_model": cpu_model(), "sample": f"{what}; {reps} steps after 1 warm-up"}
 
 
 def host_chunk_bytes(rows, cols, planes, r, band_lo, band_hi, in_lo, in_hi, call_planes=None):
@@ -380,6 +463,11 @@ def main():
         b.synchronize()
         kev.append(a.elapsed_time(b) / 10)
     kms_b2b = statistics.median(kev)
+    if world > 1:
+        # peer transport: those launches read the neighbours' buffers; nobody goes on
+        # (and later frees or unmaps anything) before every rank's reads are done
+        torch.cuda.synchronize()
+        dist.barrier()
     # When a step IS one launch of the kernel (N=1, or N>1 with in-kernel peer halo
     # reads), its duration is read from the timed region itself (CUDA events on the
     # launching stream, this rank); otherwise (NCCL transport: two launches and an
@@ -484,6 +572,46 @@ def main():
                "sc_two_pass_host_band_f32 per rank (its row band + halo rows from its pinned host copy, chunked "
                "H2D/kernel/D2H on 3 streams)"}
 
+    # ---- end to end as a sepconv_lab user makes the call: the reference's own
+    # convolve_image with the Cuda plan (plugin.py) on its numpy (PAGEABLE) planes,
+    # no workspace (the reference's internal one is unobservable: fused path), in
+    # place; the library stages pageable rows through its pinned ring
+    e2e_pageable = None
+    if args.e2e_steps > 0 and band is not None and world == 1:
+        if "host" in locals():
+            del host, planes  # noqa: F821 - release the pinned copies first
+        sl = import_reference()
+        from paper_1711_09791_b200 import plugin
+        from paper_1711_09791_b200.executors import Cuda
+
+        pg = np.empty((P, R, C), dtype=np.float32)
+        for p in range(P):
+            pg[p] = src[p].cpu().numpy()
+        if sl is not None:
+            plugin.install(sl)
+            img = sl.Image([sl.Plane(pg[p]) for p in range(P)])
+            kern, var = sl.SeparableKernel(w), sl.ConvVariant(sl.Algorithm.TWO_PASS)
+            call = "sepconv_lab.convolve_image(image, kernel, TWO_PASS, Cuda()) with the plugin installed"
+        else:
+            import paper_1711_09791_b200 as pkg
+
+            img = pkg.Image([pkg.Plane(pg[p]) for p in range(P)])
+            kern, var = pkg.SeparableKernel(w), pkg.ConvVariant(pkg.Algorithm.TWO_PASS)
+            call = "paper_1711_09791_b200.convolve_image(image, kernel, TWO_PASS, Cuda())"
+        conv = sl.convolve_image if sl is not None else pkg.convolve_image
+        conv(img, kern, var, Cuda(device=local))
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            conv(img, kern, var, Cuda(device=local))
+        pg_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        h2d, d2h = host_chunk_bytes(R, C, P, r, 0, R, 0, R)
+        e2e_pageable = {"value": round(total_px / (pg_ms / 1e3) / 1e9, 4), "unit": "Gpix/s",
+                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(pg_ms, 3),
+                        "path": call + " on pageable numpy planes (library pinned staging ring + host copy threads)"}
+        if e2e:
+            e2e_pageable["frac_of_pinned"] = round(e2e_pageable["value"] / e2e["value"], 4)
+        del img, pg
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl)
@@ -501,11 +629,15 @@ def main():
                        **({"halo": halo} if band is not None and world > 1 else {})},
             "effective_GBps": round(eff, 1), "pct_of_8TBps": round(100 * eff / NOMINAL_HBM_GBPS, 2),
             "pct_of_measured_copy": round(100 * eff / peak, 2),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,
+            "gpu_launches": int(launches),
             "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if band is not None and stepper is not None and hasattr(stepper, "close"):
+            stepper.close()  # barriers before unmapping: exporters outlive importers
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

@@ -170,6 +170,16 @@ int sc_planes_f32_to_hwc_u8(const float *src, uint8_t *dst, int rows, int cols, 
 int sc_two_pass_host_f32(const float *const *src_planes, float *const *dst_planes, int nplanes,
                          int rows, int cols, const float *taps, int width, int flags, int device);
 
+/* The reference's exact end state of BOTH host buffers of
+ * convolve_image(image, kernel, TWO_PASS, plan, workspace=workspace)
+ * (S/executors.py:303-326): workspace := H0 (zeroed, then the row pass on rows
+ * [r, R-r) or every row with SC_EXTENDED, cols [r, C-r)), image[valid] := V(H0)
+ * in place, image ring untouched. Streams like sc_two_pass_host_f32 (each chunk
+ * also writes its H0 rows back). Replaces the two per-plane phases the
+ * reference's executor runs (horizontal then vertical rows, S/executors.py:318-323). */
+int sc_two_pass_host_split_f32(float *const *image_planes, float *const *scratch_planes, int nplanes, int rows,
+                               int cols, const float *taps, int width, int flags, int device);
+
 /* Rows [out_lo, out_hi) only (one rank's row band of a host-resident image,
  * global-row rules): reads host rows [out_lo-r, out_hi+r) clipped to the image,
  * writes host rows [out_lo, out_hi); plane pointers address row 0 and no other

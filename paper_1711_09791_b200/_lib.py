@@ -52,6 +52,7 @@ EXPORTS = (
     "sc_copy_region_f32",
     "sc_fill_synthetic_f32",
     "sc_two_pass_host_f32",
+    "sc_two_pass_host_split_f32",
     "sc_two_pass_host_band_f32",
     "sc_two_pass_host_multi_f32",
     "sc_two_pass_u8hwc",
@@ -94,6 +95,7 @@ _SIGNATURES = {
     "sc_copy_region_f32": (_STRIDED + [_i32, _i32, _i32, _i32, _vp], _i32),
     "sc_fill_synthetic_f32": ([_vp, _i64, _u64, _u64, _i32, _vp], _i32),
     "sc_two_pass_host_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
+    "sc_two_pass_host_split_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_two_pass_host_band_f32": ([_vp, _vp, _i32, _i32, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_two_pass_host_multi_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _i32], _i32),
     "sc_two_pass_u8hwc": ([_vp, _vp, _i32, _i32, _i64, _i64, _fp, _i32, _i32, _vp], _i32),

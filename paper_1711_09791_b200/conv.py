@@ -66,7 +66,8 @@ def _torch():
 
 
 def _is_dev(p: Plane) -> bool:
-    return p.on_device
+    # duck-typed: the reference's Plane (numpy data) works too
+    return bool(getattr(p.data, "is_cuda", False))
 
 
 def _shares(a: Plane, b: Plane) -> bool:

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -134,28 +135,78 @@ static int occupancy(const void* kern, int threads, size_t smem) {
     return occ;
 }
 
-// Ring of zeroed [next, finished] ticket pairs per device for the kernels'
-// dynamic item scheduling; the last CTA of a launch re-zeroes its pair, so a
-// slot is reusable once its launch retired (1024 launches in flight at most).
-static constexpr int kWorkSlots = 1024;
+// [next item, finished CTAs] ticket pairs for the kernels' dynamic item
+// scheduling. The last CTA of a launch re-zeroes its pair, so a pair may be
+// reused by any launch that is ORDERED after it:
+//  * eager launches: one pair per (device, stream), keyed by the stream's
+//    unique id (cudaStreamGetId: never reused within a context, unlike the
+//    handle). Launches on one stream are ordered -- with programmatic dependent
+//    launch too, since tickets are only claimed after griddepcontrol.wait, i.e.
+//    after the previous grid completed. Launches on different streams never
+//    share a pair, however many are queued.
+//  * launches captured into a CUDA graph: a pair of their own, never handed out
+//    again (replays of one graph are serialised by CUDA, and each replay's last
+//    CTA re-zeroes it for the next).
+// Pairs come from zeroed pools of kPoolPairs, allocated on demand with stream
+// capture relaxed for this thread and zeroed on a private stream (no device-wide
+// synchronisation, legal while the caller's stream is capturing).
+static constexpr int kPoolPairs = 4096;
 
-static int* work_slot(int dev) {
-    static std::mutex mu;
-    static std::map<int, int*> bufs;
-    static std::map<int, unsigned> next;
-    std::lock_guard<std::mutex> lk(mu);
-    int*& b = bufs[dev];
-    if (!b) {
-        if (cudaMalloc(&b, sizeof(int) * 2 * kWorkSlots) != cudaSuccess) {
+struct TicketPools {
+    std::mutex mu;
+    std::map<int, std::vector<int*>> pools;            // device -> pools
+    std::map<int, long long> used;                     // device -> pairs handed out
+    std::map<std::pair<int, unsigned long long>, int*> by_stream;  // (device, stream id) -> pair
+};
+
+static TicketPools& tickets() {
+    static TicketPools t;
+    return t;
+}
+
+static int* new_pair_locked(TicketPools& t, int dev) {
+    long long& u = t.used[dev];
+    std::vector<int*>& pools = t.pools[dev];
+    if (u >= (long long)pools.size() * kPoolPairs) {
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        int* b = nullptr;
+        cudaStream_t zs = nullptr;
+        bool ok = cudaMalloc(&b, sizeof(int) * 2 * kPoolPairs) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&zs, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaMemsetAsync(b, 0, sizeof(int) * 2 * kPoolPairs, zs) == cudaSuccess &&
+                  cudaStreamSynchronize(zs) == cudaSuccess;
+        if (zs) cudaStreamDestroy(zs);
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        if (!ok) {
             cudaGetLastError();
-            b = nullptr;
+            if (b) cudaFree(b);
             return nullptr;
         }
-        cudaMemset(b, 0, sizeof(int) * 2 * kWorkSlots);
-        cudaDeviceSynchronize();
+        pools.push_back(b);
     }
-    const unsigned k = next[dev]++ % kWorkSlots;
-    return b + 2 * k;
+    int* pair = pools[u / kPoolPairs] + 2 * (u % kPoolPairs);
+    ++u;
+    return pair;
+}
+
+static int* work_slot(int dev, cudaStream_t s) {
+    TicketPools& t = tickets();
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+        cudaGetLastError();
+        cap = cudaStreamCaptureStatusNone;
+    }
+    std::lock_guard<std::mutex> lk(t.mu);
+    if (cap == cudaStreamCaptureStatusActive) return new_pair_locked(t, dev);
+    unsigned long long id = 0;
+    if (cudaStreamGetId(s, &id) != cudaSuccess) {
+        cudaGetLastError();
+        id = ~0ULL - reinterpret_cast<uintptr_t>(s);
+    }
+    int*& pair = t.by_stream[{dev, id}];
+    if (!pair) pair = new_pair_locked(t, dev);
+    return pair;
 }
 
 #ifdef SC_TRACE
@@ -521,7 +572,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.band_h2 = pl.band_h2;
     p.nitems = pl.nitems;
     p.nitems0 = pl.nitems0;
-    p.work = work_slot(dev);
+    p.work = work_slot(dev, s);
     if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
     float* side = nullptr;
     if (j.mode == MODE_SPLITF || j.mode == MODE_SINGLECB) {
@@ -671,7 +722,7 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
     const long long nitems = (long long)p.nstrips * ((R + band_h - 1) / band_h);
     p.nitems = (int)nitems;
     const int grid = (int)(nitems < G ? nitems : G);
-    p.work = work_slot(dev);
+    p.work = work_slot(dev, s);
     if (!p.work) return fail(SC_CUDA_ERROR, "cannot allocate the work counters");
     void* args[] = {&p};
     cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, s);

@@ -2,9 +2,14 @@
 // odd width on its generic and two-pass bodies (S/kernels.py:17-20,
 // S/conv.py:86-143, :215-318). The tuned row-streaming kernels keep a 4-column
 // smem halo and a 12-sample register window, i.e. r <= 4; wider kernels run
-// here: one thread per output sample, taps in global memory, the same float32
-// products and sums in the reference's order (bit-identical), no tuning. Up to
-// MAX_W_WIDE taps.
+// here: one thread per output sample, the same float32 products and sums in the
+// reference's order (bit-identical), no tuning. Up to MAX_W_WIDE taps. The taps
+// travel BY VALUE in the kernel parameters (a __grid_constant__ struct, read
+// through the constant cache): no per-launch allocation or host copy, so these
+// launches are stream-ordered like any other and capture into CUDA graphs. The
+// dense single-pass matrix fits up to width 89 (89^2 floats < the 32 KB
+// parameter limit); wider dense matrices are copied to a stream-ordered device
+// buffer per launch.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -17,7 +22,11 @@
 
 namespace sc {
 
-struct WideParams {
+constexpr int kWideSepTaps = MAX_W_WIDE + 1;  // separable taps (2r+1 <= 255)
+constexpr int kWideDenseTaps = 89 * 89;        // dense matrix by value up to width 89
+
+template <int NT>
+struct WideParamsT {
     const float* src;
     float* dst;
     long long sps, srs, dps, drs;
@@ -26,10 +35,13 @@ struct WideParams {
     int out_lo, out_hi, out_lo2, out_hi2;  // output rows (global), second segment optional
     int hrow_lo, hrow_hi;                  // rows where the row pass is live
     int flags;
-    const float* taps;  // device: 2r+1 floats, or (2r+1)^2 (single pass)
+    const float* taps_dev;  // dense matrices wider than 89: device copy (else null)
+    float taps[NT];         // 2r+1 floats, or (2r+1)^2 (single pass)
 };
+using WideParams = WideParamsT<kWideSepTaps>;
 
-__device__ __forceinline__ int wide_row(const WideParams& p, long long i, int& x, int& plane) {
+template <class P>
+__device__ __forceinline__ int wide_row(const P& p, long long i, int& x, int& plane) {
     // i -> (plane, output row of the one or two segments, column)
     const long long n1 = (long long)(p.out_hi - p.out_lo) * p.C;
     const long long n2 = (long long)(p.out_hi2 - p.out_lo2) * p.C;
@@ -46,7 +58,7 @@ __device__ __forceinline__ int wide_row(const WideParams& p, long long i, int& x
 
 // horizontal_rows_vec (S/conv.py:215-240) with the HPASS policies: live rows get
 // H on the valid columns; with F_ZERO_FILL the ring columns and dead rows get 0.
-__global__ void wide_hpass_kernel(const WideParams p) {
+__global__ void wide_hpass_kernel(const __grid_constant__ WideParams p) {
     const int W = 2 * p.rad + 1;
     const long long total = (long long)p.nplanes * ((p.out_hi - p.out_lo) + (p.out_hi2 - p.out_lo2)) * p.C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -70,7 +82,7 @@ __global__ void wide_hpass_kernel(const WideParams p) {
 // vertical_rows_vec (S/conv.py:269-293) over valid rows, valid columns; for the
 // fused two-pass (FUSED: src = H0 rows, ring = the input image) the ring samples
 // are copied from the input unless F_NO_RING.
-__global__ void wide_vpass_kernel(const WideParams p, const float* ring_src, long long ring_ps, long long ring_rs,
+__global__ void wide_vpass_kernel(const __grid_constant__ WideParams p, const float* ring_src, long long ring_ps, long long ring_rs,
                                   int ring_row0, int fused) {
     const int W = 2 * p.rad + 1;
     const long long total = (long long)p.nplanes * ((p.out_hi - p.out_lo) + (p.out_hi2 - p.out_lo2)) * p.C;
@@ -92,8 +104,10 @@ __global__ void wide_vpass_kernel(const WideParams p, const float* ring_src, lon
 }
 
 // single_pass_rows_vec (S/conv.py:86-114): row-major fold from the first product.
-__global__ void wide_single_kernel(const WideParams p) {
+template <int NT>
+__global__ void wide_single_kernel(const __grid_constant__ WideParamsT<NT> p) {
     const int W = 2 * p.rad + 1;
+    const float* k = p.taps_dev ? p.taps_dev : p.taps;
     const long long total = (long long)p.nplanes * ((p.out_hi - p.out_lo) + (p.out_hi2 - p.out_lo2)) * p.C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -101,10 +115,10 @@ __global__ void wide_single_kernel(const WideParams p) {
         const int y = wide_row(p, i, x, pl);
         if (x < p.rad || x >= p.C - p.rad || y < p.rad || y >= p.R - p.rad) continue;
         const float* s = p.src + pl * p.sps + (long long)(y - p.rad - p.src_row0) * p.srs + (x - p.rad);
-        float acc = __fmul_rn(s[0], p.taps[0]);
+        float acc = __fmul_rn(s[0], k[0]);
         for (int a = 0; a < W; ++a)
             for (int b = (a == 0 ? 1 : 0); b < W; ++b)
-                acc = __fadd_rn(acc, __fmul_rn(s[(long long)a * p.srs + b], p.taps[a * W + b]));
+                acc = __fadd_rn(acc, __fmul_rn(s[(long long)a * p.srs + b], k[a * W + b]));
         p.dst[pl * p.dps + (long long)(y - p.dst_row0) * p.drs + x] = acc;
     }
 }
@@ -118,31 +132,8 @@ static int wide_grid(long long total) {
     return b < 1 ? 1 : (int)b;
 }
 
-int launch_wide(const RowsJob& j, cudaStream_t s) {
-    if (j.above || j.below) {
-        set_error("kernel widths above 9 are not supported for peer-memory row bands");
-        return SC_UNSUPPORTED_WIDTH;
-    }
-    if (j.width > MAX_W_WIDE) {
-        set_error("kernel width " + std::to_string(j.width) + " > " + std::to_string(MAX_W_WIDE) + " not supported");
-        return SC_UNSUPPORTED_WIDTH;
-    }
-    const int rad = j.width / 2;
-    const bool single = j.mode == MODE_SINGLE;
-    const int ntaps = single ? j.width * j.width : j.width;
-    const float* host_taps = single ? j.dense : j.taps;
-    const long long outs = (long long)j.nplanes * ((j.out_hi - j.out_lo) + (j.out_hi2 - j.out_lo2)) * j.C;
-    if (outs <= 0) return SC_OK;
-    float* taps = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&taps), sizeof(float) * ntaps, s);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        set_error(std::string("wide taps allocation: ") + cudaGetErrorString(e));
-        return SC_CUDA_ERROR;
-    }
-    e = cudaMemcpyAsync(taps, host_taps, sizeof(float) * ntaps, cudaMemcpyHostToDevice, s);
-    WideParams p;
-    std::memset(&p, 0, sizeof(p));
+template <class P>
+static void fill_common(P& p, const RowsJob& j, int rad) {
     p.src = j.src;
     p.dst = j.dst;
     p.sps = j.sps;
@@ -162,61 +153,109 @@ int launch_wide(const RowsJob& j, cudaStream_t s) {
     p.hrow_lo = j.hrow_lo;
     p.hrow_hi = j.hrow_hi;
     p.flags = j.flags;
-    p.taps = taps;
-    float* h0 = nullptr;
-    if (e == cudaSuccess) {
-        switch (j.mode) {
-            case MODE_HPASS:
-                wide_hpass_kernel<<<wide_grid(outs), 256, 0, s>>>(p);
-                count_launch();
-                break;
-            case MODE_VPASS:
-                wide_vpass_kernel<<<wide_grid(outs), 256, 0, s>>>(p, nullptr, 0, 0, 0, 0);
-                count_launch();
-                break;
-            case MODE_SINGLE:
-                wide_single_kernel<<<wide_grid(outs), 256, 0, s>>>(p);
-                count_launch();
-                break;
-            case MODE_FUSED: {
-                // H0 (zero outside the live rows and on the column ring) for the rows
-                // the outputs need, then the column pass with the ring from the input
-                const int lo_all = p.out_hi2 > p.out_lo2 ? (p.out_lo < p.out_lo2 ? p.out_lo : p.out_lo2) : p.out_lo;
-                const int hi_all = p.out_hi2 > p.out_lo2 ? (p.out_hi > p.out_hi2 ? p.out_hi : p.out_hi2) : p.out_hi;
-                const int h_lo = lo_all - rad > j.src_row0 ? lo_all - rad : j.src_row0;
-                const int h_hi = hi_all + rad < j.src_row0 + j.src_rows ? hi_all + rad : j.src_row0 + j.src_rows;
-                const long long hplane = (long long)(h_hi - h_lo) * j.C;
-                e = cudaMallocAsync(reinterpret_cast<void**>(&h0), sizeof(float) * hplane * j.nplanes, s);
-                if (e != cudaSuccess) break;
-                WideParams ph = p;
-                ph.dst = h0;
-                ph.dps = hplane;
-                ph.drs = j.C;
-                ph.dst_row0 = h_lo;
-                ph.out_lo = h_lo;
-                ph.out_hi = h_hi;
-                ph.out_lo2 = ph.out_hi2 = 0;
-                ph.flags = F_ZERO_FILL;
-                wide_hpass_kernel<<<wide_grid(hplane * j.nplanes), 256, 0, s>>>(ph);
-                WideParams pv = p;
-                pv.src = h0;
-                pv.sps = hplane;
-                pv.srs = j.C;
-                pv.src_row0 = h_lo;
-                wide_vpass_kernel<<<wide_grid(outs), 256, 0, s>>>(pv, j.src, j.sps, j.srs, j.src_row0, 1);
-                count_launch(2);
-                break;
+    p.taps_dev = nullptr;
+}
+
+int launch_wide(const RowsJob& j, cudaStream_t s) {
+    if (j.above || j.below) {
+        set_error("kernel widths above 9 are not supported for peer-memory row bands");
+        return SC_UNSUPPORTED_WIDTH;
+    }
+    if (j.width > MAX_W_WIDE) {
+        set_error("kernel width " + std::to_string(j.width) + " > " + std::to_string(MAX_W_WIDE) + " not supported");
+        return SC_UNSUPPORTED_WIDTH;
+    }
+    const int rad = j.width / 2;
+    const long long outs = (long long)j.nplanes * ((j.out_hi - j.out_lo) + (j.out_hi2 - j.out_lo2)) * j.C;
+    if (outs <= 0) return SC_OK;
+    cudaError_t e = cudaSuccess;
+    if (j.mode == MODE_SINGLE) {
+        const int ntaps = j.width * j.width;
+        if (ntaps <= kWideDenseTaps) {
+            static thread_local WideParamsT<kWideDenseTaps> pd;  // 32 KB: not on the stack
+            fill_common(pd, j, rad);
+            std::memcpy(pd.taps, j.dense, sizeof(float) * ntaps);
+            wide_single_kernel<kWideDenseTaps><<<wide_grid(outs), 256, 0, s>>>(pd);
+        } else {
+            // dense matrices wider than 89: a stream-ordered device copy from a
+            // pinned staging buffer (freed after the kernel, in stream order)
+            WideParamsT<1> pd;
+            fill_common(pd, j, rad);
+            float* dev = nullptr;
+            float* pinned = nullptr;
+            e = cudaMallocAsync(reinterpret_cast<void**>(&dev), sizeof(float) * ntaps, s);
+            if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(float) * ntaps);
+            if (e == cudaSuccess) {
+                std::memcpy(pinned, j.dense, sizeof(float) * ntaps);
+                e = cudaMemcpyAsync(dev, pinned, sizeof(float) * ntaps, cudaMemcpyHostToDevice, s);
             }
-            default:
-                set_error("no wide kernel for this mode");
-                cudaFreeAsync(taps, s);
-                return SC_UNSUPPORTED_WIDTH;
+            if (e == cudaSuccess) {
+                pd.taps_dev = dev;
+                wide_single_kernel<1><<<wide_grid(outs), 256, 0, s>>>(pd);
+                e = cudaStreamSynchronize(s);  // the pinned staging buffer is released below
+            }
+            if (dev) cudaFreeAsync(dev, s);
+            if (pinned) cudaFreeHost(pinned);
         }
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            set_error(std::string("wide kernel: ") + cudaGetErrorString(e));
+            return SC_CUDA_ERROR;
+        }
+        count_launch();
+        return SC_OK;
+    }
+    WideParams p;
+    fill_common(p, j, rad);
+    for (int i = 0; i < j.width; ++i) p.taps[i] = j.taps[i];
+    float* h0 = nullptr;
+    switch (j.mode) {
+        case MODE_HPASS:
+            wide_hpass_kernel<<<wide_grid(outs), 256, 0, s>>>(p);
+            count_launch();
+            break;
+        case MODE_VPASS:
+            wide_vpass_kernel<<<wide_grid(outs), 256, 0, s>>>(p, nullptr, 0, 0, 0, 0);
+            count_launch();
+            break;
+        case MODE_FUSED: {
+            // H0 (zero outside the live rows and on the column ring) for the rows
+            // the outputs need, then the column pass with the ring from the input
+            const int lo_all = p.out_hi2 > p.out_lo2 ? (p.out_lo < p.out_lo2 ? p.out_lo : p.out_lo2) : p.out_lo;
+            const int hi_all = p.out_hi2 > p.out_lo2 ? (p.out_hi > p.out_hi2 ? p.out_hi : p.out_hi2) : p.out_hi;
+            const int h_lo = lo_all - rad > j.src_row0 ? lo_all - rad : j.src_row0;
+            const int h_hi = hi_all + rad < j.src_row0 + j.src_rows ? hi_all + rad : j.src_row0 + j.src_rows;
+            const long long hplane = (long long)(h_hi - h_lo) * j.C;
+            e = cudaMallocAsync(reinterpret_cast<void**>(&h0), sizeof(float) * hplane * j.nplanes, s);
+            if (e != cudaSuccess) break;
+            WideParams ph = p;
+            ph.dst = h0;
+            ph.dps = hplane;
+            ph.drs = j.C;
+            ph.dst_row0 = h_lo;
+            ph.out_lo = h_lo;
+            ph.out_hi = h_hi;
+            ph.out_lo2 = ph.out_hi2 = 0;
+            ph.flags = F_ZERO_FILL;
+            wide_hpass_kernel<<<wide_grid(hplane * j.nplanes), 256, 0, s>>>(ph);
+            WideParams pv = p;
+            pv.src = h0;
+            pv.sps = hplane;
+            pv.srs = j.C;
+            pv.src_row0 = h_lo;
+            wide_vpass_kernel<<<wide_grid(outs), 256, 0, s>>>(pv, j.src, j.sps, j.srs, j.src_row0, 1);
+            count_launch(2);
+            break;
+        }
+        default:
+            set_error("no wide kernel for this mode");
+            return SC_UNSUPPORTED_WIDTH;
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     if (h0) cudaFreeAsync(h0, s);
-    cudaFreeAsync(taps, s);
     if (e != cudaSuccess) {
+        cudaGetLastError();
         set_error(std::string("wide kernel: ") + cudaGetErrorString(e));
         return SC_CUDA_ERROR;
     }

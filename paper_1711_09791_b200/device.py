@@ -280,49 +280,77 @@ def synthetic(shape, seed: int, kind: int, device="cuda", offset: int = 0) -> to
     return fill_synthetic(t, seed, kind, offset)
 
 
+def _host_ptrs(planes, shape=None):
+    """Addresses of C-contiguous float32 host planes (numpy arrays or CPU tensors,
+    pinned or pageable) sharing one 2-D shape."""
+    ptrs = []
+    for arr in planes:
+        if isinstance(arr, torch.Tensor):
+            if arr.is_cuda or arr.dtype != torch.float32 or not arr.is_contiguous():
+                raise InvalidArgumentError("host planes must be contiguous CPU float32")
+            shp = tuple(arr.shape)
+            ptrs.append(arr.data_ptr())
+        else:
+            if not isinstance(arr, np.ndarray) or arr.dtype != np.float32 or not arr.flags.c_contiguous:
+                raise InvalidArgumentError("host planes must be C-contiguous float32")
+            if not arr.flags.writeable:
+                raise InvalidArgumentError("host planes must be writeable")
+            shp = arr.shape
+            ptrs.append(arr.ctypes.data)
+        if len(shp) != 2 or (shape is not None and tuple(shp) != tuple(shape)):
+            raise InvalidArgumentError("host planes must be 2-D and share one shape")
+        shape = tuple(shp)
+    return ptrs, shape
+
+
+def _ptr_array(ptrs):
+    return ctypes.cast((ctypes.c_void_p * len(ptrs))(*ptrs), ctypes.c_void_p)
+
+
 def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring: bool = True,
                   device: int = 0, devices=None) -> None:
-    """End-to-end two-pass on HOST planes (numpy arrays or CPU tensors, ideally pinned):
-    streamed H2D -> fused kernel -> D2H inside the library; blocks until done.
+    """End-to-end two-pass on HOST planes (numpy arrays or CPU tensors; pinned planes
+    are copied by DMA directly, pageable ones through the library's pinned staging
+    ring): streamed H2D -> fused kernel -> D2H inside the library; blocks until done.
     dst_planes may be src_planes (in place, as conv_two_pass). devices (a list of
     device indices, one process): row bands streamed through every listed GPU
     concurrently (sc_two_pass_host_multi_f32), same bits."""
     w = _taps(taps)
-    ptrs_in, ptrs_out = [], []
-    shape = None
-    for a, b in zip(src_planes, dst_planes):
-        for arr in (a, b):
-            if isinstance(arr, torch.Tensor):
-                if arr.is_cuda or arr.dtype != torch.float32 or not arr.is_contiguous():
-                    raise InvalidArgumentError("host planes must be contiguous CPU float32")
-                shp = tuple(arr.shape)
-            else:
-                if arr.dtype != np.float32 or not arr.flags.c_contiguous:
-                    raise InvalidArgumentError("host planes must be C-contiguous float32")
-                shp = arr.shape
-            if len(shp) != 2 or (shape is not None and shp != shape):
-                raise InvalidArgumentError("host planes must be 2-D and share one shape")
-            shape = shp
-        ptrs_in.append(a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data)
-        ptrs_out.append(b.data_ptr() if isinstance(b, torch.Tensor) else b.ctypes.data)
-    if not ptrs_in or len(ptrs_in) != len(list(dst_planes)):
+    src_planes, dst_planes = list(src_planes), list(dst_planes)
+    ptrs_in, shape = _host_ptrs(src_planes)
+    ptrs_out, _ = _host_ptrs(dst_planes, shape)
+    if not ptrs_in or len(ptrs_in) != len(ptrs_out):
         raise InvalidArgumentError("need matching, non-empty source and destination plane lists")
     n = len(ptrs_in)
-    arr_in = (ctypes.c_void_p * n)(*ptrs_in)
-    arr_out = (ctypes.c_void_p * n)(*ptrs_out)
+    arr_in, arr_out = _ptr_array(ptrs_in), _ptr_array(ptrs_out)
     flags = (_lib.SC_EXTENDED if extended else 0) | (0 if ring else _lib.SC_NO_RING)
     L = _lib.load()
     if devices is not None and len(list(devices)) > 1:
         devs = [int(d) for d in devices]
         arr_dev = (ctypes.c_int * len(devs))(*devs)
-        _lib.check(L.sc_two_pass_host_multi_f32(ctypes.cast(arr_in, ctypes.c_void_p),
-                                                ctypes.cast(arr_out, ctypes.c_void_p), n, shape[0], shape[1], _fp(w),
+        _lib.check(L.sc_two_pass_host_multi_f32(arr_in, arr_out, n, shape[0], shape[1], _fp(w),
                                                 w.size, flags, ctypes.cast(arr_dev, ctypes.c_void_p), len(devs)))
         return
     if devices is not None and len(list(devices)) == 1:
         device = int(list(devices)[0])
-    _lib.check(L.sc_two_pass_host_f32(ctypes.cast(arr_in, ctypes.c_void_p), ctypes.cast(arr_out, ctypes.c_void_p),
-                                      n, shape[0], shape[1], _fp(w), w.size, flags, int(device)))
+    _lib.check(L.sc_two_pass_host_f32(arr_in, arr_out, n, shape[0], shape[1], _fp(w), w.size, flags, int(device)))
+
+
+def two_pass_host_split(image_planes, scratch_planes, taps, *, extended: bool = False, device: int = 0) -> None:
+    """The reference's end state of convolve_image(TWO_PASS) with a workspace, on HOST
+    planes (S/executors.py:303-326): scratch_planes := H0 (zero outside the row
+    pass's rows and columns), image_planes[valid] := V(H0) in place, image ring
+    untouched. Streamed through the GPU like two_pass_host; blocks until done."""
+    w = _taps(taps)
+    image_planes, scratch_planes = list(image_planes), list(scratch_planes)
+    ptrs_img, shape = _host_ptrs(image_planes)
+    ptrs_scr, _ = _host_ptrs(scratch_planes, shape)
+    if not ptrs_img or len(ptrs_img) != len(ptrs_scr):
+        raise InvalidArgumentError("need matching, non-empty image and workspace plane lists")
+    L = _lib.load()
+    _lib.check(L.sc_two_pass_host_split_f32(_ptr_array(ptrs_img), _ptr_array(ptrs_scr), len(ptrs_img), shape[0],
+                                            shape[1], _fp(w), w.size, _lib.SC_EXTENDED if extended else 0,
+                                            int(device)))
 
 
 def two_pass_host_band(src_rows, dst_rows, taps, *, global_rows: int, row0: int, out_lo: int, out_hi: int,

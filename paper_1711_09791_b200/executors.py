@@ -6,18 +6,27 @@ plane of the image is covered by ONE grid launch per pass (the reference's
 plane agglomeration, S/executors.py:334-356, taken to its limit), and the
 results are bit-identical to every reference plan (T/test_executors.py:188-231).
 
-Two-pass end states, per buffer residency:
-  * device image, or host image with Cuda(fused=False): the split pair K2+K3
-    reproduces the reference exactly -- workspace = H0 scratch, image = V(H0).
-  * host image with Cuda(fused=True) (default): the streamed fused path
-    (H2D -> K1 -> D2H, in place on the host planes). image is bit-identical;
-    the workspace is not used as scratch and keeps its previous contents.
+Two-pass end states are the reference's in every case (S/executors.py:303-326):
+workspace = H0 scratch (zeroed, then the row pass), image = V(H0) with its ring
+untouched.
+  * device image: one pass that writes both buffers (K5, or K2+K3).
+  * host image with a workspace given: the streamed split path (H2D -> K1 + the
+    row pass -> D2H of both buffers, sc_two_pass_host_split_f32).
+  * host image without a workspace (the reference then allocates a zero one the
+    caller never sees): the streamed fused path, image only (H2D -> K1 -> D2H).
+    Cuda(fused=False) takes the split path here too.
+
+The arguments are duck-typed: the reference's own Image / Plane /
+SeparableKernel / ConvVariant objects work as well as this package's mirrors
+(the reference-side plugin, plugin.py, relies on that).
 """
 
 from __future__ import annotations
 
 import time
 from dataclasses import dataclass
+
+import numpy as np
 
 from . import _lib
 from .conv import Algorithm, ConvVariant, OpCounter
@@ -125,7 +134,8 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
 
     from . import device as dev
 
-    if variant.algorithm is Algorithm.SINGLE_PASS_UNROLLED5 and kernel.width != 5:
+    algo = Algorithm(getattr(variant.algorithm, "value", variant.algorithm))
+    if algo is Algorithm.SINGLE_PASS_UNROLLED5 and kernel.width != 5:
         raise UnsupportedWidthError(f"unrolled variant needs width 5, got {kernel.width}")
     if not isinstance(plan, Cuda):
         raise UnsupportedCombinationError(
@@ -140,20 +150,23 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
     r = kernel.radius
     region = valid_region(rows, cols, r)
     nplanes = image.plane_count
-    on_dev = image.on_device
-    if not on_dev and any(p.on_device for p in image.planes):
+    taps = np.ascontiguousarray(kernel.weights, dtype=np.float32)
+    on_dev = _on_device(image)
+    if not on_dev and any(_on_device_plane(p) for p in image.planes):
         raise InvalidArgumentError("image planes must all be host arrays or all CUDA tensors")
+    given_ws = workspace is not None
     if workspace is None:
         workspace = Image.zeros_like(image)
     if workspace.rows != rows or workspace.cols != cols or workspace.plane_count != nplanes:
         raise InvalidArgumentError("workspace must match the image's dimensions")
-    if workspace.on_device != on_dev:
+    if _on_device(workspace) != on_dev:
         raise InvalidArgumentError("workspace must live where the image lives")
 
     stats = LaunchStats()
     before = _lib.launch_count()
     t0 = time.perf_counter_ns()
-    two_pass = variant.algorithm is Algorithm.TWO_PASS
+    two_pass = algo is Algorithm.TWO_PASS
+    copy_back = bool(variant.copy_back) and not two_pass
 
     if on_dev:
         device_index = image.planes[0].data.device
@@ -165,38 +178,53 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
                 ws_groups = [p.data.unsqueeze(0) for p in workspace.planes]
             for ig, wg in zip(img_groups, ws_groups):
                 if two_pass:
-                    dev.two_pass_split(ig, wg, kernel.weights)
+                    dev.two_pass_split(ig, wg, taps)
                 else:
-                    dev.single_pass(ig, outer_product(kernel).matrix, wg, copy_back=variant.copy_back)
+                    dev.single_pass(ig, outer_product(kernel).matrix, wg, copy_back=copy_back)
             torch.cuda.current_stream().synchronize()
     else:
         device_index = plan.device if plan.device is not None else (
             plan.devices[0] if plan.devices else torch.cuda.current_device())
-        if two_pass and plan.fused:
-            planes = [p.data for p in image.planes]
-            dev.two_pass_host(planes, planes, kernel.weights, device=device_index, devices=plan.devices)
+        img_planes = [_host_array(p) for p in image.planes]
+        ws_planes = [_host_array(p) for p in workspace.planes]
+        if two_pass and plan.fused and not given_ws:
+            # the workspace is the reference's internal zero buffer: unobservable
+            dev.two_pass_host(img_planes, img_planes, taps, device=device_index, devices=plan.devices)
+        elif two_pass:
+            dev.two_pass_host_split(img_planes, ws_planes, taps, device=device_index)
         else:
             with torch.cuda.device(device_index):
-                src = torch.stack([torch.from_numpy(p.data) for p in image.planes]).cuda()
-                wsd = torch.stack([torch.from_numpy(p.data) for p in workspace.planes]).cuda()
-                if two_pass:
-                    dev.two_pass_split(src, wsd, kernel.weights)
-                else:
-                    dev.single_pass(src, outer_product(kernel).matrix, wsd, copy_back=variant.copy_back)
+                src = torch.stack([torch.from_numpy(a) for a in img_planes]).cuda()
+                wsd = torch.stack([torch.from_numpy(a) for a in ws_planes]).cuda()
+                dev.single_pass(src, outer_product(kernel).matrix, wsd, copy_back=copy_back)
                 src_h, wsd_h = src.cpu().numpy(), wsd.cpu().numpy()
             rl, rh, cl, ch = region.row_lo, region.row_hi, region.col_lo, region.col_hi
             for p in range(nplanes):
-                if two_pass:
-                    image.planes[p].data[rl:rh, cl:ch] = src_h[p, rl:rh, cl:ch]
-                    workspace.planes[p].data[...] = wsd_h[p]
-                else:
-                    workspace.planes[p].data[rl:rh, cl:ch] = wsd_h[p, rl:rh, cl:ch]
-                    if variant.copy_back:
-                        image.planes[p].data[rl:rh, cl:ch] = src_h[p, rl:rh, cl:ch]
+                ws_planes[p][rl:rh, cl:ch] = wsd_h[p, rl:rh, cl:ch]
+                if copy_back:
+                    img_planes[p][rl:rh, cl:ch] = src_h[p, rl:rh, cl:ch]
 
     stats.wall_time_ns = time.perf_counter_ns() - t0
     stats.parallel_region_launches = _lib.launch_count() - before
     return stats
+
+
+def _on_device_plane(plane) -> bool:
+    d = plane.data
+    return bool(getattr(d, "is_cuda", False))
+
+
+def _on_device(image) -> bool:
+    return all(_on_device_plane(p) for p in image.planes)
+
+
+def _host_array(plane) -> np.ndarray:
+    """The plane's host buffer, written in place (a reference Plane keeps a
+    C-contiguous float32 numpy array, S/image.py:37-39)."""
+    a = plane.data
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags.c_contiguous or a.ndim != 2:
+        raise InvalidArgumentError("host planes must be C-contiguous 2-D float32 numpy arrays")
+    return a
 
 
 def result_image(image: Image, workspace: Image, variant: ConvVariant) -> Image:

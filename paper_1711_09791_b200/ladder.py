@@ -15,8 +15,12 @@ GPU rows sit next to the reference's CPU rows:
 
 Timing uses CUDA events around the reps loop (wall time for GPU-e2e, which
 blocks). The correctness check mirrors check_stage_output (S/bench.py:182-224):
-single-pass variants bitwise against the dense reference (here the GPU dense
-single pass), two-pass within REL_TOL/ABS_TOL on the doubly-interior region.
+single-pass variants bitwise against the naive dense convolution computed on
+the CPU (the reference's conv_single_pass_generic, restated with the same
+numpy float32 fold; independent of the GPU), two-pass within REL_TOL/ABS_TOL on
+the doubly-interior region. The same stages also run inside the reference's
+own harness through the plugin (plugin.py, labels Gpu-*), checked by its own
+check_stage_output.
 """
 
 from __future__ import annotations
@@ -119,16 +123,26 @@ def _run_once(how: str, x, w, dense, copy_back: bool, out, scratch, host):
         raise ConfigError(f"unknown stage kind {how!r}")
 
 
-def _dense_reference(x, kernel: SeparableKernel):
-    """The naive dense convolution of every plane (conv_single_pass_generic on the
-    GPU): the check's reference, S/bench.py:196-198."""
-    import torch
-
-    from . import device as dev
-
-    ref = torch.zeros_like(x)
-    dev.single_pass(x, outer_product(kernel).matrix, ref)
-    return ref
+def _dense_reference(x, kernel: SeparableKernel) -> np.ndarray:
+    """The check's reference: the naive dense convolution of every plane ON THE CPU,
+    restated from the reference's vectorised single pass (single_pass_rows_vec,
+    S/conv.py:86-114: products of the shifted valid-region slices with K[i][j],
+    folded row-major from the first product, each a float32 numpy op), exactly as
+    check_stage_output computes it with conv_single_pass_generic
+    (S/bench.py:196-198). Independent of the GPU; zero outside the valid region."""
+    src = x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x, np.float32)
+    dense = outer_product(kernel).matrix
+    W = dense.shape[0]
+    r = W // 2
+    P, R, C = src.shape
+    out = np.zeros_like(src)
+    acc = None
+    for i in range(W):
+        for j in range(W):
+            term = src[:, i:R - 2 * r + i, j:C - 2 * r + j] * dense[i, j]
+            acc = term if acc is None else acc + term
+    out[:, r:R - r, r:C - r] = acc
+    return out
 
 
 def check_stage_output(x, kernel: SeparableKernel, variant: ConvVariant, how: str) -> str | None:
@@ -139,7 +153,7 @@ def check_stage_output(x, kernel: SeparableKernel, variant: ConvVariant, how: st
     w = kernel.weights
     dense = outer_product(kernel).matrix
     P, R, C = x.shape
-    ref = _dense_reference(x, kernel).cpu().numpy()
+    ref = _dense_reference(x, kernel)
     out = torch.empty_like(x)
     scratch = torch.zeros_like(x)
     host = None

@@ -85,17 +85,27 @@ def test_convolve_image_two_pass(sc, name, where):
         stats = sc.convolve_image(img, k, variant, sc.Cuda(), workspace=ws)
         assert np.array_equal(stack(ws), g["two_pass_faithful_scratch"])
     else:
+        # with a workspace given, both host paths leave the reference's end state
+        # in BOTH buffers: H0 in the workspace (S/executors.py:312-323)
         img = host_image(sc, g["input"])
-        ws = sc.Image.zeros(*g["input"].shape[1:], g["input"].shape[0])
+        ws = sc.Image([sc.Plane(np.full(g["input"].shape[1:], SENTINEL, np.float32))
+                       for _ in range(g["input"].shape[0])])
         stats = sc.convolve_image(img, k, variant, sc.Cuda(fused=(where == "host-fused")), workspace=ws)
-        if where == "host-split":
-            assert np.array_equal(stack(ws), g["two_pass_faithful_scratch"])
-        else:
-            assert not stack(ws).any()  # fused path: workspace not used as scratch
+        assert np.array_equal(stack(ws), g["two_pass_faithful_scratch"])
     out = sc.result_image(img, ws, variant)
     assert out is img
     assert np.array_equal(stack(out), g["two_pass_faithful_image"])
     assert stats.parallel_region_launches >= 1 and stats.wall_time_ns > 0
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_convolve_image_two_pass_host_no_workspace(sc, name):
+    """No workspace: the reference allocates an internal zero one the caller never
+    sees (S/executors.py:303-304), so the streamed fused path runs (image only)."""
+    g = load_golden(name)
+    img = host_image(sc, g["input"])
+    sc.convolve_image(img, sc.SeparableKernel(g["taps"]), sc.ConvVariant(sc.Algorithm.TWO_PASS), sc.Cuda())
+    assert np.array_equal(stack(img), g["two_pass_faithful_image"])
 
 
 @pytest.mark.parametrize("name", CASES)

@@ -1,0 +1,218 @@
+"""Host streaming paths (csrc/stream.cu) and launch safety, on the GPU.
+
+* the split host path (sc_two_pass_host_split_f32): the reference's end state of
+  BOTH buffers of convolve_image(TWO_PASS) with a workspace (S/executors.py:303-326);
+* pageable planes (the reference's numpy Plane, S/image.py:37-39) through the
+  pinned staging ring, pinned planes by direct DMA, and mixtures;
+* in place with radius > the 16-row chunk floor (chunks are >= r rows);
+* dynamic-scheduling tickets under CUDA-graph replay interleaved with eager
+  launches on another stream, and more than 1024 launches queued;
+* wide taps passed by value (graph-capturable), and the wide dense fallback.
+Every result is compared bit for bit with the C oracle.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_09791_b200 import device
+
+    return device
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a, np.float32), np.asarray(b, np.float32)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def taps_of(width, seed=3):
+    rng = np.random.default_rng(seed)
+    w = rng.standard_normal(width).astype(np.float32)
+    return (w / np.float32(w.sum())).astype(np.float32)
+
+
+def planes_of(x, kind):
+    """Host planes of the requested memory kind."""
+    if kind == "pageable":
+        return [p.copy() for p in x]
+    if kind == "pinned":
+        return [torch.from_numpy(p.copy()).pin_memory() for p in x]
+    # mixed: even planes pinned, odd planes pageable
+    return [torch.from_numpy(p.copy()).pin_memory() if i % 2 == 0 else p.copy() for i, p in enumerate(x)]
+
+
+def as_np(planes):
+    return np.stack([p.numpy() if isinstance(p, torch.Tensor) else p for p in planes])
+
+
+@pytest.fixture
+def small_chunks(monkeypatch):
+    monkeypatch.setenv("SC_HOST_CHUNK_MB", "0")  # 16-row (or r-row) chunks: many seams
+
+
+@pytest.mark.parametrize("kind", ["pageable", "pinned", "mixed"])
+@pytest.mark.parametrize("width,extended", [(5, False), (5, True), (3, False), (9, False), (13, False), (35, True)])
+def test_host_split_end_state(dev, oracle, small_chunks, kind, width, extended):
+    w = taps_of(width)
+    R, C = 157, 203
+    x = oracle.synthetic(4 * R * C, 40 + width, kind=2).reshape(4, R, C)
+    img = planes_of(x, kind)
+    scr = planes_of(np.full_like(x, -3.0), kind)  # whatever was there before is overwritten
+    dev.two_pass_host_split(img, scr, w, extended=extended)
+    assert bits_equal(as_np(img), oracle.two_pass(x, w, extended=extended))
+    assert bits_equal(as_np(scr), oracle.two_pass_scratch(x, w, extended=extended))
+
+
+@pytest.mark.parametrize("kind", ["pageable", "pinned"])
+@pytest.mark.parametrize("width", [35, 65])
+def test_host_in_place_radius_above_chunk_floor(dev, oracle, small_chunks, kind, width):
+    """in place with r > 16 rows (the chunk floor) used to race; chunks
+    are now >= r rows, so only the next chunk's input overlaps a chunk's output."""
+    w = taps_of(width, seed=width)
+    R, C = 211, 96
+    x = oracle.synthetic(3 * R * C, 7, kind=1).reshape(3, R, C)
+    planes = planes_of(x, kind)
+    dev.two_pass_host(planes, planes, w)
+    assert bits_equal(as_np(planes), oracle.two_pass(x, w))
+
+
+@pytest.mark.parametrize("kind", ["pageable", "pinned", "mixed"])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_host_fused_memory_kinds(dev, oracle, small_chunks, kind, inplace):
+    w = np.array([-1, -2, 7, -2, -1], dtype=np.float32)
+    R, C = 301, 260
+    x = oracle.synthetic(3 * R * C, 91, kind=2).reshape(3, R, C)
+    src = planes_of(x, kind)
+    dst = src if inplace else planes_of(np.full_like(x, 5.0), kind)
+    dev.two_pass_host(src, dst, w)
+    assert bits_equal(as_np(dst), oracle.two_pass(x, w))
+    if not inplace:
+        assert bits_equal(as_np(src), x)
+
+
+def test_host_pageable_default_chunks_large(dev, oracle):
+    """A 3 x 2048 x 4096 pageable image with the default chunking (several
+    32 MiB-class chunks per plane, staged by the host copy pool)."""
+    w = np.array([1, 4, 6, 4, 1], dtype=np.float32) / np.float32(16)
+    x = oracle.synthetic(3 * 2048 * 4096, 5, kind=1).reshape(3, 2048, 4096)
+    planes = [p.copy() for p in x]
+    scr = [np.empty_like(p) for p in x]
+    dev.two_pass_host_split(planes, scr, w)
+    assert bits_equal(np.stack(planes), oracle.two_pass(x, w))
+    assert bits_equal(np.stack(scr), oracle.two_pass_scratch(x, w))
+
+
+def test_host_split_rejects_aliased_workspace(dev):
+    from paper_1711_09791_b200.errors import InvalidArgumentError
+
+    x = np.zeros((2, 32, 32), np.float32)
+    with pytest.raises(InvalidArgumentError):
+        dev.two_pass_host_split([x[0], x[1]], [x[1], np.zeros((32, 32), np.float32)], np.ones(5, np.float32))
+
+
+def test_tickets_graph_replay_interleaved_with_eager(dev, oracle):
+    """>1024 launches captured in one CUDA graph, replayed on one
+    stream while eager launches of the same kernels run on another stream -- every
+    launch must own its work tickets (per-stream pairs; a pair per captured launch)."""
+    w = np.array([1, 4, 6, 4, 1], dtype=np.float32) / np.float32(16)
+    P, R, C = 3, 64, 256
+    x = torch.from_numpy(oracle.synthetic(P * R * C, 3, kind=1).reshape(P, R, C)).cuda()
+    want = oracle.two_pass(x.cpu().numpy(), w)
+    n_cap = 1100
+    outs = [torch.empty_like(x) for _ in range(8)]
+    s1 = torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        dev.two_pass(x, w, outs[0])  # warm the planner cache outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s1):
+        for i in range(n_cap):
+            dev.two_pass(x, w, outs[i % 4])
+    torch.cuda.synchronize()
+    for o in outs:
+        o.fill_(-1.0)
+    s2 = torch.cuda.Stream()
+    for rep in range(3):
+        with torch.cuda.stream(s1):
+            g.replay()
+        with torch.cuda.stream(s2):
+            for i in range(300):
+                dev.two_pass(x, w, outs[4 + i % 4])
+    torch.cuda.synchronize()
+    for o in outs:
+        assert bits_equal(o.cpu().numpy(), want)
+
+
+def test_many_queued_launches_one_stream(dev, oracle):
+    """More than 1024 launches queued on one stream behind a slow one (the old
+    1024-slot ring reused a slot while its launch could still be in flight)."""
+    w = np.array([-1, -2, 7, -2, -1], dtype=np.float32)
+    big = torch.rand((3, 4096, 4096), device="cuda")
+    big_out = torch.empty_like(big)
+    x = torch.rand((3, 96, 128), device="cuda")
+    want = oracle.two_pass(x.cpu().numpy(), w)
+    outs = [torch.empty_like(x) for _ in range(4)]
+    for _ in range(5):
+        dev.two_pass(big, w, big_out)
+    for i in range(2100):
+        dev.two_pass(x, w, outs[i % 4])
+    torch.cuda.synchronize()
+    for o in outs:
+        assert bits_equal(o.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("width", [11, 13, 31])
+def test_wide_taps_by_value_capture(dev, oracle, width):
+    """Widths above 9 carry their taps in the kernel parameters: no per-launch
+    allocation or host copy, so they capture into a CUDA graph."""
+    w = taps_of(width, seed=width)
+    P, R, C = 2, 70, 90
+    xn = oracle.synthetic(P * R * C, width, kind=1).reshape(P, R, C)
+    x = torch.from_numpy(xn).cuda()
+    out = torch.empty_like(x)
+    hp = torch.full_like(x, -2.0)
+    dense = oracle.outer_product(w)
+    sp = torch.zeros_like(x)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        dev.two_pass(x, w, out)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        dev.two_pass(x, w, out)
+        dev.hpass(x, w, hp)
+        dev.single_pass(x, dense, sp)
+    out.fill_(0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert bits_equal(out.cpu().numpy(), oracle.two_pass(xn, w))
+    assert bits_equal(sp.cpu().numpy(), oracle.single_pass(xn, dense))
+    exp = np.full_like(xn, -2.0)
+    r = width // 2
+    for p in range(P):
+        oracle.horizontal_rows(xn[p], exp[p], w, r, R - r)
+    assert bits_equal(hp.cpu().numpy(), exp)
+
+
+def test_wide_dense_above_param_limit(dev, oracle):
+    """A dense matrix wider than 89 (more than the 32 KB of kernel parameters)
+    goes through a stream-ordered device copy."""
+    w = taps_of(91, seed=91)
+    dense = oracle.outer_product(w)
+    xn = oracle.synthetic(1 * 100 * 120, 9, kind=1).reshape(1, 100, 120)
+    x = torch.from_numpy(xn).cuda()
+    sp = torch.full_like(x, 1.5)
+    dev.single_pass(x, dense, sp)
+    torch.cuda.synchronize()
+    assert bits_equal(sp.cpu().numpy(), oracle.single_pass(xn, dense, np.full_like(xn, 1.5)))

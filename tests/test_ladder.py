@@ -119,3 +119,19 @@ def test_gpu_ladder_cli(tmp_path):
     assert ladder.main(["--sizes", "64x64", "--reps", "2", "--csv", str(p)]) == 0
     lines = p.read_text().splitlines()
     assert lines[0] == ladder.CSV_HEADER and len(lines) == 1 + len(ladder.GPU_STAGES)
+
+
+@pytest.mark.parametrize("name", ["syn_37x23_s8_normal", "syn_24x64_s21_sharpen", "special_20x28_sigma1"])
+def test_check_reference_is_cpu_dense_pinned_to_fixtures(name):
+    """The ladder's check-before-timing reference is computed on the CPU (not by
+    the GPU it checks) and equals the reference's own dense single pass bit for bit
+    (fixtures made by sepconv_lab, tests/golden/make_golden.py)."""
+    import numpy as np
+
+    from conftest import load_golden
+    from paper_1711_09791_b200.kernels import SeparableKernel
+
+    g = load_golden(name)
+    got = ladder._dense_reference(g["input"], SeparableKernel(g["taps"]))
+    assert isinstance(got, np.ndarray)
+    assert np.array_equal(got.view(np.uint32), g["single_zero"].view(np.uint32))
