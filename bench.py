@@ -336,7 +336,7 @@ def main():
 
     from paper_1711_09791_b200 import _lib
     from paper_1711_09791_b200 import device as dev
-    from paper_1711_09791_b200.multi import BandStepper, PeerBandStepper, band_plan, frame_shard
+    from paper_1711_09791_b200.multi import BandStepper, NcclBandStepper, PeerBandStepper, band_plan, frame_shard
 
     world, rank, local = dist_env()
     backend = os.environ.get("SEPCONV_BENCH_BACKEND", "nccl")  # gloo: orchestration check on one GPU
@@ -375,7 +375,10 @@ def main():
 
             if not peer_transport_works():  # one-time probe: both transports, same bits on every rank
                 halo = "nccl"
-        rows_held = (band.lo, band.hi) if halo == "peer" else (band.in_lo, band.in_hi)
+        # owned rows only for the peer transport and the library's NCCL plan; the
+        # torch P2P stepper (gloo orchestration checks) holds the halo rows too
+        own_only = halo == "peer" or (halo == "nccl" and backend == "nccl")
+        rows_held = (band.lo, band.hi) if own_only else (band.in_lo, band.in_hi)
         src = torch.empty((P, rows_held[1] - rows_held[0], C), dtype=torch.float32, device=device)
         for p in range(P):
             # peer: owned rows only (the kernel reads the halo rows from the neighbours);
@@ -384,9 +387,16 @@ def main():
         dst = torch.empty((P, band.hi - band.lo, C), dtype=torch.float32, device=device)
         units_px = (band.hi - band.lo) * C
         stepper = None
+        # device-side readiness signals order every peer step (no host barrier per
+        # step) -- except when ranks share a GPU (one-GPU orchestration checks):
+        # kernels that wait on one another must not share a device
+        peer_signal = torch.cuda.device_count() >= world
         if halo == "peer":
-            stepper = PeerBandStepper(src, dst, band, w)
-            stepper.sync()  # every band written before any kernel reads a neighbour's rows
+            stepper = PeerBandStepper(src, dst, band, w, signal=peer_signal)
+            if not peer_signal:
+                stepper.sync()  # every band written before any kernel reads a neighbour's rows
+        elif halo == "nccl" and backend == "nccl":
+            stepper = NcclBandStepper(src, dst, band, w)  # packed halos, one graph launch per step
         elif halo == "nccl":
             stepper = BandStepper(src, dst, band, w)
 
@@ -474,7 +484,10 @@ def main():
     # exchange per step) from the back-to-back kernel-only launches above.
     one_launch = launches == args.steps
     kms = local_ms if one_launch else kms_b2b
-    kernel_bytes = 2 * 4 * P * units_px  # algorithmic: one read + one write of this rank's samples
+    kernel_px = units_px
+    if band is not None and world > 1 and hasattr(stepper, "kernel_rows"):
+        kernel_px = (stepper.kernel_rows[1] - stepper.kernel_rows[0]) * C  # NCCL plan: the interior launch
+    kernel_bytes = 2 * 4 * P * kernel_px  # algorithmic: one read + one write of the samples one launch produces
     peaks, peak_kind = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = kernel_bytes / (kms / 1e3) / 1e9
@@ -505,6 +518,35 @@ def main():
         roofline["same_size_copy_ms"] = round(copy_ms, 4)
         roofline["frac_of_same_size_copy"] = round(copy_ms / ms, 4)
         del dst_copy
+
+    # ---- N>1 row bands: the same steps with the OTHER halo transport (secondary)
+    halo_alt = None
+    if band is not None and world > 1 and backend == "nccl" and halo in ("peer", "nccl"):
+        other = "nccl" if halo == "peer" else "peer"
+        alt = None
+        try:
+            alt = (NcclBandStepper(src, dst, band, w) if other == "nccl" else
+                   PeerBandStepper(src, dst, band, w, signal=peer_signal))
+            for _ in range(args.warmup):
+                alt.step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream)
+            for _ in range(args.steps):
+                alt.step()
+            b_ev.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([a_ev.elapsed_time(b_ev) / args.steps], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            alt_ms = float(t.item())
+            halo_alt = {"halo": other, "ms_per_step": round(alt_ms, 4),
+                        "value": round(total_px / (alt_ms / 1e3) / 1e9, 3)}
+        except Exception as exc:  # noqa: BLE001 - secondary evidence only
+            halo_alt = {"halo": other, "error": str(exc)[:200]}
+        finally:
+            if alt is not None:
+                alt.close()
 
     # ---- end to end through the C-ABI host entry point (pinned host planes)
     e2e = None
@@ -627,6 +669,7 @@ def main():
                        "taps": [float(v) for v in w], "parallelism": f"rowband{world}" if wl.frames == 1
                        else f"frames{world}", "l2": l2_note,
                        **({"halo": halo} if band is not None and world > 1 else {})},
+            **({"halo_alt": halo_alt} if halo_alt is not None else {}),
             "effective_GBps": round(eff, 1), "pct_of_8TBps": round(100 * eff / NOMINAL_HBM_GBPS, 2),
             "pct_of_measured_copy": round(100 * eff / peak, 2),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,

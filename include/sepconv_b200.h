@@ -33,6 +33,7 @@ extern "C" {
 #define SC_INVALID_DIMENSION 2 /* InvalidDimensionError: plane smaller than the kernel (S/conv.py:76-79) */
 #define SC_UNSUPPORTED_WIDTH 3 /* UnsupportedWidthError: width above 255 (or above 9 on the peer-band and fused-u8 entry points) */
 #define SC_CUDA_ERROR 4        /* ExecutionError: a launch or copy failed (S/errors.py:36-42) */
+#define SC_NCCL_ERROR 5        /* ExecutionError: NCCL unavailable or a communication call failed */
 
 /* Flags */
 #define SC_EXTENDED 0x1  /* row pass over every row: conv_two_pass(extended=True), S/conv.py:417-418 */
@@ -92,6 +93,62 @@ int sc_two_pass_band_peer_f32(const float *src, float *dst, int nplanes, int glo
                               int64_t below_plane_stride, int64_t below_row_stride,
                               int dst_row0, int out_lo, int out_hi, const float *taps, int width, int flags,
                               void *stream);
+
+/* The same band step with device-side readiness signalling between ranks, so a
+ * step on FRESH inputs needs no host barrier. sig_self: this band's three u64
+ * signal words [ready epoch, done epoch, finished-CTA count] in its own device
+ * memory (zero-initialised, exported to the neighbours with sc_ipc_export);
+ * sig_above / sig_below: the neighbours' words mapped with sc_ipc_open (NULL at
+ * the image edges). epoch: this step's number, 1, 2, ... Every CTA publishes
+ * ready = epoch when it starts (the band's inputs are in place, by stream order)
+ * and waits for both neighbours' ready >= epoch before its first read or write;
+ * the last CTA publishes done = epoch. A neighbour that has started step e has
+ * finished step e-1, so ping-pong buffers (step e writes what neighbours read in
+ * step e-1) are safe too. sig_err (host-mapped u32, may be NULL) is set when a
+ * wait outlives SC_PEER_TIMEOUT_MS (default 20000 ms); the kernel then goes on
+ * rather than hang the GPU. Widths up to 9. */
+int sc_two_pass_band_peer_sig_f32(const float *src, float *dst, int nplanes, int global_rows, int cols,
+                                  int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                                  int64_t dst_row_stride, int src_row0, int src_rows, const float *above,
+                                  int above_row0, int above_rows, int64_t above_plane_stride,
+                                  int64_t above_row_stride, const float *below, int below_row0, int below_rows,
+                                  int64_t below_plane_stride, int64_t below_row_stride, int dst_row0, int out_lo,
+                                  int out_hi, const float *taps, int width, int flags, uint64_t *sig_self,
+                                  const uint64_t *sig_above, const uint64_t *sig_below, uint64_t epoch,
+                                  uint32_t *sig_err, void *stream);
+
+/* Stream-ordered wait until the neighbours' signal word `word` (0 ready, 1 done)
+ * is >= value: a rank about to overwrite its band's input rows after step e
+ * enqueues sc_band_signal_wait(above, below, 1, e, err, stream) first. */
+int sc_band_signal_wait(const uint64_t *sig_above, const uint64_t *sig_below, int word, uint64_t value,
+                        uint32_t *sig_err, void *stream);
+
+/* NCCL transport of the row-band step (one process per GPU). The library loads
+ * libnccl.so.2 at run time and keeps its own communicator:
+ *   sc_nccl_unique_id   -> 128-byte ncclUniqueId on one rank (share it, e.g. by
+ *                          torch.distributed broadcast)
+ *   sc_nccl_comm_init   -> ncclCommInitRank on `device`
+ * A band plan holds, for one band of `nplanes` planes (owned rows
+ * [band_lo, band_hi) of a global_rows x cols image; src / dst hold exactly those
+ * rows), ONE packed send and ONE receive buffer of nplanes x r x cols per
+ * neighbour, a communication stream and (use_graph) the whole step captured in a
+ * CUDA graph. A step: pack the r boundary rows of every plane (one 2-D copy per
+ * side) and exchange them (ncclSend/ncclRecv in one group) on the communication
+ * stream while the interior rows [lo+r, hi-r) compute on the caller's stream;
+ * then ONE launch produces both boundary strips, reading the halo rows straight
+ * from the receive buffers. rank_above / rank_below: the neighbours' ranks (-1 at
+ * the image edges; a rank may name itself, which the one-GPU tests use). */
+int sc_nccl_unique_id(void *id_out /* 128 bytes */);
+int sc_nccl_comm_init(const void *id /* 128 bytes */, int nranks, int rank, int device, void **comm_out);
+int sc_nccl_comm_destroy(void *comm);
+int sc_band_plan_create(void *comm, const float *src, float *dst, int nplanes, int global_rows, int cols,
+                        int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                        int64_t dst_row_stride, int band_lo, int band_hi, int rank_above, int rank_below,
+                        const float *taps, int width, int flags, int use_graph, void **plan_out);
+int sc_band_plan_step(void *plan, void *stream);
+/* 1 if the plan's steps replay a captured CUDA graph, 0 if they are issued eagerly */
+int sc_band_plan_graphed(void *plan);
+int sc_band_plan_destroy(void *plan);
 
 /* CUDA IPC for the band buffers: export a device buffer (64-byte handle of its
  * allocation + the buffer's byte offset in it), map another process's buffer for

@@ -27,6 +27,7 @@ SC_INVALID_ARGUMENT = 1
 SC_INVALID_DIMENSION = 2
 SC_UNSUPPORTED_WIDTH = 3
 SC_CUDA_ERROR = 4
+SC_NCCL_ERROR = 5
 
 SC_EXTENDED = 0x1
 SC_NO_RING = 0x2
@@ -42,6 +43,15 @@ EXPORTS = (
     "sc_two_pass_band_f32",
     "sc_two_pass_band2_f32",
     "sc_two_pass_band_peer_f32",
+    "sc_two_pass_band_peer_sig_f32",
+    "sc_band_signal_wait",
+    "sc_nccl_unique_id",
+    "sc_nccl_comm_init",
+    "sc_nccl_comm_destroy",
+    "sc_band_plan_create",
+    "sc_band_plan_step",
+    "sc_band_plan_graphed",
+    "sc_band_plan_destroy",
     "sc_ipc_export",
     "sc_ipc_open",
     "sc_ipc_close",
@@ -85,6 +95,18 @@ _SIGNATURES = {
     "sc_two_pass_band2_f32": (_STRIDED + [_i32] * 7 + [_fp, _i32, _i32, _vp], _i32),
     "sc_two_pass_band_peer_f32": (_STRIDED + [_i32, _i32, _vp, _i32, _i32, _i64, _i64, _vp, _i32, _i32, _i64, _i64,
                                               _i32, _i32, _i32, _fp, _i32, _i32, _vp], _i32),
+    "sc_two_pass_band_peer_sig_f32": (_STRIDED + [_i32, _i32, _vp, _i32, _i32, _i64, _i64, _vp, _i32, _i32, _i64,
+                                                  _i64, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _vp, _vp, _u64, _vp,
+                                                  _vp], _i32),
+    "sc_band_signal_wait": ([_vp, _vp, _i32, _u64, _vp, _vp], _i32),
+    "sc_nccl_unique_id": ([_vp], _i32),
+    "sc_nccl_comm_init": ([_vp, _i32, _i32, _i32, ctypes.POINTER(_vp)], _i32),
+    "sc_nccl_comm_destroy": ([_vp], _i32),
+    "sc_band_plan_create": ([_vp] + _STRIDED + [_i32, _i32, _i32, _i32, _fp, _i32, _i32, _i32, ctypes.POINTER(_vp)],
+                            _i32),
+    "sc_band_plan_step": ([_vp, _vp], _i32),
+    "sc_band_plan_graphed": ([_vp], _i32),
+    "sc_band_plan_destroy": ([_vp], _i32),
     "sc_ipc_export": ([_vp, _vp, ctypes.POINTER(_i64)], _i32),
     "sc_ipc_open": ([_vp, _i64, _i32, ctypes.POINTER(_vp)], _i32),
     "sc_ipc_close": ([_vp, _i64], _i32),
@@ -148,7 +170,7 @@ def check(status: int) -> None:
         raise InvalidDimensionError(msg)
     if status == SC_UNSUPPORTED_WIDTH:
         raise UnsupportedWidthError(msg)
-    raise ExecutionError([(0, RuntimeError(msg))])
+    raise ExecutionError([(0, RuntimeError(msg))])  # SC_CUDA_ERROR, SC_NCCL_ERROR
 
 
 def floats(values) -> ctypes.Array:

@@ -22,7 +22,7 @@ LIB = os.path.join(PKG, "libsepconv_b200.so")
 OBJ = os.path.join(PKG, "csrc", "_obj")
 
 SOURCES = ["capi.cu", "stream.cu", "kern_aux.cu", "kern_fused.cu", "kern_hpass.cu", "kern_vpass.cu", "kern_single.cu", "kern_u8.cu",
-           "kern_wide.cu"]
+           "kern_wide.cu", "nccl_band.cu"]
 HEADERS = ["kernels.cuh", "direct.cuh", "launch.h"]
 
 NVCC_FLAGS = [
@@ -81,7 +81,7 @@ def build(force: bool = False, verbose: bool = False, defines: list[str] | None 
                 raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
     if force or jobs or _stale(lib_path, objs):
         cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib_path,
-               "-Xcompiler", "-fPIC"]
+               "-Xcompiler", "-fPIC", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -42,13 +42,19 @@ static int cuda_fail(cudaError_t e, const char* what) {
     return fail(SC_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+int fail_arg(const std::string& msg) { return fail(SC_INVALID_ARGUMENT, msg); }
+int fail_cuda(cudaError_t e, const std::string& what) {
+    cudaGetLastError();
+    return fail(SC_CUDA_ERROR, what + ": " + cudaGetErrorString(e));
+}
+
 // Tuning knobs (SC_* environment variables, 0 = unset), read in ONE pass over the
 // environment per launch so a knob changed between calls still takes effect
 // while the common case costs no getenv() per knob.
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
     int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
-    int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0;
+    int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0, peer_timeout_ms = 0;
 };
 
 static Knobs read_knobs() {
@@ -77,7 +83,8 @@ static Knobs read_knobs() {
         else if (name == "NO_COLSYM") k.no_colsym = v;
         else if (name == "NO_PDL") k.no_pdl = v;
         else if (name == "SPLIT_PASSES") k.split_passes = v;
-        else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;  // test hook: as if the allocation failed
+        else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;
+        else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;  // test hook: as if the allocation failed
     }
     return k;
 }
@@ -507,8 +514,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
 
     // Kernel family: the TMA stage pipeline (default) or the register-streaming
     // direct kernel (SC_DIRECT=1), both bit-identical.
-    const bool direct = aligned && kn.direct != 0 && !j.above && !j.below && j.mode != MODE_SPLITF &&
-                        j.mode != MODE_SINGLECB;  // direct reads src only
+    const bool direct = aligned && kn.direct != 0 && !j.above && !j.below && !j.sig_self && j.mode != MODE_SPLITF &&
+                        j.mode != MODE_SINGLECB;  // direct reads src only, no signalling
     if (direct) {
         switch (j.mode) {
             case MODE_FUSED: kern = kernel_fused_direct(rad); break;
@@ -554,6 +561,12 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.flags = j.flags;
     p.one = 1.0f;
     if (kn.l2_evict_first) p.flags |= F_L2_EVICT_FIRST;
+    p.sig_self = j.sig_self;
+    p.sig_above = j.sig_above;
+    p.sig_below = j.sig_below;
+    p.epoch = j.sig_self ? j.epoch : 0;
+    p.sig_err = j.sig_err;
+    p.sig_timeout_ns = (long long)(kn.peer_timeout_ms > 0 ? kn.peer_timeout_ms : 20000) * 1000000LL;
     // unaligned kernels stage their output rows only when the DESTINATION rows are
     // not all 16-B aligned (a misaligned source alone keeps direct stores)
     const bool dst_aligned = (j.C % 4 == 0) && aligned16(j.dst) && (j.dps % 4 == 0) && (j.drs % 4 == 0);
@@ -858,13 +871,14 @@ int sc_two_pass_band2_f32(const float* src, float* dst, int nplanes, int global_
     return launch_rows(j, static_cast<cudaStream_t>(stream));
 }
 
-int sc_two_pass_band_peer_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
-                              int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
-                              int64_t dst_row_stride, int src_row0, int src_rows, const float* above,
-                              int above_row0, int above_rows, int64_t above_plane_stride, int64_t above_row_stride,
-                              const float* below, int below_row0, int below_rows, int64_t below_plane_stride,
-                              int64_t below_row_stride, int dst_row0, int out_lo, int out_hi, const float* taps,
-                              int width, int flags, void* stream) {
+static int band_peer(const float* src, float* dst, int nplanes, int global_rows, int cols,
+                     int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                     int64_t dst_row_stride, int src_row0, int src_rows, const float* above,
+                     int above_row0, int above_rows, int64_t above_plane_stride, int64_t above_row_stride,
+                     const float* below, int below_row0, int below_rows, int64_t below_plane_stride,
+                     int64_t below_row_stride, int dst_row0, int out_lo, int out_hi, const float* taps,
+                     int width, int flags, uint64_t* sig_self, const uint64_t* sig_above, const uint64_t* sig_below,
+                     uint64_t epoch, uint32_t* sig_err, void* stream) {
     set_error("");
     SC_TRY(check_width(width));
     SC_TRY(check_dims(nplanes, global_rows, cols, width));
@@ -928,7 +942,61 @@ int sc_two_pass_band_peer_f32(const float* src, float* dst, int nplanes, int glo
     j.below_rows = below_rows;
     j.below_ps = below_plane_stride;
     j.below_rs = below_row_stride;
+    if (sig_self && epoch) {
+        if (width > MAX_W) return fail(SC_UNSUPPORTED_WIDTH, "signalled row bands support widths up to 9");
+        j.sig_self = reinterpret_cast<unsigned long long*>(sig_self);
+        j.sig_above = reinterpret_cast<const unsigned long long*>(sig_above);
+        j.sig_below = reinterpret_cast<const unsigned long long*>(sig_below);
+        j.epoch = epoch;
+        j.sig_err = sig_err;
+    }
     return launch_rows(j, static_cast<cudaStream_t>(stream));
+}
+
+int sc_two_pass_band_peer_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
+                              int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                              int64_t dst_row_stride, int src_row0, int src_rows, const float* above,
+                              int above_row0, int above_rows, int64_t above_plane_stride, int64_t above_row_stride,
+                              const float* below, int below_row0, int below_rows, int64_t below_plane_stride,
+                              int64_t below_row_stride, int dst_row0, int out_lo, int out_hi, const float* taps,
+                              int width, int flags, void* stream) {
+    return band_peer(src, dst, nplanes, global_rows, cols, src_plane_stride, dst_plane_stride, src_row_stride,
+                     dst_row_stride, src_row0, src_rows, above, above_row0, above_rows, above_plane_stride,
+                     above_row_stride, below, below_row0, below_rows, below_plane_stride, below_row_stride, dst_row0,
+                     out_lo, out_hi, taps, width, flags, nullptr, nullptr, nullptr, 0, nullptr, stream);
+}
+
+int sc_two_pass_band_peer_sig_f32(const float* src, float* dst, int nplanes, int global_rows, int cols,
+                                  int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
+                                  int64_t dst_row_stride, int src_row0, int src_rows, const float* above,
+                                  int above_row0, int above_rows, int64_t above_plane_stride,
+                                  int64_t above_row_stride, const float* below, int below_row0, int below_rows,
+                                  int64_t below_plane_stride, int64_t below_row_stride, int dst_row0, int out_lo,
+                                  int out_hi, const float* taps, int width, int flags, uint64_t* sig_self,
+                                  const uint64_t* sig_above, const uint64_t* sig_below, uint64_t epoch,
+                                  uint32_t* sig_err, void* stream) {
+    if (!sig_self || epoch == 0) {
+        set_error("signalled band step needs this band's signal words and an epoch > 0");
+        return SC_INVALID_ARGUMENT;
+    }
+    return band_peer(src, dst, nplanes, global_rows, cols, src_plane_stride, dst_plane_stride, src_row_stride,
+                     dst_row_stride, src_row0, src_rows, above, above_row0, above_rows, above_plane_stride,
+                     above_row_stride, below, below_row0, below_rows, below_plane_stride, below_row_stride, dst_row0,
+                     out_lo, out_hi, taps, width, flags, sig_self, sig_above, sig_below, epoch, sig_err, stream);
+}
+
+int sc_band_signal_wait(const uint64_t* sig_above, const uint64_t* sig_below, int word, uint64_t value,
+                        uint32_t* sig_err, void* stream) {
+    set_error("");
+    if (word < 0 || word > 1) return fail(SC_INVALID_ARGUMENT, "signal word must be 0 (ready) or 1 (done)");
+    if (!sig_above && !sig_below) return SC_OK;
+    const Knobs kn = read_knobs();
+    const long long tmo = (long long)(kn.peer_timeout_ms > 0 ? kn.peer_timeout_ms : 20000) * 1000000LL;
+    cudaError_t e = launch_signal_wait(reinterpret_cast<const unsigned long long*>(sig_above),
+                                       reinterpret_cast<const unsigned long long*>(sig_below), word, value, sig_err,
+                                       tmo, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "signal wait launch");
+    return SC_OK;
 }
 
 // IPC: export a device buffer to another process (its allocation's handle plus the

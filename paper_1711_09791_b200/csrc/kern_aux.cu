@@ -160,4 +160,21 @@ cudaError_t launch_fill_synthetic(float* dst, long long count, uint64_t seed, ui
     return cudaGetLastError();
 }
 
+// Stream-ordered wait for the neighbouring bands' signal words (a caller about to
+// overwrite its band's input rows waits until both neighbours are done reading
+// them, S/executors.py:142-151's launch barrier on the device).
+__global__ void signal_wait_kernel(const unsigned long long* a, const unsigned long long* b, int word,
+                                   unsigned long long value, unsigned int* err, long long timeout_ns) {
+    if (threadIdx.x != 0) return;
+    wait_signal(a ? a + word : nullptr, value, err, timeout_ns);
+    wait_signal(b ? b + word : nullptr, value, err, timeout_ns);
+}
+
+cudaError_t launch_signal_wait(const unsigned long long* a, const unsigned long long* b, int word,
+                               unsigned long long value, unsigned int* err, long long timeout_ns, cudaStream_t s) {
+    signal_wait_kernel<<<1, 32, 0, s>>>(a, b, word, value, err, timeout_ns);
+    count_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace sc

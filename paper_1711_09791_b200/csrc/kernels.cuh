@@ -127,6 +127,22 @@ struct Params {
     // last: inserting fields before w/k shifts the taps' constant-bank offsets,
     // which measurably changes register allocation (fused 76 -> 84, unaligned 96 -> 102)
     int snap_lo, snap_hi;
+    // Row-band readiness signalling between ranks (peer transport, epoch > 0):
+    // sig_self = this band's [ready epoch, done epoch, finished-CTA count] in its own
+    // device memory (mapped by the neighbours); sig_above / sig_below = the
+    // neighbours' words (peer-mapped, may be null). Every CTA publishes
+    // ready = epoch when it starts (its inputs are in place: stream order), waits
+    // until both neighbours published ready >= epoch before its first read or
+    // write (their halo rows are current; and a neighbour that started this step
+    // has finished the previous one, so buffers it read then may be overwritten),
+    // and the last CTA to finish publishes done = epoch. sig_err (host-mapped) is
+    // set if a wait outlives sig_timeout_ns.
+    unsigned long long* sig_self;
+    const unsigned long long* sig_above;
+    const unsigned long long* sig_below;
+    unsigned long long epoch;
+    unsigned int* sig_err;
+    long long sig_timeout_ns;
 };
 
 // SC_TRACE (a dev-only build variant): per-CTA timeline of TRACE_SLOTS words.
@@ -239,6 +255,38 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     return pol;
+}
+
+// System-scope release / acquire on 64-bit signal words (peer memory over NVLink).
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Spin until *flag >= value (acquire, system scope); on timeout flag the error word
+// and go on (a hung neighbour must not hang this GPU).
+static __device__ __noinline__ void wait_signal(const unsigned long long* flag, unsigned long long value,
+                                         unsigned int* err, long long timeout_ns) {
+    if (!flag) return;
+    const unsigned long long t0 = global_ns();
+    unsigned ns = 32;
+    while (ld_acquire_sys(flag) < value) {
+        if ((long long)(global_ns() - t0) > timeout_ns) {
+            if (err) atomicExch_system(err, 1u);
+            return;
+        }
+        __nanosleep(ns);
+        if (ns < 1024) ns *= 2;
+    }
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -420,6 +468,14 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
 #ifdef SC_TRACE
     int ntr = 0;
 #endif
+    if (p.epoch) {
+        // neighbours' rows current (and their previous step finished) before this
+        // CTA reads or writes anything; then order the async-proxy (TMA) reads
+        // after the acquire
+        wait_signal(p.sig_above, p.epoch, p.sig_err, p.sig_timeout_ns);
+        wait_signal(p.sig_below, p.epoch, p.sig_err, p.sig_timeout_ns);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     // The first item of every CTA is its own index (no atomic: 600-900 CTAs
     // claiming from one counter at launch serialise on it); later items come
     // from the ticket, offset by the grid size.
@@ -1190,6 +1246,7 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     // launched with programmatic stream serialization: the setup above overlapped
     // the previous kernel's tail; no global memory is touched before it completed
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.epoch && threadIdx.x == 0) st_release_sys(p.sig_self, p.epoch);  // this band's inputs are in place
 
     if (warp == 0) {
 #ifdef SC_TRACE
@@ -1232,6 +1289,21 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
 #endif
     }
     if (!ALIGNED && threadIdx.x == 32) bulk_wait_all();  // staged rows fully stored before smem goes away
+    if (p.epoch) {
+        // done: every consumer of this CTA has stored its rows; the last CTA out
+        // publishes the epoch (the neighbours' reads of this band ended with their
+        // own kernels, which waited for this step's ready)
+        consumer_bar(ncw * 32);
+        if (threadIdx.x == 32) {
+            __threadfence_system();
+            unsigned long long* cnt = p.sig_self + 2;
+            if (atomicAdd(cnt, 1ULL) == (unsigned long long)gridDim.x - 1) {
+                *cnt = 0;
+                __threadfence_system();
+                st_release_sys(p.sig_self + 1, p.epoch);
+            }
+        }
+    }
 #ifdef SC_TRACE
     if (threadIdx.x == 32) {
         SC_TR(p, 40, clock64());

@@ -68,7 +68,18 @@ struct RowsJob {
     // MODE_SPLITF: scratch planes (H0); MODE_SINGLECB: the image (copy-back); same rows
     float* scr = nullptr;
     long long scr_ps = 0, scr_rs = 0;
+    // row-band readiness signalling between ranks (Params::sig_*; epoch 0 = off)
+    unsigned long long* sig_self = nullptr;
+    const unsigned long long* sig_above = nullptr;
+    const unsigned long long* sig_below = nullptr;
+    unsigned long long epoch = 0;
+    unsigned int* sig_err = nullptr;
 };
+
+// one-thread kernel: wait until the neighbours' signal word `word` (0 ready,
+// 1 done) reaches `value` (kern_aux.cu)
+cudaError_t launch_signal_wait(const unsigned long long* a, const unsigned long long* b, int word,
+                               unsigned long long value, unsigned int* err, long long timeout_ns, cudaStream_t s);
 
 // Plans and launches one row-streaming kernel; returns an SC_* status and sets
 // the thread's last error on failure.
@@ -77,6 +88,8 @@ int launch_rows(const RowsJob& job, cudaStream_t s);
 int launch_wide(const RowsJob& job, cudaStream_t s);
 
 void set_error(const std::string& msg);
+int fail_arg(const std::string& msg);                   // SC_INVALID_ARGUMENT with a message
+int fail_cuda(cudaError_t e, const std::string& what);  // SC_CUDA_ERROR with the CUDA error string
 void count_launch(uint64_t n = 1);
 
 }  // namespace sc

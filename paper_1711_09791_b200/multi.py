@@ -302,6 +302,112 @@ class BandStepper:
         self._check(self._lib.sc_two_pass_band2_f32(*args))
 
 
+_COMMS: dict = {}
+
+
+def nccl_comm(group=None, device: int | None = None) -> int:
+    """The library's own NCCL communicator over the ranks of `group` (cached): rank 0
+    draws the unique id (sc_nccl_unique_id), torch.distributed broadcasts it, every
+    rank calls sc_nccl_comm_init on its device. A world of one needs no process
+    group (the one-GPU tests)."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import _lib
+
+    L = _lib.load()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    dev_index = torch.cuda.current_device() if device is None else int(device)
+    key = (id(group), world, rank, dev_index)
+    if key in _COMMS:
+        return _COMMS[key]
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        _lib.check(L.sc_nccl_unique_id(uid))
+    if world > 1:
+        box = [uid.raw if rank == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = ctypes.create_string_buffer(box[0], 128)
+    comm = ctypes.c_void_p(0)
+    _lib.check(L.sc_nccl_comm_init(uid, world, rank, dev_index, ctypes.byref(comm)))
+    _COMMS[key] = int(comm.value)
+    return _COMMS[key]
+
+
+class NcclBandStepper:
+    """The row-band step with the halo exchange in the library (csrc/nccl_band.cu).
+
+    Each rank holds its OWNED rows only, (P, hi - lo, C). Per step: the r boundary
+    rows of every plane are packed into ONE buffer per neighbour and exchanged by
+    ncclSend/ncclRecv in one group on a communication stream while the interior
+    rows compute; then ONE launch produces both boundary strips, reading the halo
+    rows from the receive buffers. The step is captured once into a CUDA graph, so
+    the host issues one cudaGraphLaunch per step."""
+
+    def __init__(self, local_src, local_dst, band: Band, taps, *, extended: bool = False, group=None,
+                 use_graph: bool = True, comm: int | None = None, rank_above: int | None = None,
+                 rank_below: int | None = None):
+        import ctypes
+
+        from . import _lib
+        from . import device as dev
+
+        self.band = band
+        self.src, self.dst = local_src, local_dst
+        n, Rs, C, sps, srs = dev._planes(local_src, "local_src")
+        n2, Rd, C2, dps, drs = dev._planes(local_dst, "local_dst")
+        if Rs != band.hi - band.lo or Rd != band.hi - band.lo or n2 != n or C2 != C:
+            raise InvalidArgumentError("NCCL band buffers must hold exactly the owned rows")
+        if rank_above is None:
+            rank_above = band.rank - 1 if band.rank > 0 else -1
+        if rank_below is None:
+            rank_below = band.rank + 1 if band.rank < band.world - 1 else -1
+        self._lib = _lib.load()
+        self._check = _lib.check
+        w = dev._taps(taps)
+        self._w = w
+        with torch.cuda.device(local_src.device):
+            if comm is None and (rank_above >= 0 or rank_below >= 0):
+                comm = nccl_comm(group, local_src.device.index)
+            plan = ctypes.c_void_p(0)
+            _lib.check(self._lib.sc_band_plan_create(comm or None, local_src.data_ptr(), local_dst.data_ptr(), n,
+                                                     band.rows, C, sps, dps, srs, drs, band.lo, band.hi, rank_above,
+                                                     rank_below, w.ctypes.data, w.size,
+                                                     _lib.SC_EXTENDED if extended else 0, int(bool(use_graph)),
+                                                     ctypes.byref(plan)))
+        self._plan = plan.value
+        self.graphed = bool(self._lib.sc_band_plan_graphed(self._plan))
+        self._stream = torch.cuda.current_stream(local_src.device).cuda_stream
+        r = band.radius
+        i_lo = band.lo + (r if rank_above >= 0 else 0)
+        i_hi = band.hi - (r if rank_below >= 0 else 0)
+        # the dominant kernel alone (roofline): the interior rows, which need no halo
+        self.kernel_rows = (i_lo, i_hi) if i_hi > i_lo else (band.lo, band.lo)
+        self._kernel_args = (local_src.data_ptr(), local_dst.data_ptr(), n, band.rows, C, sps, dps, srs, drs,
+                             band.lo, Rs, band.lo, i_lo, max(i_lo, i_hi), 0, 0, w.ctypes.data, w.size,
+                             _lib.SC_EXTENDED if extended else 0, self._stream)
+
+    def step(self):
+        self._check(self._lib.sc_band_plan_step(self._plan, self._stream))
+
+    def kernel_only(self):
+        self._check(self._lib.sc_two_pass_band2_f32(*self._kernel_args))
+
+    def close(self):
+        if self._plan:
+            torch.cuda.current_stream(self.src.device).synchronize()
+            self._check(self._lib.sc_band_plan_destroy(self._plan))
+            self._plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
 @dataclass(frozen=True)
 class PeerMeta:
     """What a rank publishes about its band buffer: owned rows [lo, hi) of every
@@ -316,6 +422,8 @@ class PeerMeta:
     row_stride: int
     cols: int
     planes: int
+    sig_handle: bytes = b""  # IPC handle + offset of the band's signal words (empty: no signalling)
+    sig_offset: int = 0
 
 
 def peer_neighbours(metas, band: Band) -> tuple[PeerMeta | None, PeerMeta | None]:
@@ -354,21 +462,27 @@ class PeerBandStepper:
     """Banded two-pass with the halo exchange folded into the kernel.
 
     Each rank keeps only its OWNED input rows (P, hi - lo, C). At construction
-    the ranks publish CUDA IPC handles of their band buffers (one
-    all_gather_object over the process group) and map their two neighbours'
-    buffers into their own device's address space (peer access over
-    NVLink/NVSwitch). A step is then ONE launch: the producer warp's TMA row
-    copies read the r halo rows directly from the neighbours' memory, tile by
-    tile, as the interior streams -- no send/recv, no staging buffer, no second
-    launch for the boundary rows.
+    the ranks publish CUDA IPC handles of their band buffers and of three u64
+    signal words (one all_gather_object over the process group) and map their two
+    neighbours' buffers and words into their own device's address space (peer
+    access over NVLink/NVSwitch). A step is then ONE launch: the producer warp's
+    TMA row copies read the r halo rows directly from the neighbours' memory,
+    tile by tile, as the interior streams -- no send/recv, no staging buffer, no
+    second launch for the boundary rows.
 
-    Ordering contract: a neighbour's owned rows must be written before a step
-    reads them, and not overwritten while it runs. Inputs that stay fixed across
-    steps (the benchmark) need nothing per step; `sync()` is a process-group
-    barrier for callers that refill their bands between steps.
+    Ordering is device-side (signal=True, the default with neighbours): step e
+    is epoch e; every CTA publishes ready = e when it starts and waits for both
+    neighbours' ready >= e before it reads or writes, and the last CTA publishes
+    done = e (csrc/kernels.cuh wait_signal). So a step on FRESH inputs needs no
+    host barrier: a caller that refills its band in place between steps first
+    calls `wait_consumed()` (a stream-ordered wait for the neighbours' done), and
+    ping-pong buffers (step e writes what the neighbours read in step e-1) need
+    nothing at all. `check()` raises if a wait timed out (SC_PEER_TIMEOUT_MS).
+    signal=False keeps the old contract: `sync()` is a process-group barrier.
     """
 
-    def __init__(self, local_src, local_dst, band: Band, taps, *, extended: bool = False, group=None):
+    def __init__(self, local_src, local_dst, band: Band, taps, *, extended: bool = False, group=None,
+                 signal: bool = True):
         from . import _lib
         from . import device as dev
 
@@ -378,33 +492,48 @@ class PeerBandStepper:
         n2, Rd, C2, dps, drs = dev._planes(local_dst, "local_dst")
         if Rs != band.hi - band.lo or Rd != band.hi - band.lo or n2 != n or C2 != C:
             raise InvalidArgumentError("peer band buffers must hold exactly the owned rows")
+        self.signal = bool(signal) and band.world > 1
+        # signal words: [ready, done, finished-CTA count] in this device's memory;
+        # the error word in pinned host memory (read by the host without a sync)
+        self.sig = torch.zeros(3, dtype=torch.int64, device=local_src.device)
+        self.err = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.epoch = 0
         if band.world > 1:
             handle, offset = dev.ipc_export(local_src)
+            sh, so = dev.ipc_export(self.sig) if self.signal else (b"", 0)
         else:
-            handle, offset = b"\0" * 64, 0
-        me = PeerMeta(band.rank, band.lo, band.hi, handle, offset, sps, srs, C, n)
+            handle, offset, sh, so = b"\0" * 64, 0, b"", 0
+        me = PeerMeta(band.rank, band.lo, band.hi, handle, offset, sps, srs, C, n, sh, so)
         above, below = peer_neighbours(publish_peer_meta(me, band, group), band)
         self._opened = []
-        rows = {}
+        rows, sigs = {}, {}
         for side, m in (("above", above), ("below", below)):
+            rows[side] = sigs[side] = None
             if m is None:
-                rows[side] = None
                 continue
             ptr = dev.ipc_open(m.handle, m.offset, local_src.device.index)
             self._opened.append((ptr, m.offset))
             rows[side] = dev.PeerRows(ptr, m.lo, m.hi - m.lo, m.plane_stride, m.row_stride)
+            if self.signal:
+                if not m.sig_handle:
+                    raise InvalidArgumentError("a neighbour published no signal words")
+                sp = dev.ipc_open(m.sig_handle, m.sig_offset, local_src.device.index)
+                self._opened.append((sp, m.sig_offset))
+                sigs[side] = sp
         self.above, self.below = rows["above"], rows["below"]
+        self._sig_above, self._sig_below = sigs["above"], sigs["below"]
         self._lib = _lib.load()
         self._check = _lib.check
         w = dev._taps(taps)
         self._w = w
         a = self.above or dev.PeerRows(0, 0, 0, 0, 0)
         b = self.below or dev.PeerRows(0, 0, 0, 0, 0)
-        stream = torch.cuda.current_stream(local_src.device).cuda_stream
+        self._stream = torch.cuda.current_stream(local_src.device).cuda_stream
         self._args = (local_src.data_ptr(), local_dst.data_ptr(), n, band.rows, C, sps, dps, srs, drs, band.lo, Rs,
                       a.ptr or None, a.row0, a.rows, a.plane_stride, a.row_stride,
                       b.ptr or None, b.row0, b.rows, b.plane_stride, b.row_stride,
-                      band.lo, band.lo, band.hi, w.ctypes.data, w.size, _lib.SC_EXTENDED if extended else 0, stream)
+                      band.lo, band.lo, band.hi, w.ctypes.data, w.size, _lib.SC_EXTENDED if extended else 0)
+        self._sig_args = (self.sig.data_ptr(), self._sig_above, self._sig_below)
 
     def sync(self):
         """Process-group barrier (all ranks' prior band writes complete)."""
@@ -415,14 +544,40 @@ class PeerBandStepper:
             dist.barrier(group=self.group)
 
     def step(self):
-        self._check(self._lib.sc_two_pass_band_peer_f32(*self._args))
+        if self.signal:
+            self.epoch += 1
+            self._check(self._lib.sc_two_pass_band_peer_sig_f32(*self._args, *self._sig_args, self.epoch,
+                                                                self.err.data_ptr(), self._stream))
+        else:
+            self._check(self._lib.sc_two_pass_band_peer_f32(*self._args, self._stream))
 
     kernel_only = step  # the step IS the dominant kernel
 
+    def wait_consumed(self):
+        """Stream-ordered: the neighbours have finished the current epoch (they no
+        longer read this band's rows), so the caller may overwrite them."""
+        if self.signal and self.epoch:
+            self._check(self._lib.sc_band_signal_wait(self._sig_above, self._sig_below, 1, self.epoch,
+                                                      self.err.data_ptr(), self._stream))
+
+    def check(self):
+        """Raise if a neighbour wait timed out (the step's output is then invalid)."""
+        from .errors import ExecutionError
+
+        if int(self.err.item()) != 0:
+            raise ExecutionError([(self.band.rank, RuntimeError("row-band neighbour signal wait timed out"))])
+
     def close(self):
+        """Unmap the neighbours' buffers after EVERY rank has finished reading
+        (a barrier first: exporters outlive importers)."""
         from . import device as dev
 
         torch.cuda.current_stream(self.src.device).synchronize()
+        if self.band.world > 1:
+            import torch.distributed as dist
+
+            if dist.is_initialized():
+                dist.barrier(group=self.group)
         for ptr, off in self._opened:
             dev.ipc_close(ptr, off)
         self._opened = []

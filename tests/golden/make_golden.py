@@ -141,9 +141,64 @@ def wide_cases():
     return out
 
 
+def subnormal_cases():
+    """Products and sums in the float32 subnormal range (|x| < 2^-126 ~ 1.18e-38):
+    numpy on x86 keeps subnormals (no FTZ/DAZ), so the reference's bits depend on
+    gradual underflow in every multiply and add. Cases: tiny taps x tiny inputs,
+    inputs just above and below FLT_MIN with ordinary taps, exact subnormal
+    inputs, signed zeros and mixed signs; shapes with C % 4 == 0 (TMA path) and
+    odd C (generic path)."""
+    out = []
+    rng = np.random.default_rng(1126)
+    tiny = np.float32(np.finfo(np.float32).tiny)  # 2^-126
+    for R, C in ((24, 40), (23, 37)):
+        # 1. tiny taps (~1e-20) x tiny inputs (~1e-20): products ~1e-40, subnormal
+        a = (rng.uniform(-1, 1, size=(2, R, C)) * 1e-20).astype(np.float32)
+        a[0, 3, :] = 0.0
+        a[1, :, 5] = -0.0
+        out.append(plane_case(f"subnormal_{R}x{C}_tinytaps", a,
+                              np.array([1e-20, 3e-20, 5e-20, 3e-20, 1e-20], dtype=np.float32)))
+        out.append(plane_case(f"subnormal_{R}x{C}_tinyasym", a,
+                              np.array([2e-20, -7e-21, 4e-20, 1.5e-20, -3e-20], dtype=np.float32)))
+        # 2. inputs near FLT_MIN (some normal, some subnormal), ordinary taps
+        b = (rng.uniform(-4, 4, size=(2, R, C)) * tiny).astype(np.float32)
+        b[0, ::3, ::2] = (rng.uniform(-1, 1, size=b[0, ::3, ::2].shape) * 1e-40).astype(np.float32)
+        b[1, 7, :] = np.float32(1e-45)  # the smallest subnormal
+        for tname in ("gauss5", "sharpen", "normal"):
+            out.append(plane_case(f"subnormal_{R}x{C}_fltmin_{tname}", b, CONFIG_TAPS[tname]))
+        # 3. ordinary inputs x subnormal taps (width 3)
+        c = rng.uniform(0, 256, size=(1, R, C)).astype(np.float32)
+        out.append(plane_case(f"subnormal_{R}x{C}_subtaps_w3", c,
+                              np.array([3e-41, 1e-40, 3e-41], dtype=np.float32)))
+    return out
+
+
+def subnormal_ppm():
+    """u8 payload with subnormal and tiny taps: read_ppm -> two-pass -> write_ppm."""
+    res = {}
+    rng = np.random.default_rng(77)
+    for (R, C), taps in (((32, 48), [1e-40, 2e-40, 5e-40, 2e-40, 1e-40]),
+                         ((40, 64), [1e-39, -3e-39, 9e-39, -3e-39, 1e-39])):
+        pix = rng.integers(0, 256, size=(R, C, 3), dtype=np.uint8)
+        data = f"P6\n{C} {R}\n255\n".encode() + pix.tobytes()
+        img = ref.read_ppm_bytes(data)
+        k = ref.SeparableKernel(taps)
+        ref.convolve_image(img, k, ref.ConvVariant(ref.Algorithm.TWO_PASS), ref.Sequential())
+        key = f"{R}x{C}"
+        res[f"in_{key}"] = np.frombuffer(data, dtype=np.uint8)
+        res[f"out_{key}"] = np.frombuffer(ref.write_ppm_bytes(img), dtype=np.uint8)
+        res[f"taps_{key}"] = k.weights
+        res[f"planes_out_{key}"] = np.stack([p.data for p in img.planes])
+    np.savez(os.path.join(OUT, "subnormal_ppm.npz"), **res)
+
+
 def main():
     if "--only-wide" in sys.argv:  # add the wide fixtures without rewriting the others
         print(wide_cases())
+        return
+    if "--only-subnormal" in sys.argv:  # add the subnormal fixtures without rewriting the others
+        print(subnormal_cases())
+        subnormal_ppm()
         return
     written = []
     # 1. reference-test shapes on make_synthetic inputs (values in [0, 256))
@@ -172,6 +227,8 @@ def main():
     written.append(plane_case("syn_12x16_s4_delta5", data, ref.delta(5).weights))
     written.append(plane_case("syn_12x16_s4_w3", data, np.array([0.1, 0.7, 0.3], dtype=np.float32)))
     written.extend(wide_cases())
+    written.extend(subnormal_cases())
+    subnormal_ppm()
     # 3. special values: negative, zero rows, large magnitudes (FMA-sensitive)
     rng = np.random.default_rng(1234)
     spec = rng.uniform(-1e4, 1e4, size=(2, 20, 28)).astype(np.float32)

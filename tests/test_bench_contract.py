@@ -13,8 +13,9 @@ from conftest import ROOT
 
 
 def test_reference_arm_json_line():
+    # cfg1 keeps the CPU suite short; the driver runs the default (cfg5, the full image)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "1", "--ref-rows", "8"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+                        "--warmup", "1", "--config", "cfg1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1
@@ -23,9 +24,11 @@ def test_reference_arm_json_line():
               "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e", "impl"):
         assert k in d, k
     assert d["impl"] == "reference" and d["warmup"] >= 3 and d["value"] > 0
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # the real reference package (baseline/_ref) on the full configured image
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert "sepconv_lab" in d["cpu_baseline"]["sample"] and d["cpu_baseline"]["cpu_model"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
-    assert d["config"]["workload"].startswith("cfg5")
+    assert d["config"]["workload"].startswith("cfg1") and d["config"]["rows"] == 1152
 
 
 def test_host_chunk_accounting():

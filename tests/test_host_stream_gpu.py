@@ -216,3 +216,36 @@ def test_wide_dense_above_param_limit(dev, oracle):
     dev.single_pass(x, dense, sp)
     torch.cuda.synchronize()
     assert bits_equal(sp.cpu().numpy(), oracle.single_pass(xn, dense, np.full_like(xn, 1.5)))
+
+
+@pytest.mark.parametrize("shape", [(3, 300, 512), (2, 257, 389)])
+def test_subnormal_random_all_paths(dev, oracle, shape):
+    """Random inputs straddling FLT_MIN (normal and subnormal, both signs) with
+    ordinary and tiny taps: fused, split (one pass / two launches), single pass
+    with and without copy-back, host streaming -- bit-exact vs the oracle (gcc
+    without FTZ/DAZ, like numpy on x86)."""
+    rng = np.random.default_rng(sum(shape))
+    tiny = np.float32(np.finfo(np.float32).tiny)
+    x = (rng.uniform(-3, 3, size=shape) * tiny).astype(np.float32)
+    x[..., ::5] = (rng.uniform(-1, 1, size=x[..., ::5].shape) * 1e-42).astype(np.float32)
+    for w in (np.array([1, 4, 6, 4, 1], np.float32) / np.float32(16),
+              np.array([0.3, -0.2, 0.9, 0.1, -0.1], np.float32),
+              np.array([1e-3, 2e-3, 1e-3], np.float32)):
+        want = oracle.two_pass(x, w)
+        assert bits_equal(dev.two_pass(torch.from_numpy(x).cuda(), w).cpu().numpy(), want)
+        img, scr = torch.from_numpy(x.copy()).cuda(), torch.zeros(shape, device="cuda")
+        dev.two_pass_split(img, scr, w)
+        assert bits_equal(img.cpu().numpy(), want)
+        assert bits_equal(scr.cpu().numpy(), oracle.two_pass_scratch(x, w))
+        dense = oracle.outer_product(w)
+        img, ws = torch.from_numpy(x.copy()).cuda(), torch.zeros(shape, device="cuda")
+        dev.single_pass(img, dense, ws, copy_back=True)
+        ds = oracle.single_pass(x, dense)
+        assert bits_equal(ws.cpu().numpy(), ds)
+        r = len(w) // 2
+        exp = x.copy()
+        exp[:, r:-r, r:-r] = ds[:, r:-r, r:-r]
+        assert bits_equal(img.cpu().numpy(), exp)
+        planes = [p.copy() for p in x]
+        dev.two_pass_host(planes, planes, w)
+        assert bits_equal(np.stack(planes), want)

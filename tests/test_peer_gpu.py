@@ -99,7 +99,9 @@ def _ipc_worker(rank, world, port, R, C, q):
         src = x[:, band.lo:band.hi].clone()
         dst = torch.full_like(src, float("nan"))
         del x
-        stepper = PeerBandStepper(src, dst, band, w)
+        # ranks share the one GPU here: no device-side waits between their kernels
+        # (B200_PROFILING.md: kernels that wait on one another must not share a GPU)
+        stepper = PeerBandStepper(src, dst, band, w, signal=False)
         stepper.sync()          # every band written before any kernel reads a neighbour
         for _ in range(3):
             stepper.step()      # inputs fixed across steps: no per-step synchronisation needed

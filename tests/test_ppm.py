@@ -114,3 +114,23 @@ def test_fused_u8_large_payload_lean_loops():
         fused_ext = dev.two_pass_u8hwc(src, w, extended=True)
         ref_ext = dev.planes_to_hwc(dev.two_pass(dev.hwc_to_planes(src), w, extended=True))
         assert torch.equal(fused_ext, ref_ext)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["32x48", "40x64"])
+def test_fused_u8_subnormal_taps(key):
+    """Subnormal / near-FLT_MIN taps through the fused u8 kernel (cols % 16 == 0) and
+    the float planes path: bytes and float planes the reference produced
+    (tests/golden/make_golden.py subnormal_ppm)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_09791_b200 import device as dev
+    from paper_1711_09791_b200.ppm import convolve_ppm_bytes, read_ppm_bytes
+
+    z = load_golden("subnormal_ppm")
+    data = z[f"in_{key}"].tobytes()
+    assert convolve_ppm_bytes(data, z[f"taps_{key}"]) == z[f"out_{key}"].tobytes()
+    planes = np.stack([p.data for p in read_ppm_bytes(data).planes])
+    got = dev.two_pass(torch.from_numpy(planes).cuda(), z[f"taps_{key}"]).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), z[f"planes_out_{key}"].view(np.uint32))
