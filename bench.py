@@ -641,17 +641,37 @@ def main():
             kern, var = pkg.SeparableKernel(w), pkg.ConvVariant(pkg.Algorithm.TWO_PASS)
             call = "paper_1711_09791_b200.convolve_image(image, kernel, TWO_PASS, Cuda())"
         conv = sl.convolve_image if sl is not None else pkg.convolve_image
-        conv(img, kern, var, Cuda(device=local))
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            conv(img, kern, var, Cuda(device=local))
-        pg_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
         h2d, d2h = host_chunk_bytes(R, C, P, r, 0, R, 0, R)
-        e2e_pageable = {"value": round(total_px / (pg_ms / 1e3) / 1e9, 4), "unit": "Gpix/s",
-                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(pg_ms, 3),
-                        "path": call + " on pageable numpy planes (library pinned staging ring + host copy threads)"}
+
+        def timed(plan, n):
+            t0 = time.perf_counter()
+            for _ in range(n):
+                conv(img, kern, var, plan)
+            return (time.perf_counter() - t0) * 1e3 / n
+
+        # (a) the default plan: the image's buffer is page-locked on the first call
+        # (timed on its own) and stays registered while it lives, so later calls DMA
+        # straight from it
+        first_ms = timed(Cuda(device=local), 1)
+        reg_ms = timed(Cuda(device=local), args.e2e_steps)
+        # (b) never registered: every call stages through the pinned ring
+        from paper_1711_09791_b200.device import host_registry
+
+        host_registry.clear()
+        staged = Cuda(device=local, register_host=False)
+        timed(staged, 1)
+        st_ms = timed(staged, args.e2e_steps)
+        e2e_pageable = {"value": round(total_px / (reg_ms / 1e3) / 1e9, 4), "unit": "Gpix/s",
+                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(reg_ms, 3),
+                        "first_call_ms": round(first_ms, 3),
+                        "path": call + " on pageable numpy planes; the buffer is page-locked on the first call "
+                                       "(first_call_ms) and kept registered while it lives",
+                        "staged": {"value": round(total_px / (st_ms / 1e3) / 1e9, 4), "ms_per_step": round(st_ms, 3),
+                                   "path": "Cuda(register_host=False): every call through the library's pinned "
+                                           "staging ring (host copy threads, non-temporal stores)"}}
         if e2e:
             e2e_pageable["frac_of_pinned"] = round(e2e_pageable["value"] / e2e["value"], 4)
+            e2e_pageable["staged"]["frac_of_pinned"] = round(e2e_pageable["staged"]["value"] / e2e["value"], 4)
         del img, pg
 
     cpu = None

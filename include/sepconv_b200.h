@@ -221,11 +221,20 @@ int sc_planes_f32_to_hwc_u8(const float *src, uint8_t *dst, int rows, int cols, 
 
 /* End-to-end two-pass on HOST planes (the reference's Image: one pointer per
  * C-contiguous plane): streams row chunks H2D -> fused kernel -> D2H on three
- * CUDA streams with double/triple buffering, on `device`. In-place
- * (dst_planes == src_planes) is allowed, as in conv_two_pass. Pinned host memory
- * gives full PCIe rate; pageable memory works at lower rate. Blocks until done. */
+ * CUDA streams with triple buffering, on `device`. In-place
+ * (dst_planes == src_planes) is allowed, as in conv_two_pass. Pinned or
+ * registered planes are copied by DMA directly; pageable planes go through a
+ * pinned staging ring filled and drained by a pool of host threads (bound by
+ * host memory bandwidth). Blocks until done. */
 int sc_two_pass_host_f32(const float *const *src_planes, float *const *dst_planes, int nplanes,
                          int rows, int cols, const float *taps, int width, int flags, int device);
+
+/* Page-lock (cudaHostRegister, portable) / release a caller's host range, so the
+ * host entry points above DMA straight from / into it instead of staging it
+ * through their pinned ring. The Python layer caches this per numpy buffer for
+ * the buffer's lifetime (device.HostRegistry). */
+int sc_host_register(void *ptr, int64_t bytes);
+int sc_host_unregister(void *ptr);
 
 /* The reference's exact end state of BOTH host buffers of
  * convolve_image(image, kernel, TWO_PASS, plan, workspace=workspace)

@@ -63,6 +63,8 @@ EXPORTS = (
     "sc_fill_synthetic_f32",
     "sc_two_pass_host_f32",
     "sc_two_pass_host_split_f32",
+    "sc_host_register",
+    "sc_host_unregister",
     "sc_two_pass_host_band_f32",
     "sc_two_pass_host_multi_f32",
     "sc_two_pass_u8hwc",
@@ -117,6 +119,8 @@ _SIGNATURES = {
     "sc_copy_region_f32": (_STRIDED + [_i32, _i32, _i32, _i32, _vp], _i32),
     "sc_fill_synthetic_f32": ([_vp, _i64, _u64, _u64, _i32, _vp], _i32),
     "sc_two_pass_host_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
+    "sc_host_register": ([_vp, _i64], _i32),
+    "sc_host_unregister": ([_vp], _i32),
     "sc_two_pass_host_split_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_two_pass_host_band_f32": ([_vp, _vp, _i32, _i32, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_two_pass_host_multi_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _i32], _i32),

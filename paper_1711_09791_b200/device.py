@@ -280,6 +280,93 @@ def synthetic(shape, seed: int, kind: int, device="cuda", offset: int = 0) -> to
     return fill_synthetic(t, seed, kind, offset)
 
 
+class HostRegistry:
+    """Page-locked registration of callers' numpy buffers, cached for the buffer's
+    lifetime, so repeated end-to-end calls on the same pageable image (a reps
+    loop, a video buffer reused frame after frame) DMA straight from and into it
+    instead of going through the library's pinned staging ring, whose two host
+    copies make the pageable path host-memory-bound.
+
+    * registers the ROOT buffer that owns the data (views of one (P, R, C) array
+      share pages; one registration covers all of them) when it holds at least
+      `min_bytes` (SC_HOST_REGISTER_MIN_MB, default 64) and owns its memory;
+    * releases it when the buffer is garbage-collected (weakref.finalize runs
+      before numpy frees the data) or when the total registered exceeds
+      `max_bytes` (SC_HOST_REGISTER_MAX_GB, default half of physical memory;
+      least recently used first);
+    * any failure (e.g. pages already registered elsewhere) leaves the buffer
+      unregistered: the staging ring handles it with the same bits.
+    The first call on a buffer pays the page-locking (measured ~0.1 s per GB on
+    the B200 box, profiles/r02_host_mem_probe.txt); later calls do not."""
+
+    def __init__(self):
+        import os
+        from collections import OrderedDict
+
+        self._regs = OrderedDict()  # root address -> (nbytes, finalizer)
+        self.min_bytes = int(float(os.environ.get("SC_HOST_REGISTER_MIN_MB", "64")) * (1 << 20))
+        try:
+            phys = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        except (ValueError, OSError):
+            phys = 64 << 30
+        self.max_bytes = int(float(os.environ.get("SC_HOST_REGISTER_MAX_GB", str(phys / 2 / 2**30))) * 2**30)
+        self.total = 0
+
+    @staticmethod
+    def _root(arr):
+        root = arr
+        while isinstance(root.base, np.ndarray):
+            root = root.base
+        return root
+
+    def pin(self, arr) -> bool:
+        if not isinstance(arr, np.ndarray):
+            return False
+        root = self._root(arr)
+        if root.nbytes < self.min_bytes or not root.flags.owndata or root.base is not None:
+            return False
+        key = root.ctypes.data
+        if key in self._regs:
+            self._regs.move_to_end(key)
+            return True
+        while self._regs and self.total + root.nbytes > self.max_bytes:
+            old_key, (old_n, fin) = self._regs.popitem(last=False)
+            fin.detach()
+            self._release(old_key, old_n)
+        if self.total + root.nbytes > self.max_bytes:
+            return False
+        L = _lib.load()
+        if L.sc_host_register(key, root.nbytes) != _lib.SC_OK:
+            return False
+        import weakref
+
+        fin = weakref.finalize(root, self._on_free, key)
+        self._regs[key] = (root.nbytes, fin)
+        self.total += root.nbytes
+        return True
+
+    def _release(self, key, nbytes):
+        self.total -= nbytes
+        _lib.load().sc_host_unregister(key)
+
+    def _on_free(self, key):
+        item = self._regs.pop(key, None)
+        if item is not None:
+            self._release(key, item[0])
+
+    def registered(self, arr) -> bool:
+        return isinstance(arr, np.ndarray) and self._root(arr).ctypes.data in self._regs
+
+    def clear(self):
+        for key, (n, fin) in list(self._regs.items()):
+            fin.detach()
+            self._release(key, n)
+        self._regs.clear()
+
+
+host_registry = HostRegistry()
+
+
 def _host_ptrs(planes, shape=None):
     """Addresses of C-contiguous float32 host planes (numpy arrays or CPU tensors,
     pinned or pageable) sharing one 2-D shape."""
@@ -308,15 +395,20 @@ def _ptr_array(ptrs):
 
 
 def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring: bool = True,
-                  device: int = 0, devices=None) -> None:
+                  device: int = 0, devices=None, register: bool = True) -> None:
     """End-to-end two-pass on HOST planes (numpy arrays or CPU tensors; pinned planes
     are copied by DMA directly, pageable ones through the library's pinned staging
     ring): streamed H2D -> fused kernel -> D2H inside the library; blocks until done.
     dst_planes may be src_planes (in place, as conv_two_pass). devices (a list of
     device indices, one process): row bands streamed through every listed GPU
-    concurrently (sc_two_pass_host_multi_f32), same bits."""
+    concurrently (sc_two_pass_host_multi_f32), same bits. register: large numpy
+    buffers are page-locked once and kept registered while they live
+    (HostRegistry), so repeated calls DMA directly."""
     w = _taps(taps)
     src_planes, dst_planes = list(src_planes), list(dst_planes)
+    if register:
+        for a in src_planes + dst_planes:
+            host_registry.pin(a)
     ptrs_in, shape = _host_ptrs(src_planes)
     ptrs_out, _ = _host_ptrs(dst_planes, shape)
     if not ptrs_in or len(ptrs_in) != len(ptrs_out):
@@ -336,13 +428,17 @@ def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring:
     _lib.check(L.sc_two_pass_host_f32(arr_in, arr_out, n, shape[0], shape[1], _fp(w), w.size, flags, int(device)))
 
 
-def two_pass_host_split(image_planes, scratch_planes, taps, *, extended: bool = False, device: int = 0) -> None:
+def two_pass_host_split(image_planes, scratch_planes, taps, *, extended: bool = False, device: int = 0,
+                        register: bool = True) -> None:
     """The reference's end state of convolve_image(TWO_PASS) with a workspace, on HOST
     planes (S/executors.py:303-326): scratch_planes := H0 (zero outside the row
     pass's rows and columns), image_planes[valid] := V(H0) in place, image ring
     untouched. Streamed through the GPU like two_pass_host; blocks until done."""
     w = _taps(taps)
     image_planes, scratch_planes = list(image_planes), list(scratch_planes)
+    if register:
+        for a in image_planes + scratch_planes:
+            host_registry.pin(a)
     ptrs_img, shape = _host_ptrs(image_planes)
     ptrs_scr, _ = _host_ptrs(scratch_planes, shape)
     if not ptrs_img or len(ptrs_img) != len(ptrs_scr):

@@ -42,11 +42,15 @@ class Cuda:
     for host images). fused: stream host images through the fused kernel.
     devices: several GPUs from this one process (host images, fused two-pass):
     the image is split into row bands (the reference's partition_block), each
-    streamed through its own GPU and PCIe link concurrently; same bits."""
+    streamed through its own GPU and PCIe link concurrently; same bits.
+    register_host: host images' buffers of 64 MB and more are page-locked on
+    first use and stay registered while they live, so repeated calls DMA
+    straight from them (False: always stage through the pinned ring)."""
 
     device: int | None = None
     fused: bool = True
     devices: tuple[int, ...] | None = None
+    register_host: bool = True  # page-lock large host buffers once, for their lifetime (device.HostRegistry)
 
     def __post_init__(self):
         if self.device is not None and self.device < 0:
@@ -189,9 +193,10 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
         ws_planes = [_host_array(p) for p in workspace.planes]
         if two_pass and plan.fused and not given_ws:
             # the workspace is the reference's internal zero buffer: unobservable
-            dev.two_pass_host(img_planes, img_planes, taps, device=device_index, devices=plan.devices)
+            dev.two_pass_host(img_planes, img_planes, taps, device=device_index, devices=plan.devices,
+                              register=plan.register_host)
         elif two_pass:
-            dev.two_pass_host_split(img_planes, ws_planes, taps, device=device_index)
+            dev.two_pass_host_split(img_planes, ws_planes, taps, device=device_index, register=plan.register_host)
         else:
             with torch.cuda.device(device_index):
                 src = torch.stack([torch.from_numpy(a) for a in img_planes]).cuda()

@@ -249,3 +249,70 @@ def test_subnormal_random_all_paths(dev, oracle, shape):
         planes = [p.copy() for p in x]
         dev.two_pass_host(planes, planes, w)
         assert bits_equal(np.stack(planes), want)
+
+
+def test_host_registry_lifetime_and_bits(dev, oracle):
+    """Large pageable buffers are page-locked once (the ROOT buffer, covering all its
+    plane views), reused while they live, released when garbage-collected; the
+    registered path gives the same bits as the staged one."""
+    import gc
+
+    from paper_1711_09791_b200.device import HostRegistry
+
+    reg = HostRegistry()
+    reg.min_bytes = 1 << 20
+    w = np.array([1, 4, 6, 4, 1], np.float32) / np.float32(16)
+    P, R, C = 3, 700, 1024
+    x = oracle.synthetic(P * R * C, 12, kind=1).reshape(P, R, C)
+    buf = x.copy()
+    planes = [buf[p] for p in range(P)]
+    assert reg.pin(planes[0]) and reg.pin(planes[2])
+    assert len(reg._regs) == 1 and reg.total == buf.nbytes and reg.registered(planes[1])
+    L = dev._lib.load()
+    ptrs = dev._ptr_array([p.ctypes.data for p in planes])
+    dev._lib.check(L.sc_two_pass_host_f32(ptrs, ptrs, P, R, C, w.ctypes.data, 5, 0, 0))
+    assert bits_equal(buf, oracle.two_pass(x, w))
+    del planes, ptrs, buf
+    gc.collect()
+    assert reg.total == 0 and not reg._regs
+    assert not reg.pin(np.zeros((10, 10), np.float32))  # below min_bytes: staged
+    tmp = np.zeros((2, 1 << 20), np.float32)
+    assert reg.pin(tmp[1]) and reg.registered(tmp) and reg.total == tmp.nbytes  # a view pins its root
+    del tmp
+    gc.collect()
+    assert reg.total == 0
+
+
+def test_host_registry_budget_evicts_lru(dev):
+    from paper_1711_09791_b200.device import HostRegistry
+
+    reg = HostRegistry()
+    reg.min_bytes = 1 << 20
+    reg.max_bytes = 3 * (4 << 20)
+    bufs = [np.zeros(1 << 20, np.float32) for _ in range(4)]  # 4 MB each
+    for b in bufs[:3]:
+        assert reg.pin(b)
+    assert reg.pin(bufs[3]) and not reg.registered(bufs[0]) and reg.registered(bufs[3])
+    assert reg.total <= reg.max_bytes
+    reg.clear()
+    assert reg.total == 0
+
+
+def test_convolve_image_register_host_same_bits(dev, oracle):
+    import paper_1711_09791_b200 as sc
+
+    w = np.array([-1, -2, 7, -2, -1], np.float32)
+    x = oracle.synthetic(3 * 2100 * 4096, 3, kind=2).reshape(3, 2100, 4096)  # 103 MB: above the 64 MB floor
+    want = oracle.two_pass(x, w)
+    for reg in (True, False):
+        buf = x.copy()
+        img = sc.Image([sc.Plane(buf[p]) for p in range(3)])
+        for _ in range(2):  # first call registers, second reuses
+            buf[...] = x
+            sc.convolve_image(img, sc.SeparableKernel(w), sc.ConvVariant(sc.Algorithm.TWO_PASS),
+                              sc.Cuda(register_host=reg))
+            assert bits_equal(buf, want)
+        from paper_1711_09791_b200.device import host_registry
+
+        assert host_registry.registered(buf) == reg
+        host_registry.clear()
