@@ -127,6 +127,26 @@ def dist_env():
     return world, rank, local
 
 
+def workload_config(wl, world):
+    """The `config` object of both arms' JSON lines (identical for the same
+    workload and N): what is convolved, how it is split, and the L2 protocol,
+    which follows from the largest per-rank input (rank 0's share)."""
+    from paper_1711_09791_b200.multi import partition_block
+
+    if wl.frames > 1:
+        f0, f1 = partition_block(0, wl.frames, 0, world)
+        share_px = (f1 - f0) * wl.rows * wl.cols
+    else:
+        lo, hi = partition_block(0, wl.rows, 0, world)
+        share_px = (hi - lo) * wl.cols
+    in_bytes = 4 * wl.planes * share_px
+    l2 = ("inputs %.1f GB >> 126 MB L2; no flush needed" % (in_bytes / 1e9) if in_bytes >= (256 << 20) else
+          "inputs %.0f MB < 2x L2: a 256 MB L2 flush before every step, outside the step's events" % (in_bytes / 1e6))
+    return {"workload": f"{wl.name}: {wl.note}", "frames": wl.frames, "planes": wl.planes, "rows": wl.rows,
+            "cols": wl.cols, "taps": [float(v) for v in wl.tap_vector()],
+            "parallelism": f"rowband{world}" if wl.frames == 1 else f"frames{world}", "l2": l2}
+
+
 REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
 
 
@@ -239,8 +259,7 @@ def reference_arm(args, wl):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "weak" if wl.frames > 1 else "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{wl.name}: {wl.note}", "frames": wl.frames, "planes": wl.planes, "rows": wl.rows,
-                   "cols": wl.cols, "taps": [float(v) for v in wl.tap_vector()]},
+        "config": workload_config(wl, world),
         "cpu_baseline": {"value": round(value, 6), "unit": "Gpix/s", "cores": cores, "kind": kind,
                          "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 6), "unit": "Gpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -411,9 +430,6 @@ def main():
     # flush L2 before every timed step instead and time the steps one by one
     in_bytes = 4 * P * units_px
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device) if in_bytes < (256 << 20) else None
-    l2_note = ("inputs %.1f GB >> 126 MB L2; no flush needed" % (in_bytes / 1e9) if flush is None else
-               "inputs %.0f MB < 2x L2: a 256 MB L2 flush before every step, outside the step's events"
-               % (in_bytes / 1e6))
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -547,6 +563,27 @@ def main():
         finally:
             if alt is not None:
                 alt.close()
+
+    # ---- N>1 row bands: bit-exactness spot check of the timed transport's output
+    # against the single-GPU band kernel on the same rows (each rank regenerates its
+    # input rows plus halo from the counter-based generator; no data moves)
+    band_check = None
+    if band is not None and world > 1:
+        stepper.step()
+        torch.cuda.synchronize()
+        ref_in = torch.empty((P, band.in_hi - band.in_lo, C), dtype=torch.float32, device=device)
+        for p in range(P):
+            dev.fill_synthetic(ref_in[p], wl.seed, wl.kind, offset=p * R * C + band.in_lo * C)
+        ref_out = torch.empty_like(dst)
+        dev.two_pass_band(ref_in, w, ref_out, global_rows=R, src_row0=band.in_lo, dst_row0=band.lo,
+                          out_lo=band.lo, out_hi=band.hi)
+        same = torch.equal(ref_out.view(torch.int32), dst.view(torch.int32))
+        flag = torch.tensor([1 if same else 0], device=device if backend == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        band_check = ("bit-exact on every rank vs the single-GPU band kernel" if int(flag.item()) == 1
+                      else "MISMATCH")
+        del ref_in, ref_out
+        dist.barrier()
 
     # ---- end to end through the C-ABI host entry point (pinned host planes)
     e2e = None
@@ -685,11 +722,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak" if wl.frames > 1 else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{wl.name}: {wl.note}", "frames": wl.frames, "planes": P, "rows": R, "cols": C,
-                       "taps": [float(v) for v in w], "parallelism": f"rowband{world}" if wl.frames == 1
-                       else f"frames{world}", "l2": l2_note,
-                       **({"halo": halo} if band is not None and world > 1 else {})},
+            "config": workload_config(wl, world),
+            **({"halo": halo} if band is not None and world > 1 else {}),
             **({"halo_alt": halo_alt} if halo_alt is not None else {}),
+            **({"band_check": band_check} if band_check is not None else {}),
             "effective_GBps": round(eff, 1), "pct_of_8TBps": round(100 * eff / NOMINAL_HBM_GBPS, 2),
             "pct_of_measured_copy": round(100 * eff / peak, 2),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,

@@ -131,8 +131,9 @@ int sc_band_signal_wait(const uint64_t *sig_above, const uint64_t *sig_below, in
  * A band plan holds, for one band of `nplanes` planes (owned rows
  * [band_lo, band_hi) of a global_rows x cols image; src / dst hold exactly those
  * rows), ONE packed send and ONE receive buffer of nplanes x r x cols per
- * neighbour, a communication stream and (use_graph) the whole step captured in a
- * CUDA graph. A step: pack the r boundary rows of every plane (one 2-D copy per
+ * neighbour, a communication stream and, with use_graph, the whole step captured
+ * in a CUDA graph (off by default in the Python layer: measured, the graph launch
+ * with NCCL nodes costs the host more than the eager step's ~25 us). A step: pack the r boundary rows of every plane (one 2-D copy per
  * side) and exchange them (ncclSend/ncclRecv in one group) on the communication
  * stream while the interior rows [lo+r, hi-r) compute on the caller's stream;
  * then ONE launch produces both boundary strips, reading the halo rows straight

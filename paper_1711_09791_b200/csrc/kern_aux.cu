@@ -177,4 +177,32 @@ cudaError_t launch_signal_wait(const unsigned long long* a, const unsigned long 
     return cudaGetLastError();
 }
 
+// Halo pack of the NCCL band step: rows [row_a, row_a + r) and [row_b, row_b + r)
+// of every plane into two contiguous (P, r, C) buffers, in one launch (either
+// destination may be null).
+__global__ void pack_rows_kernel(const float* src, long long sps, long long srs, int P, int r, int C, int row_a,
+                                 float* out_a, int row_b, float* out_b) {
+    const long long per = (long long)P * r * C;
+    const long long total = 2 * per;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const bool second = i >= per;
+        float* out = second ? out_b : out_a;
+        if (!out) continue;
+        const long long k = second ? i - per : i;
+        const int p = (int)(k / ((long long)r * C));
+        const long long rem = k - (long long)p * r * C;
+        const int y = (int)(rem / C), x = (int)(rem - (long long)y * C);
+        out[k] = src[p * sps + (long long)((second ? row_b : row_a) + y) * srs + x];
+    }
+}
+
+cudaError_t launch_pack_rows(const float* src, long long sps, long long srs, int P, int r, int C, int row_a,
+                             float* out_a, int row_b, float* out_b, cudaStream_t s) {
+    const long long total = 2LL * P * r * C;
+    pack_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, sps, srs, P, r, C, row_a, out_a, row_b, out_b);
+    count_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace sc

@@ -135,7 +135,8 @@ struct Params {
     // until both neighbours published ready >= epoch before its first read or
     // write (their halo rows are current; and a neighbour that started this step
     // has finished the previous one, so buffers it read then may be overwritten),
-    // and the last CTA to finish publishes done = epoch. sig_err (host-mapped) is
+    // and the last CTA to finish publishes done = epoch. (ready is published by
+    // CTA 0 alone: the grid is resident, and nothing it waits for depends on it.) sig_err (host-mapped) is
     // set if a wait outlives sig_timeout_ns.
     unsigned long long* sig_self;
     const unsigned long long* sig_above;
@@ -1246,7 +1247,8 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     // launched with programmatic stream serialization: the setup above overlapped
     // the previous kernel's tail; no global memory is touched before it completed
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (p.epoch && threadIdx.x == 0) st_release_sys(p.sig_self, p.epoch);  // this band's inputs are in place
+    // this band's inputs are in place (the previous grid completed): one CTA says so
+    if (p.epoch && threadIdx.x == 0 && blockIdx.x == 0) st_release_sys(p.sig_self, p.epoch);
 
     if (warp == 0) {
 #ifdef SC_TRACE
@@ -1295,7 +1297,9 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
         // own kernels, which waited for this step's ready)
         consumer_bar(ncw * 32);
         if (threadIdx.x == 32) {
-            __threadfence_system();
+            // GPU-scope ordering of this CTA's stores before its count; the last CTA
+            // (which observed every count) releases them all at system scope
+            __threadfence();
             unsigned long long* cnt = p.sig_self + 2;
             if (atomicAdd(cnt, 1ULL) == (unsigned long long)gridDim.x - 1) {
                 *cnt = 0;

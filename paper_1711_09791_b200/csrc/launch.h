@@ -76,6 +76,10 @@ struct RowsJob {
     unsigned int* sig_err = nullptr;
 };
 
+// NCCL band step: both halo packs in one launch (kern_aux.cu)
+cudaError_t launch_pack_rows(const float* src, long long sps, long long srs, int P, int r, int C, int row_a,
+                             float* out_a, int row_b, float* out_b, cudaStream_t s);
+
 // one-thread kernel: wait until the neighbours' signal word `word` (0 ready,
 // 1 done) reaches `value` (kern_aux.cu)
 cudaError_t launch_signal_wait(const unsigned long long* a, const unsigned long long* b, int word,

@@ -7,15 +7,16 @@
 // A band plan owns, per neighbour, ONE packed send buffer and ONE receive buffer
 // of nplanes x r x cols floats, a communication stream and two events. A step:
 //   comm stream : wait(inputs ready) -> pack the r boundary rows of every plane
-//                 (one 2-D copy per side) -> one NCCL group (send + recv per
+//                 (one launch for both sides) -> one NCCL group (send + recv per
 //                 neighbour)
 //   caller's    : interior rows [lo+r, hi-r) (they need no halo) -> wait(exchange)
 //   stream        -> ONE launch for both boundary strips, whose producer reads the
 //                 halo rows straight from the receive buffers (the kernel's
 //                 above/below row sources, no unpack copy)
-// The whole step is captured once into a CUDA graph (NCCL operations capture), so
-// a step costs the host one cudaGraphLaunch; if capture is refused the plan
-// issues the same operations eagerly.
+// Steps are issued eagerly by default (~25 us of host time, measured; far below
+// the GPU time of a step). use_graph captures the step once into a CUDA graph
+// (NCCL operations capture); measured on one B200 its launch cost the host MORE
+// (~100 us per step with the NCCL nodes), so it is opt-in.
 //
 // libnccl.so.2 is loaded at run time (the one torch already mapped, if any):
 // the library itself does not link against NCCL.
@@ -23,6 +24,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -124,31 +128,27 @@ static RowsJob band_job(const BandPlan& b) {
     return j;
 }
 
-static cudaError_t pack(const BandPlan& b, float* out, int row /* band-local first row */) {
-    const size_t rowb = (size_t)b.C * sizeof(float);
-    if (b.srs == b.C)  // the r rows of a plane are contiguous: one 2-D copy over the planes
-        return cudaMemcpy2DAsync(out, (size_t)b.r * rowb, b.src + (size_t)row * b.C, (size_t)b.sps * sizeof(float),
-                                 (size_t)b.r * rowb, (size_t)b.P, cudaMemcpyDeviceToDevice, b.cs);
-    for (int p = 0; p < b.P; ++p) {
-        cudaError_t e = cudaMemcpy2DAsync(out + (size_t)p * b.r * b.C, rowb, b.src + p * b.sps + (size_t)row * b.srs,
-                                          (size_t)b.srs * sizeof(float), rowb, (size_t)b.r,
-                                          cudaMemcpyDeviceToDevice, b.cs);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+static double host_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-// The step's operations on stream s (eager, or under capture).
+// The step's operations on stream s (eager, or under capture). SC_BAND_TIMING=1
+// prints the host time of each phase (tools/band_host_time.py).
 static int issue_step(BandPlan& b, cudaStream_t s) {
     const NcclApi& api = nccl();
+    const bool timing = std::getenv("SC_BAND_TIMING") != nullptr;
+    double t[5] = {timing ? host_us() : 0.0, 0, 0, 0, 0};
     const bool has_a = b.above >= 0, has_b = b.below >= 0;
     cudaError_t e;
     const size_t n = (size_t)b.P * b.r * b.C;
     if (has_a || has_b) {
         if ((e = cudaEventRecord(b.ev_in, s)) != cudaSuccess || (e = cudaStreamWaitEvent(b.cs, b.ev_in, 0)) != cudaSuccess)
             return fail_cuda(e, "band step: event");
-        if (has_a && (e = pack(b, b.send_top, 0)) != cudaSuccess) return fail_cuda(e, "band step: pack");
-        if (has_b && (e = pack(b, b.send_bot, b.hi - b.lo - b.r)) != cudaSuccess) return fail_cuda(e, "band step: pack");
+        // both packs in one launch (two 2-D copies cost the host more than a launch)
+        if ((e = launch_pack_rows(b.src, b.sps, b.srs, b.P, b.r, b.C, 0, has_a ? b.send_top : nullptr,
+                                  b.hi - b.lo - b.r, has_b ? b.send_bot : nullptr, b.cs)) != cudaSuccess)
+            return fail_cuda(e, "band step: pack");
+        if (timing) t[1] = host_us();
         ncclResult_t nr = api.group_start();
         if (nr == ncclSuccess && has_a) nr = api.send(b.send_top, n, ncclFloat32, b.above, b.comm, b.cs);
         if (nr == ncclSuccess && has_a) nr = api.recv(b.recv_top, n, ncclFloat32, b.above, b.comm, b.cs);
@@ -159,6 +159,7 @@ static int issue_step(BandPlan& b, cudaStream_t s) {
         if (ne != ncclSuccess) return nccl_fail(ne, "band step: group");
         if ((e = cudaEventRecord(b.ev_x, b.cs)) != cudaSuccess) return fail_cuda(e, "band step: event");
     }
+    if (timing) t[2] = host_us();
     const int ilo = b.lo + (has_a ? b.r : 0), ihi = b.hi - (has_b ? b.r : 0);
     RowsJob j = band_job(b);
     if (ihi > ilo && (has_a || has_b)) {
@@ -168,6 +169,7 @@ static int issue_step(BandPlan& b, cudaStream_t s) {
         const int rc = launch_rows(j, s);
         if (rc != SC_OK) return rc;
     }
+    if (timing) t[3] = host_us();
     if ((has_a || has_b) && (e = cudaStreamWaitEvent(s, b.ev_x, 0)) != cudaSuccess)
         return fail_cuda(e, "band step: event");
     j = band_job(b);
@@ -195,7 +197,13 @@ static int issue_step(BandPlan& b, cudaStream_t s) {
         j.out_lo = b.lo;  // band too short for an interior (or no neighbours): one launch
         j.out_hi = b.hi;
     }
-    return launch_rows(j, s);
+    const int rc = launch_rows(j, s);
+    if (timing) {
+        t[4] = host_us();
+        std::fprintf(stderr, "[sc band step] pack+events %.1f us, nccl group %.1f us, interior launch %.1f us, "
+                     "boundary launch %.1f us\n", t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3]);
+    }
+    return rc;
 }
 
 }  // namespace sc

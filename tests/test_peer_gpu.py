@@ -156,8 +156,10 @@ def test_bench_two_ranks_on_one_gpu(halo):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["config"]["halo"] == halo and line["value"] > 0
+    assert line["n_gpus"] == 2 and line["halo"] == halo and line["value"] > 0
     assert line["gpu_launches"] >= 5 and line["e2e"]["value"] > 0
+    assert line["band_check"].startswith("bit-exact"), line["band_check"]
+    assert line["config"]["parallelism"] == "rowband2"
 
 
 @pytest.mark.parametrize("world,extended", [(3, False), (4, True)])
