@@ -14,7 +14,12 @@ the roofline fraction uses; ncu's dram__bytes show the real traffic.
 import argparse, csv, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-OPS = ["fused", "split", "hpass_zero", "vpass", "single", "single_copyback", "u8"]
+OPS = ["fused", "split", "hpass_zero", "vpass", "single", "single_general", "single_copyback", "u8"]
+
+# FP32 pipe peak for the FP-bound kernels: 126.7 lane-ops per cycle per SM measured
+# for FFMA/FMUL/FADD and their packed forms alike (tools/fp2_rate.cu,
+# profiles/r02_fp2_rate.txt) x 148 SMs x the 1965 MHz maximum SM clock
+FP32_PEAK_OPS = 126.7 * 148 * 1.965e9
 
 
 def build_ops(cfg):
@@ -29,6 +34,9 @@ def build_ops(cfg):
     y = torch.empty_like(x)
     z = torch.zeros_like(x)
     dense = np.outer(w, w).astype(np.float32)
+    from paper_1711_09791_b200.configs import CONFIG_TAPS
+    wn = CONFIG_TAPS["normal"]  # asymmetric taps (config 2): a dense matrix with no mirror symmetry
+    dense_general = np.outer(wn, wn).astype(np.float32)
     n_px = x.numel()                      # samples of all planes
     R, C = wl.rows, wl.cols
     valid = (R - 2 * r) * (C - 2 * r) * (n_px // (R * C))
@@ -43,6 +51,8 @@ def build_ops(cfg):
                        "read image + write scratch (all rows, ring zeroed)"),
         "vpass": (lambda: dev.vpass(y, w, z), 4 * n_px + 4 * valid, "read scratch + write valid region"),
         "single": (lambda: dev.single_pass(x, dense, y), 4 * n_px + 4 * valid, "read image + write valid region"),
+        "single_general": (lambda: dev.single_pass(x, dense_general, y), 4 * n_px + 4 * valid,
+                           "read image + write valid region (config-2 taps: no mirror symmetry)"),
         "single_copyback": (lambda: dev.single_pass(x, dense, y, copy_back=True), 4 * n_px + 8 * valid,
                             "read image + write valid region to workspace and image"),
         "u8": (lambda: dev.two_pass_u8hwc(u8, w, u8o), 6 * R * C, "read + write 3 B/pixel"),
@@ -83,8 +93,17 @@ def main():
             e.synchronize()
             ts.append(s.elapsed_time(e) / 5)
         ms = float(np.median(ts))
+        W = len(wl.tap_vector())
+        R, C = wl.rows, wl.cols
+        valid = (R - 2 * (W // 2)) * (C - 2 * (W // 2)) * (wl.frames * wl.planes)
+        # the reference algorithm's float32 operations (S/conv.py:86-114, 215-293)
+        ops_n = {"single": valid * (2 * W * W - 1), "single_general": valid * (2 * W * W - 1),
+                 "single_copyback": valid * (2 * W * W - 1), "fused": valid * 2 * (2 * W - 1),
+                 "split": valid * 2 * (2 * W - 1), "u8": (R - 2 * (W // 2)) * (C - 2 * (W // 2)) * 3 * 2 * (2 * W - 1),
+                 "hpass_zero": valid * (2 * W - 1), "vpass": valid * (2 * W - 1)}[name]
         print(json.dumps({"cfg": a.cfg, "op": name, "ms": round(ms, 4), "alg_bytes": alg,
-                          "alg_GBps": round(alg / ms / 1e6, 1), "what": what}), flush=True)
+                          "alg_GBps": round(alg / ms / 1e6, 1), "fp32_ops": ops_n,
+                          "fp32_frac": round(ops_n / (ms / 1e3) / FP32_PEAK_OPS, 3), "what": what}), flush=True)
 
 
 def merge(ncu_csv, times):
@@ -112,14 +131,16 @@ def merge(ncu_csv, times):
     peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                         "MEASURED_PEAKS.json")))
     peak = float(peaks.get("hbm_gbs", 6551.4))
-    print("| op | kernels | event ms | alg bytes | alg GB/s | frac of measured copy | ncu ms (sum) | ncu dram bytes | dram / alg |")
-    print("|---|---|---|---|---|---|---|---|---|")
+    print("| op | kernels | event ms | alg bytes | alg GB/s | frac of measured copy | FP32 ops (ref. algorithm) | "
+          "frac of FP32 pipe | ncu ms (sum) | ncu dram bytes | dram / alg |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|")
     for d, g in zip(t, groups):
         dram = sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in g)
         nms = sum(x.get("gpu__time_duration.sum", 0) for x in g)
         names = ", ".join(sorted({x["name"].split("(")[0].replace("void ", "").replace("sc::", "") for x in g}))
         print(f"| {d['op']} | `{names}` | {d['ms']} | {d['alg_bytes'] / 1e9:.3f} G | {d['alg_GBps']} | "
-              f"{d['alg_GBps'] / peak:.3f} | {nms:.4f} | {dram / 1e9:.3f} G | {dram / d['alg_bytes']:.3f} |")
+              f"{d['alg_GBps'] / peak:.3f} | {d.get('fp32_ops', 0) / 1e9:.2f} G | {d.get('fp32_frac', 0):.3f} | "
+              f"{nms:.4f} | {dram / 1e9:.3f} G | {dram / d['alg_bytes']:.3f} |")
 
 
 if __name__ == "__main__":
