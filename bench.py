@@ -709,6 +709,16 @@ def main():
         if e2e:
             e2e_pageable["frac_of_pinned"] = round(e2e_pageable["value"] / e2e["value"], 4)
             e2e_pageable["staged"]["frac_of_pinned"] = round(e2e_pageable["staged"]["value"] / e2e["value"], 4)
+        ndev = torch.cuda.device_count()
+        if ndev > 1:
+            # one process driving every visible GPU (the reference's plans are
+            # single-process): row bands streamed through each GPU's own PCIe link
+            multi_plan = Cuda(devices=tuple(range(ndev)))
+            timed(multi_plan, 1)
+            m_ms = timed(multi_plan, args.e2e_steps)
+            e2e_pageable["devices"] = {"n": ndev, "value": round(total_px / (m_ms / 1e3) / 1e9, 4),
+                                       "ms_per_step": round(m_ms, 3),
+                                       "path": f"Cuda(devices=range({ndev})): sc_two_pass_host_multi_f32"}
         del img, pg
 
     cpu = None
