@@ -535,6 +535,34 @@ def main():
         roofline["frac_of_same_size_copy"] = round(copy_ms / ms, 4)
         del dst_copy
 
+    # ---- N=1: the drop-in call on HBM-resident planes, as a sepconv_lab user's
+    # convolve_image(image, kernel, TWO_PASS, Cuda()) runs it -- in place, without a
+    # workspace (one pass, no scratch) and with one (the reference's scratch end
+    # state too: one read, two writes)
+    dropin = None
+    if band is not None and world == 1 and args.e2e_steps > 0:
+        img = src.clone()
+        scr = torch.empty_like(src)
+
+        def ev_ms(fn, n=10):
+            fn()
+            torch.cuda.synchronize()
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream)
+            for _ in range(n):
+                fn()
+            b_ev.record(stream)
+            torch.cuda.synchronize()
+            return a_ev.elapsed_time(b_ev) / n
+
+        ip_ms = ev_ms(lambda: dev.two_pass_inplace(img, w))
+        sp_ms = ev_ms(lambda: dev.two_pass_split(img, scr, w))
+        dropin = {"no_workspace": {"ms": round(ip_ms, 4), "value": round(total_px / (ip_ms / 1e3) / 1e9, 3),
+                                   "path": "sc_two_pass_inplace_f32: in place, one pass + halo snapshot"},
+                  "workspace": {"ms": round(sp_ms, 4), "value": round(total_px / (sp_ms / 1e3) / 1e9, 3),
+                                "path": "sc_two_pass_split_f32: image and scratch (H0), one pass + halo snapshot"}}
+        del img, scr
+
     # ---- N>1 row bands: the same steps with the OTHER halo transport (secondary)
     halo_alt = None
     if band is not None and world > 1 and backend == "nccl" and halo in ("peer", "nccl"):
@@ -736,6 +764,7 @@ def main():
             **({"halo": halo} if band is not None and world > 1 else {}),
             **({"halo_alt": halo_alt} if halo_alt is not None else {}),
             **({"band_check": band_check} if band_check is not None else {}),
+            **({"dropin_device": dropin} if dropin is not None else {}),
             "effective_GBps": round(eff, 1), "pct_of_8TBps": round(100 * eff / NOMINAL_HBM_GBPS, 2),
             "pct_of_measured_copy": round(100 * eff / peak, 2),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,

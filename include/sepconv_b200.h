@@ -184,6 +184,15 @@ int sc_two_pass_split_f32(float *image, float *scratch, int nplanes, int rows, i
                           int64_t image_row_stride, int64_t scratch_row_stride,
                           const float *taps, int width, int flags, void *stream);
 
+/* The two-pass in place on device planes with NO observable scratch -- what
+ * convolve_image(image, kernel, TWO_PASS, plan) does when the caller passes no
+ * workspace (the reference then zeroes a fresh one nobody sees,
+ * S/executors.py:303-304): image[valid] := V(H0), image ring untouched.
+ * 16-B aligned rows: one pass over the image (2 traversals + the halo snapshot);
+ * otherwise the row pass into a stream-ordered temporary + the column pass. */
+int sc_two_pass_inplace_f32(float *image, int nplanes, int rows, int cols, int64_t plane_stride,
+                            int64_t row_stride, const float *taps, int width, int flags, void *stream);
+
 /* Single pass with the dense width x width matrix (row-major, pass the reference's
  * outer_product(k).matrix, S/kernels.py:66-72): dst[valid] := D, dst ring untouched
  * (single_pass_rows_vec S/conv.py:86-114 == unrolled5 :146-175). SC_COPY_BACK then

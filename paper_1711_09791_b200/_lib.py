@@ -58,6 +58,7 @@ EXPORTS = (
     "sc_hpass_f32",
     "sc_vpass_f32",
     "sc_two_pass_split_f32",
+    "sc_two_pass_inplace_f32",
     "sc_single_pass_f32",
     "sc_copy_region_f32",
     "sc_fill_synthetic_f32",
@@ -115,6 +116,7 @@ _SIGNATURES = {
     "sc_hpass_f32": (_STRIDED + [_i32, _i32, _fp, _i32, _i32, _vp], _i32),
     "sc_vpass_f32": (_STRIDED + [_i32, _i32, _fp, _i32, _i32, _vp], _i32),
     "sc_two_pass_split_f32": (_STRIDED + [_fp, _i32, _i32, _vp], _i32),
+    "sc_two_pass_inplace_f32": ([_vp, _i32, _i32, _i32, _i64, _i64, _fp, _i32, _i32, _vp], _i32),
     "sc_single_pass_f32": (_STRIDED + [_fp, _i32, _i32, _vp], _i32),
     "sc_copy_region_f32": (_STRIDED + [_i32, _i32, _i32, _i32, _vp], _i32),
     "sc_fill_synthetic_f32": ([_vp, _i64, _u64, _u64, _i32, _vp], _i32),

@@ -1207,6 +1207,64 @@ int sc_two_pass_split_f32(float* image, float* scratch, int nplanes, int rows, i
                        scratch_row_stride, image_row_stride, r, rows - r, taps, nullptr, width, 0, stream);
 }
 
+int sc_two_pass_inplace_f32(float* image, int nplanes, int rows, int cols, int64_t plane_stride, int64_t row_stride,
+                            const float* taps, int width, int flags, void* stream) {
+    set_error("");
+    SC_TRY(check_width(width));
+    SC_TRY(check_dims(nplanes, rows, cols, width));
+    if (!taps) return fail(SC_INVALID_ARGUMENT, "null taps");
+    SC_TRY(check_strides(nplanes, rows, cols, plane_stride, row_stride, "image"));
+    SC_TRY(prepare(image));
+    const int r = width / 2;
+    const int h_lo = (flags & SC_EXTENDED) ? 0 : r;
+    const int h_hi = (flags & SC_EXTENDED) ? rows : rows - r;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Knobs kn = read_knobs();
+    const bool aligned = cols % 4 == 0 && aligned16(image) && plane_stride % 4 == 0 && row_stride % 4 == 0 &&
+                         !kn.force_generic;
+    if (aligned && !kn.split_passes && width <= MAX_W) {
+        // the one-pass split kernel without its scratch writes: each item reads its
+        // own rows before overwriting them, other items' halos from the pre-launch
+        // snapshot -- 2 traversals (+ the ~5% snapshot) instead of 3
+        RowsJob j{};
+        j.mode = MODE_SPLITF;
+        j.src = image;
+        j.dst = image;
+        j.sps = j.dps = plane_stride;
+        j.srs = j.drs = row_stride;
+        j.nplanes = nplanes;
+        j.R = rows;
+        j.C = cols;
+        j.src_row0 = 0;
+        j.src_rows = rows;
+        j.dst_row0 = 0;
+        j.out_lo = 0;
+        j.out_hi = rows;
+        j.hrow_lo = h_lo;
+        j.hrow_hi = h_hi;
+        j.flags = (flags & SC_EXTENDED) | SC_NO_RING;
+        j.width = width;
+        j.taps = taps;
+        j.scr = nullptr;
+        const int rc = launch_rows(j, s);
+        if (rc != kNeedTwoLaunches) return rc;
+        set_error("");
+    }
+    // any other shape: H0 into a stream-ordered temporary, then the column pass
+    float* tmp = nullptr;
+    const size_t n = (size_t)nplanes * rows * cols;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * sizeof(float), s);
+    if (e != cudaSuccess) return cuda_fail(e, "in-place two-pass scratch allocation");
+    const long long tps = (long long)rows * cols;
+    int rc = pass_common(MODE_HPASS, image, tmp, nplanes, rows, cols, plane_stride, tps, row_stride, cols, h_lo, h_hi,
+                         taps, nullptr, width, SC_ZERO_FILL, stream);
+    if (rc == SC_OK)
+        rc = pass_common(MODE_VPASS, tmp, image, nplanes, rows, cols, tps, plane_stride, cols, row_stride, r, rows - r,
+                         taps, nullptr, width, 0, stream);
+    cudaFreeAsync(tmp, s);
+    return rc;
+}
+
 int sc_single_pass_f32(float* src, float* dst, int nplanes, int rows, int cols, int64_t src_plane_stride,
                        int64_t dst_plane_stride, int64_t src_row_stride, int64_t dst_row_stride, const float* dense,
                        int width, int flags, void* stream) {

@@ -1074,8 +1074,9 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                             if constexpr (MODE == MODE_SPLITF) {
                                 // the reference's scratch row: H0 on the valid columns, 0 on the
                                 // column ring and on dead rows (the workspace is zeroed first,
-                                // S/conv.py:414); own rows only
-                                if (yi >= it.ylo && yi < it.yhi) {
+                                // S/conv.py:414); own rows only. No scratch (null): the
+                                // in-place fused two-pass -- image only, 2 traversals
+                                if (p.scr && yi >= it.ylo && yi < it.yhi) {
                                     float* hrow = p.scr + (long long)it.plane * p.scr_ps + (long long)yi * p.scr_rs;
                                     if (fast[g]) {
                                         st4(hrow + x4[g], v);

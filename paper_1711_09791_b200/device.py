@@ -241,6 +241,18 @@ def two_pass_split(image: torch.Tensor, scratch: torch.Tensor, taps, *, extended
     return image
 
 
+def two_pass_inplace(image: torch.Tensor, taps, *, extended: bool = False) -> torch.Tensor:
+    """The two-pass in place with no observable scratch (convolve_image without a
+    workspace): image[valid] := V(H0), ring untouched. One pass over the image
+    (plus a small halo snapshot) on 16-B aligned rows. Returns image."""
+    w = _taps(taps)
+    n, R, C, ps, rs = _planes(image, "image")
+    L = _lib.load()
+    _lib.check(L.sc_two_pass_inplace_f32(image.data_ptr(), n, R, C, ps, rs, _fp(w), w.size,
+                                         _lib.SC_EXTENDED if extended else 0, _stream(image)))
+    return image
+
+
 def single_pass(src: torch.Tensor, dense, out: torch.Tensor, *, copy_back: bool = False) -> torch.Tensor:
     """single_pass_rows_vec (S/conv.py:86-114) with the dense matrix; out's ring untouched.
     copy_back additionally writes the valid region into src (S/executors.py:330-331)."""

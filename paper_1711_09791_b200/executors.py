@@ -9,7 +9,9 @@ results are bit-identical to every reference plan (T/test_executors.py:188-231).
 Two-pass end states are the reference's in every case (S/executors.py:303-326):
 workspace = H0 scratch (zeroed, then the row pass), image = V(H0) with its ring
 untouched.
-  * device image: one pass that writes both buffers (K5, or K2+K3).
+  * device image with a workspace given: one pass that writes both buffers (K5,
+    or K2+K3); without one: the same pass without the scratch writes
+    (sc_two_pass_inplace_f32, 2 traversals).
   * host image with a workspace given: the streamed split path (H2D -> K1 + the
     row pass -> D2H of both buffers, sc_two_pass_host_split_f32).
   * host image without a workspace (the reference then allocates a zero one the
@@ -158,30 +160,34 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
     on_dev = _on_device(image)
     if not on_dev and any(_on_device_plane(p) for p in image.planes):
         raise InvalidArgumentError("image planes must all be host arrays or all CUDA tensors")
+    two_pass = algo is Algorithm.TWO_PASS
+    copy_back = bool(variant.copy_back) and not two_pass
     given_ws = workspace is not None
-    if workspace is None:
-        workspace = Image.zeros_like(image)
-    if workspace.rows != rows or workspace.cols != cols or workspace.plane_count != nplanes:
-        raise InvalidArgumentError("workspace must match the image's dimensions")
-    if _on_device(workspace) != on_dev:
-        raise InvalidArgumentError("workspace must live where the image lives")
+    if workspace is None and not (two_pass and plan.fused):
+        workspace = Image.zeros_like(image)  # the reference's fresh zero workspace (S/executors.py:303-304)
+    if workspace is not None:
+        if workspace.rows != rows or workspace.cols != cols or workspace.plane_count != nplanes:
+            raise InvalidArgumentError("workspace must match the image's dimensions")
+        if _on_device(workspace) != on_dev:
+            raise InvalidArgumentError("workspace must live where the image lives")
+    # (two-pass without a workspace: the fused paths need none, nothing is allocated)
 
     stats = LaunchStats()
     before = _lib.launch_count()
     t0 = time.perf_counter_ns()
-    two_pass = algo is Algorithm.TWO_PASS
-    copy_back = bool(variant.copy_back) and not two_pass
 
     if on_dev:
         device_index = image.planes[0].data.device
         with torch.cuda.device(device_index):
             img_groups = _device_groups(image)
-            ws_groups = _device_groups(workspace)
+            ws_groups = _device_groups(workspace) if workspace is not None else [None] * len(img_groups)
             if len(img_groups) != len(ws_groups):
                 img_groups = [p.data.unsqueeze(0) for p in image.planes]
                 ws_groups = [p.data.unsqueeze(0) for p in workspace.planes]
             for ig, wg in zip(img_groups, ws_groups):
-                if two_pass:
+                if two_pass and not given_ws and plan.fused:
+                    dev.two_pass_inplace(ig, taps)  # the workspace is unobservable: image only
+                elif two_pass:
                     dev.two_pass_split(ig, wg, taps)
                 else:
                     dev.single_pass(ig, outer_product(kernel).matrix, wg, copy_back=copy_back)
@@ -190,7 +196,7 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
         device_index = plan.device if plan.device is not None else (
             plan.devices[0] if plan.devices else torch.cuda.current_device())
         img_planes = [_host_array(p) for p in image.planes]
-        ws_planes = [_host_array(p) for p in workspace.planes]
+        ws_planes = [_host_array(p) for p in workspace.planes] if workspace is not None else None
         if two_pass and plan.fused and not given_ws:
             # the workspace is the reference's internal zero buffer: unobservable
             dev.two_pass_host(img_planes, img_planes, taps, device=device_index, devices=plan.devices,

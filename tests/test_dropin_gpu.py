@@ -99,6 +99,16 @@ def test_convolve_image_two_pass(sc, name, where):
 
 
 @pytest.mark.parametrize("name", CASES)
+def test_convolve_image_two_pass_device_no_workspace(sc, name):
+    """Device image, no workspace: the in-place pass without scratch writes."""
+    g = load_golden(name)
+    img = sc.Image.from_tensor(torch.from_numpy(g["input"].copy()).cuda())
+    stats = sc.convolve_image(img, sc.SeparableKernel(g["taps"]), sc.ConvVariant(sc.Algorithm.TWO_PASS), sc.Cuda())
+    assert np.array_equal(stack(img), g["two_pass_faithful_image"])
+    assert stats.parallel_region_launches >= 1
+
+
+@pytest.mark.parametrize("name", CASES)
 def test_convolve_image_two_pass_host_no_workspace(sc, name):
     """No workspace: the reference allocates an internal zero one the caller never
     sees (S/executors.py:303-304), so the streamed fused path runs (image only)."""
