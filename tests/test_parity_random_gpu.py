@@ -266,3 +266,33 @@ def test_random_in_place_one_pass_modes(oracle, P, R, C4, width, seed, extended,
     exp[:, r:R - r, r:C - r] = want[:, r:R - r, r:C - r]
     assert bits(ws.cpu().numpy(), want)
     assert bits(img.cpu().numpy(), exp)
+
+
+@settings(max_examples=120 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(shape=shapes, width=st.sampled_from([1, 3, 5, 7, 9, 11, 15]), seed=st.integers(0, 2**32 - 1),
+       generic=st.booleans(), extended=st.booleans(), tiny=st.booleans())
+def test_random_inplace_and_host_split(oracle, monkeypatch, shape, width, seed, generic, extended, tiny):
+    """Round-2 paths: the in-place two-pass (no scratch) on device planes, and the
+    host split path (image + workspace end state, 16-row chunks) on pageable
+    planes; tiny: values around FLT_MIN (subnormal products and sums)."""
+    _need_gpu()
+    from paper_1711_09791_b200 import device as dev
+
+    P, R, C = shape
+    if R < width or C < width:
+        return
+    monkeypatch.setenv("SC_FORCE_GENERIC", "1" if generic else "0")
+    monkeypatch.setenv("SC_HOST_CHUNK_MB", "0")
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(-2, 2, size=width).astype(np.float32)
+    scale = np.float32(np.finfo(np.float32).tiny) if tiny else np.float32(300)
+    x = (rng.uniform(-1, 1, size=(P, R, C)) * scale).astype(np.float32)
+    want = oracle.two_pass(x, w, extended=extended)
+    xd = torch.from_numpy(x).cuda()
+    dev.two_pass_inplace(xd, w, extended=extended)
+    assert bits(xd.cpu().numpy(), want)
+    planes = [p.copy() for p in x]
+    scr = [np.full_like(p, 9.0) for p in x]
+    dev.two_pass_host_split(planes, scr, w, extended=extended, register=False)
+    assert bits(np.stack(planes), want)
+    assert bits(np.stack(scr), oracle.two_pass_scratch(x, w, extended=extended))
