@@ -95,14 +95,16 @@ int sc_two_pass_band_peer_f32(const float *src, float *dst, int nplanes, int glo
                               void *stream);
 
 /* The same band step with device-side readiness signalling between ranks, so a
- * step on FRESH inputs needs no host barrier. sig_self: this band's three u64
- * signal words [ready epoch, done epoch, finished-CTA count] in its own device
- * memory (zero-initialised, exported to the neighbours with sc_ipc_export);
+ * step on FRESH inputs needs no host barrier. sig_self: this band's signal
+ * block of 8 u64 words in its own device memory (zero-initialised, exported to
+ * the neighbours with sc_ipc_export): [0] ready epoch, [2] / [3] running counts
+ * of this band's items that finished reading the band above / below, [4] / [5]
+ * how many per launch;
  * sig_above / sig_below: the neighbours' words mapped with sc_ipc_open (NULL at
  * the image edges). epoch: this step's number, 1, 2, ... Every CTA publishes
  * ready = epoch when it starts (the band's inputs are in place, by stream order)
  * and waits for both neighbours' ready >= epoch before its first read or write;
- * the last CTA publishes done = epoch. A neighbour that has started step e has
+ * every item that read a neighbour's rows counts itself once its copies landed. A neighbour that has started step e has
  * finished step e-1, so ping-pong buffers (step e writes what neighbours read in
  * step e-1) are safe too. sig_err (host-mapped u32, may be NULL) is set when a
  * wait outlives SC_PEER_TIMEOUT_MS (default 20000 ms); the kernel then goes on
@@ -117,9 +119,11 @@ int sc_two_pass_band_peer_sig_f32(const float *src, float *dst, int nplanes, int
                                   const uint64_t *sig_above, const uint64_t *sig_below, uint64_t epoch,
                                   uint32_t *sig_err, void *stream);
 
-/* Stream-ordered wait until the neighbours' signal word `word` (0 ready, 1 done)
- * is >= value: a rank about to overwrite its band's input rows after step e
- * enqueues sc_band_signal_wait(above, below, 1, e, err, stream) first. */
+/* Stream-ordered wait until the neighbours reached epoch `value`: word 0 = their
+ * launch of it started (ready), word 1 = it finished reading this band's rows
+ * (count >= value * per-launch target). A rank
+ * about to overwrite its band's input rows after step e enqueues
+ * sc_band_signal_wait(above, below, 1, e, err, stream) first. */
 int sc_band_signal_wait(const uint64_t *sig_above, const uint64_t *sig_below, int word, uint64_t value,
                         uint32_t *sig_err, void *stream);
 

@@ -17,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <algorithm>
 #include <array>
 #include <unistd.h>
 
@@ -84,7 +85,7 @@ static Knobs read_knobs() {
         else if (name == "NO_PDL") k.no_pdl = v;
         else if (name == "SPLIT_PASSES") k.split_passes = v;
         else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;
-        else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;  // test hook: as if the allocation failed
+        else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;
     }
     return k;
 }
@@ -669,6 +670,25 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+    }
+    if (p.epoch) {
+        // per-launch counts of the items that read the band above / below (each
+        // counts once when its copies have landed, kernels.cuh): every row band of
+        // the plan whose input rows leave src, times the (plane, strip) units
+        const long long units = (long long)j.nplanes * pl.nstrips;
+        unsigned long long na = 0, nb = 0;
+        auto count = [&](int lo, int hi, int bh) {
+            for (int y = lo; y < hi; y += bh) {
+                const int in_lo = std::max(std::max(y - rad, 0), (int)p.avail_lo);
+                const int in_hi = std::min(std::min(std::min(y + bh, hi) + rad, j.R), (int)p.avail_hi);
+                if (in_lo < j.src_row0) na += units;
+                if (in_hi > j.src_row0 + j.src_rows) nb += units;
+            }
+        };
+        if (pl.hi1 > pl.lo1) count(pl.lo1, pl.hi1, pl.band_h);
+        if (pl.hi2 > pl.lo2) count(pl.lo2, pl.hi2, pl.band_h2);
+        p.sig_n_above = na;
+        p.sig_n_below = nb;
     }
     cudaError_t e = cudaLaunchKernelExC(&cfg, kern, args);
     if (side) cudaFreeAsync(side, s);  // after the kernel, in stream order

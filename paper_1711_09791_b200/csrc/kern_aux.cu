@@ -163,11 +163,24 @@ cudaError_t launch_fill_synthetic(float* dst, long long count, uint64_t seed, ui
 // Stream-ordered wait for the neighbouring bands' signal words (a caller about to
 // overwrite its band's input rows waits until both neighbours are done reading
 // them, S/executors.py:142-151's launch barrier on the device).
+// word 0: the neighbours' launch of epoch `value` started (ready >= value);
+// word 1: it finished reading THIS band's rows -- the band above counts its
+// below-reading items in [3] (target [5] per launch), the band below its
+// above-reading items in [2] (target [4]).
 __global__ void signal_wait_kernel(const unsigned long long* a, const unsigned long long* b, int word,
                                    unsigned long long value, unsigned int* err, long long timeout_ns) {
     if (threadIdx.x != 0) return;
-    wait_signal(a ? a + word : nullptr, value, err, timeout_ns);
-    wait_signal(b ? b + word : nullptr, value, err, timeout_ns);
+    const unsigned long long* sides[2] = {a, b};
+    for (int s = 0; s < 2; ++s) {
+        const unsigned long long* w = sides[s];
+        if (!w) continue;
+        wait_signal(w, value, err, timeout_ns);  // the launch of that epoch has started: targets current
+        if (word == 1) {
+            const int cnt = s == 0 ? 3 : 2;
+            const unsigned long long target = value * ld_acquire_sys(w + cnt + 2);
+            wait_signal(w + cnt, target, err, timeout_ns);
+        }
+    }
 }
 
 cudaError_t launch_signal_wait(const unsigned long long* a, const unsigned long long* b, int word,

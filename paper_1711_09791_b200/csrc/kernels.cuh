@@ -67,6 +67,7 @@ constexpr int F_NO_RING = 0x2;
 constexpr int F_ZERO_FILL = 0x4;
 // tuning flags (set by the planner from SC_* environment variables)
 constexpr int F_STAGED_STORE = 0x200;  // unaligned kernels: dst rows not all 16-B aligned -> staged TMA stores
+constexpr int SIG_WORDS = 8;  // signal block: [0] ready, [2]/[3] done counts above/below, [4]/[5] per-launch targets
 constexpr int F_U8_LEAN = 0x400;  // u8 kernel: interior strips take the lean loops (large payloads)
 constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (default: evict_normal,
                                          // which lets neighbouring bands' halo rows hit in L2)
@@ -128,15 +129,21 @@ struct Params {
     // which measurably changes register allocation (fused 76 -> 84, unaligned 96 -> 102)
     int snap_lo, snap_hi;
     // Row-band readiness signalling between ranks (peer transport, epoch > 0):
-    // sig_self = this band's [ready epoch, done epoch, finished-CTA count] in its own
-    // device memory (mapped by the neighbours); sig_above / sig_below = the
-    // neighbours' words (peer-mapped, may be null). Every CTA publishes
-    // ready = epoch when it starts (its inputs are in place: stream order), waits
-    // until both neighbours published ready >= epoch before its first read or
-    // write (their halo rows are current; and a neighbour that started this step
-    // has finished the previous one, so buffers it read then may be overwritten),
-    // and the last CTA to finish publishes done = epoch. (ready is published by
-    // CTA 0 alone: the grid is resident, and nothing it waits for depends on it.) sig_err (host-mapped) is
+    // sig_self = this band's signal words in its own device memory (mapped by the
+    // neighbours): [0] ready epoch; [2] / [3] running counts of the items that
+    // have finished reading the band above / below; [4] / [5] how many items read
+    // it per launch (sig_n_above / sig_n_below, fixed by the plan). sig_above /
+    // sig_below = the neighbours' words (peer-mapped, may be null). CTA 0
+    // publishes ready = epoch when the grid starts (its inputs are in place:
+    // stream order; the grid is resident and nothing it waits for depends on
+    // it); every CTA waits until both neighbours published ready >= epoch before
+    // its first neighbour read or any write (their halo rows are current; and a
+    // neighbour that started this step has finished the previous one, so buffers
+    // it read then may be overwritten). "Done reading my rows" for epoch e is
+    // count >= e * n on the neighbour's side: each neighbour-reading item adds 1
+    // once its copies landed. Only those items (one band of strips at each end)
+    // count, early and late in the launch -- a per-launch counter that every CTA
+    // bumped at its end cost 4 us per step (measured), per-CTA done words 6 us. sig_err (host-mapped) is
     // set if a wait outlives sig_timeout_ns.
     unsigned long long* sig_self;
     const unsigned long long* sig_above;
@@ -144,6 +151,7 @@ struct Params {
     unsigned long long epoch;
     unsigned int* sig_err;
     long long sig_timeout_ns;
+    unsigned long long sig_n_above, sig_n_below;
 };
 
 // SC_TRACE (a dev-only build variant): per-CTA timeline of TRACE_SLOTS words.
@@ -199,6 +207,11 @@ __device__ __forceinline__ void mbar_fence_init() {
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Transaction count without an arrival: the phase also needs a later mbar_arrive.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t tx) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t tx) {
@@ -266,6 +279,13 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+// A system-scope count without a fence: used only after the counted reads have
+// COMPLETED (their mbarrier phase was waited, the data is in shared memory), so no
+// later write by the reader's neighbour can reach them; a release here stalled the
+// counting warp behind every earlier store of its item (+5 us per step, measured).
+__device__ __forceinline__ void red_add_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
@@ -469,14 +489,19 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
 #ifdef SC_TRACE
     int ntr = 0;
 #endif
-    if (p.epoch) {
-        // neighbours' rows current (and their previous step finished) before this
-        // CTA reads or writes anything; then order the async-proxy (TMA) reads
-        // after the acquire
+    // Row-band signalling: the neighbours' rows must be current (and their previous
+    // step finished) before this CTA reads a neighbour row or writes anything. The
+    // wait is deferred past the first stage's own-row copies: those are issued
+    // first with the stage's transaction count (no arrival), the wait overlaps
+    // their DRAM latency, and the producer's arrival -- after the wait -- is what
+    // releases the stage to the consumers, so no store precedes the wait.
+    bool waited = p.epoch == 0;
+    auto wait_neighbours = [&]() {
         wait_signal(p.sig_above, p.epoch, p.sig_err, p.sig_timeout_ns);
         wait_signal(p.sig_below, p.epoch, p.sig_err, p.sig_timeout_ns);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads after the acquire
+        waited = true;
+    };
     // The first item of every CTA is its own index (no atomic: 600-900 CTAs
     // claiming from one counter at launch serialise on it); later items come
     // from the ticket, offset by the grid size.
@@ -519,6 +544,7 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
             float* sbase = ring + slot * SROWS * SW + soff;
             sitem[slot] = item;
             if (snap_mode(MODE)) {
+                if (!waited) wait_neighbours();
                 // own rows: the item's own columns from the image (nobody else writes
                 // them), the 4-column halos from the column snapshot; halo rows (other
                 // bands' rows) wholly from the row snapshot
@@ -556,10 +582,21 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
                 }
             } else if (ALIGNED) {
                 const uint32_t bytes = (uint32_t)n * 4u;
-                mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
-                for (int k = 0; k < nrows; ++k)
-                    bulk_g2s(sbase + k * SW, src_row(p, it.plane, r0 + k) + cx0, bytes, &full[slot], pol);
+                if (!waited && r0 >= p.src_row0 && r0 + nrows <= p.src_row0 + p.src_rows) {
+                    // first stage, own rows only: copies first, the wait under them
+                    mbar_expect_tx(&full[slot], bytes * (uint32_t)nrows);
+                    for (int k = 0; k < nrows; ++k)
+                        bulk_g2s(sbase + k * SW, src_row(p, it.plane, r0 + k) + cx0, bytes, &full[slot], pol);
+                    wait_neighbours();
+                    mbar_arrive(&full[slot]);
+                } else {
+                    if (!waited) wait_neighbours();
+                    mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
+                    for (int k = 0; k < nrows; ++k)
+                        bulk_g2s(sbase + k * SW, src_row(p, it.plane, r0 + k) + cx0, bytes, &full[slot], pol);
+                }
             } else {
+                if (!waited) wait_neighbours();
                 // the segment [g, g+n) lands at the 16-B aligned smem index 4 + soff, preceded
                 // by its shift s = (g mod 16 B) / 4 floats: column c sits at c - x0 + 8 + s
                 uint32_t total = 0;
@@ -1005,6 +1042,13 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 
     for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
         if (r0 != it.in_lo) mbar_wait(&full[slot], phase);  // the item's first stage was waited by the caller
+        if (p.epoch && threadIdx.x == 32) {
+            // done accounting of the row-band signalling: this stage's copies have
+            // landed, so an item that read the band above (its first stage) or the
+            // band below (its last stage) has finished reading that neighbour
+            if (r0 == it.in_lo && it.in_lo < p.src_row0) red_add_relaxed_sys(p.sig_self + 2, 1ULL);
+            if (r0 + SROWS >= it.in_hi && it.in_hi > p.src_row0 + p.src_rows) red_add_relaxed_sys(p.sig_self + 3, 1ULL);
+        }
 #ifdef SC_TRACE
         if (threadIdx.x == 32 && gs < 8) SC_TR(p, 48 + gs, clock64());
 #endif
@@ -1249,7 +1293,13 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     // the previous kernel's tail; no global memory is touched before it completed
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // this band's inputs are in place (the previous grid completed): one CTA says so
-    if (p.epoch && threadIdx.x == 0 && blockIdx.x == 0) st_release_sys(p.sig_self, p.epoch);
+    if (p.epoch && threadIdx.x == 0 && blockIdx.x == 0) {
+        // per-epoch counts of the items that read the band above / below (fixed
+        // by the plan), ordered before ready by the release
+        p.sig_self[4] = p.sig_n_above;
+        p.sig_self[5] = p.sig_n_below;
+        st_release_sys(p.sig_self, p.epoch);
+    }
 
     if (warp == 0) {
 #ifdef SC_TRACE
@@ -1292,23 +1342,6 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
 #endif
     }
     if (!ALIGNED && threadIdx.x == 32) bulk_wait_all();  // staged rows fully stored before smem goes away
-    if (p.epoch) {
-        // done: every consumer of this CTA has stored its rows; the last CTA out
-        // publishes the epoch (the neighbours' reads of this band ended with their
-        // own kernels, which waited for this step's ready)
-        consumer_bar(ncw * 32);
-        if (threadIdx.x == 32) {
-            // GPU-scope ordering of this CTA's stores before its count; the last CTA
-            // (which observed every count) releases them all at system scope
-            __threadfence();
-            unsigned long long* cnt = p.sig_self + 2;
-            if (atomicAdd(cnt, 1ULL) == (unsigned long long)gridDim.x - 1) {
-                *cnt = 0;
-                __threadfence_system();
-                st_release_sys(p.sig_self + 1, p.epoch);
-            }
-        }
-    }
 #ifdef SC_TRACE
     if (threadIdx.x == 32) {
         SC_TR(p, 40, clock64());

@@ -303,6 +303,7 @@ class BandStepper:
 
 
 _COMMS: dict = {}
+SIG_WORDS = 8  # the band signal block (csrc/kernels.cuh SIG_WORDS)
 
 
 def nccl_comm(group=None, device: int | None = None) -> int:
@@ -494,9 +495,11 @@ class PeerBandStepper:
         if Rs != band.hi - band.lo or Rd != band.hi - band.lo or n2 != n or C2 != C:
             raise InvalidArgumentError("peer band buffers must hold exactly the owned rows")
         self.signal = bool(signal) and band.world > 1
-        # signal words: [ready, done, finished-CTA count] in this device's memory;
-        # the error word in pinned host memory (read by the host without a sync)
-        self.sig = torch.zeros(3, dtype=torch.int64, device=local_src.device)
+        # signal words (kernels.cuh: [0] ready, [2]/[3] done counts of the items
+        # that read the band above/below, [4]/[5] their per-launch targets) in this
+        # device's memory; the error word in pinned host memory (read by the host
+        # without a sync)
+        self.sig = torch.zeros(SIG_WORDS, dtype=torch.int64, device=local_src.device)
         self.err = torch.zeros(1, dtype=torch.int32).pin_memory()
         self.epoch = 0
         if band.world > 1:

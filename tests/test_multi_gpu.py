@@ -135,8 +135,8 @@ def test_peer_signal_waits_for_late_neighbour(env, oracle):
     src = torch.from_numpy(np.ascontiguousarray(x[:, lo:hi])).cuda()
     above = torch.from_numpy(np.ascontiguousarray(x[:, lo - 2:lo])).cuda()
     dst = torch.full((P, hi - lo, C), -1.0, device="cuda")
-    sig_self = torch.zeros(3, dtype=torch.int64, device="cuda")
-    nb, nb_ptr = _host_words(3)
+    sig_self = torch.zeros(multi.SIG_WORDS, dtype=torch.int64, device="cuda")
+    nb, nb_ptr = _host_words(multi.SIG_WORDS)
     errw = torch.zeros(1, dtype=torch.int32).pin_memory()
     want = oracle.two_pass(x, w)[:, lo:hi]
     for epoch in (1, 2):
@@ -156,7 +156,9 @@ def test_peer_signal_waits_for_late_neighbour(env, oracle):
         assert int(errw.item()) == 0
         assert bits_equal(dst.cpu().numpy(), want)
         s = sig_self.cpu().numpy()
-        assert s[0] == epoch and s[1] == epoch and s[2] == 0, s
+        # ready, and the done count of the items that read the band above: every
+        # launch adds its per-launch target (no band below here)
+        assert s[0] == epoch and s[4] > 0 and s[2] == epoch * s[4] and s[3] == 0 and s[5] == 0, s
 
 
 def test_peer_signal_timeout_flags_error(env, oracle, monkeypatch):
@@ -168,8 +170,8 @@ def test_peer_signal_timeout_flags_error(env, oracle, monkeypatch):
     src = torch.rand((P, hi - lo, C), device="cuda")
     above = torch.rand((P, 2, C), device="cuda")
     dst = torch.zeros_like(src)
-    sig_self = torch.zeros(3, dtype=torch.int64, device="cuda")
-    nb, nb_ptr = _host_words(3)  # never published
+    sig_self = torch.zeros(multi.SIG_WORDS, dtype=torch.int64, device="cuda")
+    nb, nb_ptr = _host_words(multi.SIG_WORDS)  # never published
     errw = torch.zeros(1, dtype=torch.int32).pin_memory()
     t0 = time.perf_counter()
     _lib.check(_peer_call(L, src, dst, above, lo, hi, R, C, P, w, sig_self.data_ptr(), nb_ptr, 5, errw.data_ptr()))
@@ -180,27 +182,38 @@ def test_peer_signal_timeout_flags_error(env, oracle, monkeypatch):
 
 def test_signal_wait_kernel(env):
     """sc_band_signal_wait: the stream waits (device side) until the neighbour's
-    done word reaches the value; work queued behind it runs after."""
+    launch of the epoch has started (ready) and, for done, until every CTA of it
+    has published done; work queued behind it runs after."""
     _lib, dev, multi = env
     L = _lib.load()
-    nb, nb_ptr = _host_words(3)
+    nb, nb_ptr = _host_words(multi.SIG_WORDS)
     errw = torch.zeros(1, dtype=torch.int32).pin_memory()
     marker = torch.zeros(1, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    for word in (0, 1):
+        nb.zero_()
 
-    def publish():
-        time.sleep(0.3)
-        nb[1] = 7
+        def publish():
+            time.sleep(0.2)
+            nb[5] = 3       # the neighbour above has 3 items per launch that read this band (its "below")
+            nb[0] = 7       # ... and started epoch 7
+            time.sleep(0.2)
+            nb[3] = 20      # epochs 1..6 counted, 2 of 3 items of epoch 7
+            time.sleep(0.1)
+            nb[3] = 21      # its last such item finished: 7 * 3
 
-    th = threading.Thread(target=publish)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    th.start()
-    _lib.check(L.sc_band_signal_wait(nb_ptr, None, 1, 7, errw.data_ptr(), torch.cuda.current_stream().cuda_stream))
-    marker.fill_(1.0)
-    torch.cuda.synchronize()
-    th.join()
-    assert time.perf_counter() - t0 >= 0.25
-    assert marker.item() == 1.0 and int(errw.item()) == 0
+        th = threading.Thread(target=publish)
+        marker.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        th.start()
+        _lib.check(L.sc_band_signal_wait(nb_ptr, None, word, 7, errw.data_ptr(), stream))
+        marker.fill_(1.0)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        th.join()
+        assert el >= (0.45 if word == 1 else 0.15), (word, el)
+        assert marker.item() == 1.0 and int(errw.item()) == 0
     with pytest.raises(Exception):
         _lib.check(L.sc_band_signal_wait(nb_ptr, None, 2, 7, None, None))
 

@@ -75,8 +75,10 @@ def main():
     L = _lib.load()
     above = dev.synthetic((P, 2, C), 6, 1)
     below = dev.synthetic((P, 2, C), 7, 1)
-    sig = torch.zeros(3, dtype=torch.int64, device="cuda")
-    nbr = torch.full((3,), 1 << 40, dtype=torch.int64, device="cuda")
+    from paper_1711_09791_b200.multi import SIG_WORDS
+
+    sig = torch.zeros(SIG_WORDS, dtype=torch.int64, device="cuda")
+    nbr = torch.full((SIG_WORDS,), 1 << 40, dtype=torch.int64, device="cuda")  # always "ready"
     err = torch.zeros(1, dtype=torch.int32).pin_memory()
     stream = torch.cuda.current_stream().cuda_stream
     epoch = [0]
@@ -90,6 +92,23 @@ def main():
 
     host_us, gpu_us = measure(peer_step, args.steps)
     out["peer_signalled"] = {"host_us_per_step": round(host_us, 2), "gpu_us_per_step": round(gpu_us, 2)}
+    # the same without neighbour words (no waits: only the ready store and the done count)
+    base_nowait = base[:-2] + (None, None)
+
+    def peer_step_nowait():
+        epoch[0] += 1
+        _lib.check(L.sc_two_pass_band_peer_sig_f32(*base_nowait, epoch[0], err.data_ptr(), stream))
+
+    host_us, gpu_us = measure(peer_step_nowait, args.steps)
+    out["peer_signalled_nowait"] = {"host_us_per_step": round(host_us, 2), "gpu_us_per_step": round(gpu_us, 2)}
+    # the plain peer call with the same neighbour rows (no signalling at all)
+    base_plain = base[:-3]
+
+    def peer_step_plain():
+        _lib.check(L.sc_two_pass_band_peer_f32(*base_plain, stream))
+
+    host_us, gpu_us = measure(peer_step_plain, args.steps)
+    out["peer_unsignalled_same_rows"] = {"host_us_per_step": round(host_us, 2), "gpu_us_per_step": round(gpu_us, 2)}
     solo = PeerBandStepper(src, dst, Band(0, 1, hi - lo, 2, 0, hi - lo), w)
     host_us, gpu_us = measure(solo.step, args.steps)
     out["peer_plain_call"] = {"host_us_per_step": round(host_us, 2), "gpu_us_per_step": round(gpu_us, 2)}
