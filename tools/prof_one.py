@@ -19,5 +19,7 @@ for _ in range(a.n):
     if a.op == "fused": dev.two_pass(x, w, y)
     elif a.op == "hpass": dev.hpass(x, w, y)
     elif a.op == "single": dev.single_pass(x, dense, y)
+    elif a.op == "inplace": dev.two_pass_inplace(x, w)
+    elif a.op == "split": dev.two_pass_split(x, y, w)
 torch.cuda.synchronize()
 print("done")
