@@ -315,7 +315,10 @@ class HostRegistry:
         import os
         from collections import OrderedDict
 
+        import threading
+
         self._regs = OrderedDict()  # root address -> (nbytes, finalizer)
+        self._lock = threading.RLock()  # finalizers may run on any thread (garbage collection)
         self.min_bytes = int(float(os.environ.get("SC_HOST_REGISTER_MIN_MB", "64")) * (1 << 20))
         try:
             phys = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
@@ -337,6 +340,10 @@ class HostRegistry:
         root = self._root(arr)
         if root.nbytes < self.min_bytes or not root.flags.owndata or root.base is not None:
             return False
+        with self._lock:
+            return self._pin_locked(root)
+
+    def _pin_locked(self, root) -> bool:
         key = root.ctypes.data
         if key in self._regs:
             self._regs.move_to_end(key)
@@ -362,18 +369,21 @@ class HostRegistry:
         _lib.load().sc_host_unregister(key)
 
     def _on_free(self, key):
-        item = self._regs.pop(key, None)
-        if item is not None:
-            self._release(key, item[0])
+        with self._lock:
+            item = self._regs.pop(key, None)
+            if item is not None:
+                self._release(key, item[0])
 
     def registered(self, arr) -> bool:
-        return isinstance(arr, np.ndarray) and self._root(arr).ctypes.data in self._regs
+        with self._lock:
+            return isinstance(arr, np.ndarray) and self._root(arr).ctypes.data in self._regs
 
     def clear(self):
-        for key, (n, fin) in list(self._regs.items()):
-            fin.detach()
-            self._release(key, n)
-        self._regs.clear()
+        with self._lock:
+            for key, (n, fin) in list(self._regs.items()):
+                fin.detach()
+                self._release(key, n)
+            self._regs.clear()
 
 
 host_registry = HostRegistry()
