@@ -564,13 +564,15 @@ def main():
         del img, scr
 
     # ---- N>1 row bands: the same steps with the OTHER halo transport (secondary)
+    # (only when the peer transport is the timed one: the NCCL plan then always
+    # exists, while a peer stepper built where peer access failed could leave the
+    # ranks out of step in its collectives)
     halo_alt = None
-    if band is not None and world > 1 and backend == "nccl" and halo in ("peer", "nccl"):
-        other = "nccl" if halo == "peer" else "peer"
+    if band is not None and world > 1 and backend == "nccl" and halo == "peer":
+        other = "nccl"
         alt = None
         try:
-            alt = (NcclBandStepper(src, dst, band, w) if other == "nccl" else
-                   PeerBandStepper(src, dst, band, w, signal=peer_signal))
+            alt = NcclBandStepper(src, dst, band, w)
             for _ in range(args.warmup):
                 alt.step()
             torch.cuda.synchronize()
