@@ -372,7 +372,9 @@ static int host_band(const HostJob& J) {
     std::vector<char> stage_src(J.nplanes), stage_dst(J.nplanes), stage_scr(J.nplanes);
     bool any_in = false, any_out = false;
     for (int p = 0; p < J.nplanes; ++p) {
-        stage_src[p] = pageable(J.src[p]) || J.halo_top || J.halo_bot;
+        // (the multi-device halo copies are small host vectors: their rows go by a
+        // plain pageable cudaMemcpyAsync, the band's own rows by DMA when they can)
+        stage_src[p] = pageable(J.src[p]);
         stage_dst[p] = pageable(J.dst[p]);
         stage_scr[p] = split && pageable(J.scr[p]);
         any_in |= stage_src[p] != 0;

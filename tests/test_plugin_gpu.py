@@ -225,3 +225,33 @@ def test_ladder_gpu_stages_through_reference_harness(sl, tmp_path):
     rows = [ln.split(",") for ln in path.read_text().splitlines()[1:]]
     assert {r[3] for r in rows if r[0].startswith("Gpu")} == {"cuda"}
     assert [r[0] for r in rows][:4] == ["Opt-0", "Opt-0", "Opt-2", "Opt-2"]
+
+
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+                                                                 HealthCheck.function_scoped_fixture])
+@given(rows=st.integers(5, 70), cols=st.integers(5, 90), planes=st.integers(1, 3), seed=st.integers(0, 2**20),
+       algo=st.sampled_from(["two-pass", "single-generic", "single-unrolled"]), copy=st.booleans(),
+       with_ws=st.booleans(), width=st.sampled_from([1, 3, 5, 7, 9, 11]), fused=st.booleans())
+def test_random_cuda_plan_equals_sequential(sl, rows, cols, planes, seed, algo, copy, with_ws, width, fused):
+    """Random images, taps and variants through the reference's own convolve_image:
+    the Cuda plan leaves the same bits as Sequential in the image AND the workspace
+    (T/test_executors.py:188-221, randomised like T/conftest.py:13-19)."""
+    if rows < width or cols < width or (algo == "single-unrolled" and width != 5):
+        return
+    rng = np.random.default_rng(seed)
+    k = sl.SeparableKernel(rng.uniform(-2, 2, size=width).astype(np.float32))
+    variant = sl.ConvVariant(sl.Algorithm(algo), copy_back=copy)
+    data = rng.uniform(-50, 300, size=(planes, rows, cols)).astype(np.float32)
+    ends = []
+    for plan in (sl.Sequential(), sl.Cuda(fused=fused)):
+        img = sl.Image([sl.Plane(data[p].copy()) for p in range(planes)])
+        ws = sl.Image([sl.Plane(np.full((rows, cols), -7.0, np.float32)) for _ in range(planes)]) if with_ws else None
+        sl.convolve_image(img, k, variant, plan, workspace=ws)
+        ends.append((stack(img), stack(ws) if ws is not None else None))
+    assert bits_equal(ends[1][0], ends[0][0])
+    if with_ws:
+        assert bits_equal(ends[1][1], ends[0][1])
