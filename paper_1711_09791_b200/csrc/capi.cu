@@ -496,7 +496,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     bool symw = !kn.no_sym && (j.mode == MODE_FUSED || j.mode == MODE_SPLITF) && j.taps;
     for (int i = 0; i < j.width && symw; ++i) symw = std::memcmp(&j.taps[i], &j.taps[j.width - 1 - i], sizeof(float)) == 0;
     switch (j.mode) {
-        case MODE_FUSED: kern = kernel_fused(rad, aligned, symw); break;
+        case MODE_FUSED: kern = kernel_fused(rad, aligned, symw, j.sig_self != nullptr); break;
         case MODE_HPASS: kern = kernel_hpass(rad, aligned); break;
         case MODE_VPASS: kern = kernel_vpass(rad, aligned); break;
         case MODE_SINGLE: kern = kernel_single(rad, aligned, sym); break;

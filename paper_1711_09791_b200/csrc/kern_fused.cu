@@ -6,12 +6,18 @@
 
 namespace sc {
 
-// symw: mirror-symmetric taps (w[j] == w[2r-j] bitwise): products shared by value
-const void* kernel_fused(int rad, bool aligned, bool symw) {
+// symw: mirror-symmetric taps (w[j] == w[2r-j] bitwise): products shared by value;
+// sig: the peer-band instantiation with the row-band readiness signalling
+const void* kernel_fused(int rad, bool aligned, bool symw, bool sig) {
     if (rad < 1) symw = false;
-#define SC_KF(R, S)                                                                      \
-    return aligned ? (const void*)sepconv_rows_kernel<MODE_FUSED, R, true, (R >= 1 ? S : 0)> \
-                   : (const void*)sepconv_rows_kernel<MODE_FUSED, R, false, (R >= 1 ? S : 0)>;
+#define SC_KF(R, S)                                                                                        \
+    {                                                                                                      \
+        if (sig)                                                                                           \
+            return aligned ? (const void*)sepconv_rows_kernel<MODE_FUSED, R, true, (R >= 1 ? S : 0), true>  \
+                           : (const void*)sepconv_rows_kernel<MODE_FUSED, R, false, (R >= 1 ? S : 0), true>; \
+        return aligned ? (const void*)sepconv_rows_kernel<MODE_FUSED, R, true, (R >= 1 ? S : 0)>           \
+                       : (const void*)sepconv_rows_kernel<MODE_FUSED, R, false, (R >= 1 ? S : 0)>;          \
+    }
 #define SC_K(R)                \
     case R:                    \
         if (symw) SC_KF(R, 1)  \

@@ -467,7 +467,7 @@ __device__ __forceinline__ const float* src_row(const Params& p, int plane, int 
 #define SC_STATIC_FIRST 1
 #endif
 
-template <int MODE, int RAD, bool ALIGNED>
+template <int MODE, int RAD, bool ALIGNED, bool SIG = false>
 __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t* full, uint64_t* empty,
                                          int* sitem, int* sshift) {
     // Items are claimed dynamically (atomic ticket), so CTAs that get more
@@ -495,7 +495,7 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
     // first with the stage's transaction count (no arrival), the wait overlaps
     // their DRAM latency, and the producer's arrival -- after the wait -- is what
     // releases the stage to the consumers, so no store precedes the wait.
-    bool waited = p.epoch == 0;
+    bool waited = !SIG || p.epoch == 0;  // SIG: the peer-signalled instantiation only
     auto wait_neighbours = [&]() {
         wait_signal(p.sig_above, p.epoch, p.sig_err, p.sig_timeout_ns);
         wait_signal(p.sig_below, p.epoch, p.sig_err, p.sig_timeout_ns);
@@ -990,7 +990,7 @@ __device__ __forceinline__ void publish_row(float* drow, const float* srow, int 
 // every group with one STG.128 and need no per-row column tests (measured: -2% at
 // cfg5 under the bench's sustained power cap, where issue slots are scarce; not
 // used by the single pass, whose register allocation it upset: cfg2 +13%).
-template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE, int SYM, bool COL_EDGE = true>
+template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE, int SYM, bool COL_EDGE = true, bool SIG = false>
 __device__ __forceinline__ void consume_item(const Params& p, const Item& it, const float* ring, uint64_t* full,
                                              uint64_t* empty, const int* sshift, float* stage_out, int& slot,
                                              uint32_t& phase, int& gs) {
@@ -1042,7 +1042,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 
     for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
         if (r0 != it.in_lo) mbar_wait(&full[slot], phase);  // the item's first stage was waited by the caller
-        if (p.epoch && threadIdx.x == 32) {
+        if (SIG && p.epoch && threadIdx.x == 32) {
             // done accounting of the row-band signalling: this stage's copies have
             // landed, so an item that read the band above (its first stage) or the
             // band below (its last stage) has finished reading that neighbour
@@ -1264,7 +1264,9 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 // ---------------------------------------------------------------------------
 // The kernel
 
-template <int MODE, int RAD, bool ALIGNED, int SYM = 0>
+// SIG: the row-band readiness signalling (Params::sig_*) is compiled in; only the
+// peer-band launches use it, so every other kernel carries none of its code.
+template <int MODE, int RAD, bool ALIGNED, int SYM = 0, bool SIG = false>
 #ifndef SC_MINB
 #define SC_MINB 1
 #endif
@@ -1293,7 +1295,7 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     // the previous kernel's tail; no global memory is touched before it completed
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // this band's inputs are in place (the previous grid completed): one CTA says so
-    if (p.epoch && threadIdx.x == 0 && blockIdx.x == 0) {
+    if (SIG && p.epoch && threadIdx.x == 0 && blockIdx.x == 0) {
         // per-epoch counts of the items that read the band above / below (fixed
         // by the plan), ordered before ready by the release
         p.sig_self[4] = p.sig_n_above;
@@ -1311,7 +1313,7 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
             SC_TR(p, 43, smid);
         }
 #endif
-        producer<MODE, RAD, ALIGNED>(p, ring, full, empty, sitem, sshift);
+        producer<MODE, RAD, ALIGNED, SIG>(p, ring, full, empty, sitem, sshift);
         return;
     }
 
@@ -1330,11 +1332,13 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
         if (item_rows_edge<MODE, RAD>(p, it))
-            consume_item<MODE, RAD, ALIGNED, true, SYM>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
+            consume_item<MODE, RAD, ALIGNED, true, SYM, true, SIG>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
+                                                                   gs);
         else if (single_like(MODE) || !ALIGNED || it.x0 < RAD || it.x0 + p.tw > p.C - RAD)
-            consume_item<MODE, RAD, ALIGNED, false, SYM>(p, it, ring, full, empty, sshift, stage_out, slot, phase, gs);
+            consume_item<MODE, RAD, ALIGNED, false, SYM, true, SIG>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
+                                                                    gs);
         else
-            consume_item<MODE, RAD, ALIGNED, false, SYM, false>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
+            consume_item<MODE, RAD, ALIGNED, false, SYM, false, SIG>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
                                                                 gs);
 #ifdef SC_TRACE
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 30 + ntr, clock64());

@@ -11,7 +11,7 @@ namespace sc {
 struct Params;
 
 // Kernel entry for (mode, radius, aligned); nullptr if unsupported.
-const void* kernel_fused(int rad, bool aligned, bool symw = false);
+const void* kernel_fused(int rad, bool aligned, bool symw = false, bool sig = false);
 const void* kernel_hpass(int rad, bool aligned);
 const void* kernel_vpass(int rad, bool aligned);
 const void* kernel_single(int rad, bool aligned, int sym = 0);  // sym: 0, 1 rows mirror, 2 rows+cols
