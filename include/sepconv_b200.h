@@ -279,6 +279,13 @@ int sc_two_pass_host_band_f32(const float *const *src_planes, float *const *dst_
 int sc_two_pass_host_multi_f32(const float *const *src_planes, float *const *dst_planes, int nplanes, int rows,
                                int cols, const float *taps, int width, int flags, const int *devices, int ndev);
 
+/* sc_two_pass_host_split_f32 over several GPUs from one process: the same row
+ * bands as sc_two_pass_host_multi_f32, each writing its image rows (ring
+ * untouched) and its workspace rows (H0); the reference's end state of both
+ * buffers, same bits as one device. */
+int sc_two_pass_host_multi_split_f32(float *const *image_planes, float *const *scratch_planes, int nplanes, int rows,
+                                     int cols, const float *taps, int width, int flags, const int *devices, int ndev);
+
 #ifdef __cplusplus
 }
 #endif

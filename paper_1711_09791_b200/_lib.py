@@ -68,6 +68,7 @@ EXPORTS = (
     "sc_host_unregister",
     "sc_two_pass_host_band_f32",
     "sc_two_pass_host_multi_f32",
+    "sc_two_pass_host_multi_split_f32",
     "sc_two_pass_u8hwc",
     "sc_hwc_u8_to_planes_f32",
     "sc_planes_f32_to_hwc_u8",
@@ -126,6 +127,7 @@ _SIGNATURES = {
     "sc_two_pass_host_split_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_two_pass_host_band_f32": ([_vp, _vp, _i32, _i32, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_two_pass_host_multi_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _i32], _i32),
+    "sc_two_pass_host_multi_split_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _i32], _i32),
     "sc_two_pass_u8hwc": ([_vp, _vp, _i32, _i32, _i64, _i64, _fp, _i32, _i32, _vp], _i32),
     "sc_hwc_u8_to_planes_f32": ([_vp, _vp, _i32, _i32, _i64, _i64, _i64, _vp], _i32),
     "sc_planes_f32_to_hwc_u8": ([_vp, _vp, _i32, _i32, _i64, _i64, _i64, _vp], _i32),

@@ -674,9 +674,9 @@ extern "C" int sc_two_pass_host_band_f32(const float* const* src_planes, float* 
 // 2r rows around every band boundary are copied aside on the host, so that in
 // place (dst == src) a band never reads halo rows its neighbour has already
 // overwritten. A device listed twice runs its bands one after the other.
-extern "C" int sc_two_pass_host_multi_f32(const float* const* src_planes, float* const* dst_planes, int nplanes,
-                                          int rows, int cols, const float* taps, int width, int flags,
-                                          const int* devices, int ndev) {
+static int host_multi(const float* const* src_planes, float* const* dst_planes, float* const* scr_planes,
+                      int nplanes, int rows, int cols, const float* taps, int width, int flags, const int* devices,
+                      int ndev) {
     set_error("");
     if (!devices || ndev < 1) {
         set_error("need at least one device");
@@ -690,7 +690,11 @@ extern "C" int sc_two_pass_host_multi_f32(const float* const* src_planes, float*
     // bands no shorter than r rows, so that a halo comes from the adjacent band only
     int nb = ndev;
     while (nb > 1 && rows / nb < (r > 1 ? r : 1)) --nb;
-    if (nb == 1) return sc_two_pass_host_f32(src_planes, dst_planes, nplanes, rows, cols, taps, width, flags, devices[0]);
+    if (nb == 1) {
+        HostJob j{src_planes, dst_planes, scr_planes, nplanes, rows, cols, 0, rows, taps, width, flags, devices[0],
+                  nullptr, nullptr};
+        return host_band(j);
+    }
     std::vector<int> lo(nb + 1);
     const int q = rows / nb, rem = rows % nb;
     for (int g = 0; g <= nb; ++g) lo[g] = g * q + (g < rem ? g : rem);
@@ -713,7 +717,7 @@ extern "C" int sc_two_pass_host_multi_f32(const float* const* src_planes, float*
             top[p] = g > 0 ? side_rows(g, p) : nullptr;                                // rows [lo-r, lo)
             bot[p] = g + 1 < nb ? side_rows(g + 1, p) + (size_t)r * cols : nullptr;  // rows [hi, hi+r)
         }
-        HostJob j{src_planes, dst_planes, nullptr, nplanes, rows, cols, lo[g], lo[g + 1], taps, width, flags,
+        HostJob j{src_planes, dst_planes, scr_planes, nplanes, rows, cols, lo[g], lo[g + 1], taps, width, flags,
                   devices[g % ndev], g > 0 && r > 0 ? top.data() : nullptr,
                   g + 1 < nb && r > 0 ? bot.data() : nullptr};
         rcs[g] = host_band(j);
@@ -730,4 +734,30 @@ extern "C" int sc_two_pass_host_multi_f32(const float* const* src_planes, float*
         }
     set_error("");
     return SC_OK;
+}
+
+// One process, several GPUs (the reference's single-process plan model): the
+// image is split into ndev row bands by the reference's balanced block split
+// (S/executors.py:121-139); every band streams through its own GPU (and PCIe
+// link) concurrently, one host thread per device. Before any device starts, the
+// 2r rows around every band boundary are copied aside on the host, so that in
+// place (dst == src) a band never reads halo rows its neighbour has already
+// overwritten. A device listed twice runs its bands one after the other.
+extern "C" int sc_two_pass_host_multi_f32(const float* const* src_planes, float* const* dst_planes, int nplanes,
+                                          int rows, int cols, const float* taps, int width, int flags,
+                                          const int* devices, int ndev) {
+    return host_multi(src_planes, dst_planes, nullptr, nplanes, rows, cols, taps, width, flags, devices, ndev);
+}
+
+// The same with the reference's workspace end state (sc_two_pass_host_split_f32
+// per band: the image ring untouched, H0 into the workspace rows of each band).
+extern "C" int sc_two_pass_host_multi_split_f32(float* const* image_planes, float* const* scratch_planes,
+                                                int nplanes, int rows, int cols, const float* taps, int width,
+                                                int flags, const int* devices, int ndev) {
+    if (!scratch_planes) {
+        set_error("null workspace planes");
+        return SC_INVALID_ARGUMENT;
+    }
+    return host_multi(image_planes, image_planes, scratch_planes, nplanes, rows, cols, taps, width,
+                      (flags & SC_EXTENDED) | SC_NO_RING, devices, ndev);
 }

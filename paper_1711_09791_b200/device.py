@@ -451,11 +451,12 @@ def two_pass_host(src_planes, dst_planes, taps, *, extended: bool = False, ring:
 
 
 def two_pass_host_split(image_planes, scratch_planes, taps, *, extended: bool = False, device: int = 0,
-                        register: bool = True) -> None:
+                        register: bool = True, devices=None) -> None:
     """The reference's end state of convolve_image(TWO_PASS) with a workspace, on HOST
     planes (S/executors.py:303-326): scratch_planes := H0 (zero outside the row
     pass's rows and columns), image_planes[valid] := V(H0) in place, image ring
-    untouched. Streamed through the GPU like two_pass_host; blocks until done."""
+    untouched. Streamed through the GPU like two_pass_host; blocks until done.
+    devices: row bands through several GPUs from this process, same bits."""
     w = _taps(taps)
     image_planes, scratch_planes = list(image_planes), list(scratch_planes)
     if register:
@@ -466,9 +467,18 @@ def two_pass_host_split(image_planes, scratch_planes, taps, *, extended: bool = 
     if not ptrs_img or len(ptrs_img) != len(ptrs_scr):
         raise InvalidArgumentError("need matching, non-empty image and workspace plane lists")
     L = _lib.load()
+    flags = _lib.SC_EXTENDED if extended else 0
+    if devices is not None and len(list(devices)) > 1:
+        devs = [int(d) for d in devices]
+        arr_dev = (ctypes.c_int * len(devs))(*devs)
+        _lib.check(L.sc_two_pass_host_multi_split_f32(_ptr_array(ptrs_img), _ptr_array(ptrs_scr), len(ptrs_img),
+                                                      shape[0], shape[1], _fp(w), w.size, flags,
+                                                      ctypes.cast(arr_dev, ctypes.c_void_p), len(devs)))
+        return
+    if devices is not None and len(list(devices)) == 1:
+        device = int(list(devices)[0])
     _lib.check(L.sc_two_pass_host_split_f32(_ptr_array(ptrs_img), _ptr_array(ptrs_scr), len(ptrs_img), shape[0],
-                                            shape[1], _fp(w), w.size, _lib.SC_EXTENDED if extended else 0,
-                                            int(device)))
+                                            shape[1], _fp(w), w.size, flags, int(device)))
 
 
 def two_pass_host_band(src_rows, dst_rows, taps, *, global_rows: int, row0: int, out_lo: int, out_hi: int,

@@ -202,7 +202,8 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
             dev.two_pass_host(img_planes, img_planes, taps, device=device_index, devices=plan.devices,
                               register=plan.register_host)
         elif two_pass:
-            dev.two_pass_host_split(img_planes, ws_planes, taps, device=device_index, register=plan.register_host)
+            dev.two_pass_host_split(img_planes, ws_planes, taps, device=device_index, register=plan.register_host,
+                                    devices=plan.devices)
         else:
             with torch.cuda.device(device_index):
                 src = torch.stack([torch.from_numpy(a) for a in img_planes]).cuda()

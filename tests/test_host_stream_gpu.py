@@ -316,3 +316,32 @@ def test_convolve_image_register_host_same_bits(dev, oracle):
 
         assert host_registry.registered(buf) == reg
         host_registry.clear()
+
+
+@pytest.mark.parametrize("ndev", [2, 3, 5])
+@pytest.mark.parametrize("kind", ["pageable", "pinned"])
+def test_host_multi_device_split(dev, oracle, small_chunks, ndev, kind):
+    """Several GPUs from one process (the same device listed ndev times here) with
+    the reference's workspace end state: row bands, halo rows copied aside first,
+    in place -- both buffers bit-identical to the oracle."""
+    w = np.array([-1, -2, 7, -2, -1], np.float32)
+    R, C = 203, 260
+    x = oracle.synthetic(3 * R * C, 77, kind=2).reshape(3, R, C)
+    img = planes_of(x, kind)
+    scr = planes_of(np.full_like(x, 4.0), kind)
+    dev.two_pass_host_split(img, scr, w, devices=[0] * ndev)
+    assert bits_equal(as_np(img), oracle.two_pass(x, w))
+    assert bits_equal(as_np(scr), oracle.two_pass_scratch(x, w))
+
+
+def test_convolve_image_devices_with_workspace(dev, oracle):
+    import paper_1711_09791_b200 as sc
+
+    w = np.array([1, 4, 6, 4, 1], np.float32) / np.float32(16)
+    x = oracle.synthetic(3 * 150 * 300, 8, kind=1).reshape(3, 150, 300)
+    img = sc.Image([sc.Plane(p.copy()) for p in x])
+    ws = sc.Image([sc.Plane(np.full((150, 300), 2.0, np.float32)) for _ in range(3)])
+    sc.convolve_image(img, sc.SeparableKernel(w), sc.ConvVariant(sc.Algorithm.TWO_PASS), sc.Cuda(devices=[0, 0, 0]),
+                      workspace=ws)
+    assert bits_equal(np.stack([p.data for p in img.planes]), oracle.two_pass(x, w))
+    assert bits_equal(np.stack([p.data for p in ws.planes]), oracle.two_pass_scratch(x, w))
