@@ -680,6 +680,43 @@ def main():
                if (world == 1 or band is None) else
                "sc_two_pass_host_band_f32 per rank (its row band + halo rows from its pinned host copy, chunked "
                "H2D/kernel/D2H on 3 streams)"}
+        if band is not None and world == 1:
+            # the PCIe floor of this step on this box: the same planes' plain pinned
+            # H2D alone and D2H alone (one cudaMemcpyAsync per plane, CUDA events);
+            # the duplex step cannot beat the slower direction
+            def copy_ms(fn):
+                fn()
+                torch.cuda.synchronize()
+                a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_ev.record(stream)
+                fn()
+                b_ev.record(stream)
+                torch.cuda.synchronize()
+                return a_ev.elapsed_time(b_ev)
+
+            scratch_dev = torch.empty_like(src)
+            h2d_ms = copy_ms(lambda: [scratch_dev[p].copy_(host[p], non_blocking=True) for p in range(P)])
+            d2h_ms = copy_ms(lambda: [host[p].copy_(scratch_dev[p], non_blocking=True) for p in range(P)])
+            # both directions at once (the step's real floor: the link is not fully duplex)
+            back = [torch.empty((R, C), dtype=torch.float32, pin_memory=True) for _ in range(P)]
+            s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
+
+            def duplex():
+                for p in range(P):
+                    with torch.cuda.stream(s_up):
+                        scratch_dev[p].copy_(host[p], non_blocking=True)
+                    with torch.cuda.stream(s_down):
+                        back[p].copy_(src[p], non_blocking=True)
+
+            duplex()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            duplex()
+            torch.cuda.synchronize()
+            dup_ms = (time.perf_counter() - t0) * 1e3
+            del scratch_dev, back
+            e2e.update({"pcie_h2d_alone_ms": round(h2d_ms, 3), "pcie_d2h_alone_ms": round(d2h_ms, 3),
+                        "pcie_duplex_ms": round(dup_ms, 3), "frac_of_pcie_duplex": round(dup_ms / e_ms, 4)})
 
     # ---- end to end as a sepconv_lab user makes the call: the reference's own
     # convolve_image with the Cuda plan (plugin.py) on its numpy (PAGEABLE) planes,
