@@ -787,6 +787,8 @@ def main():
                                        "ms_per_step": round(m_ms, 3),
                                        "path": f"Cuda(devices=range({ndev})): sc_two_pass_host_multi_f32"}
         del img, pg
+        if sl is not None:
+            plugin.uninstall()  # the CPU baseline below runs the unmodified reference
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
