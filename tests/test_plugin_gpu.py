@@ -255,3 +255,17 @@ def test_random_cuda_plan_equals_sequential(sl, rows, cols, planes, seed, algo, 
     assert bits_equal(ends[1][0], ends[0][0])
     if with_ws:
         assert bits_equal(ends[1][1], ends[0][1])
+
+
+def test_cli_ladder_with_gpu_stages(sl, tmp_path):
+    """`sepconv ladder --stages Opt-2,Gpu-2,...` (S/cli.py:229-256) through the plugin's
+    entry point: the reference's harness checks and times the GPU stages and writes
+    them in its CSV with plan "cuda"."""
+    r = _run(["-m", "paper_1711_09791_b200.plugin", "ladder", "--sizes", "48x64,64x64", "--reps", "2",
+              "--workers", "2", "--cutoff", "3", "--stages", "Opt-0,Opt-2,Gpu-0,Gpu-1-nocopy,Gpu-2",
+              "--csv", "out.csv"], tmp_path)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = [ln.split(",") for ln in (tmp_path / "out.csv").read_text().splitlines()[1:]]
+    gpu = [row for row in rows if row[0].startswith("Gpu")]
+    assert len(gpu) == 6 and {row[3] for row in gpu} == {"cuda"}
+    assert all(row[13] for row in rows)  # speedups against Opt-0 filled in
