@@ -234,3 +234,40 @@ def test_peer_stepper_world_one_unsignalled(env, oracle):
     torch.cuda.synchronize()
     assert bits_equal(dst.cpu().numpy(), oracle.two_pass(x, w))
     st.close()
+
+
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+                                                                 HealthCheck.function_scoped_fixture])
+@given(P=st.integers(1, 3), R=st.integers(20, 90), C=st.integers(9, 200), width=st.sampled_from([3, 5, 7, 9]),
+       cut=st.floats(0.1, 0.9), frac=st.floats(0.2, 0.8), top=st.booleans(), bot=st.booleans(),
+       seed=st.integers(0, 2**20), extended=st.booleans())
+def test_random_nccl_plan_self_exchange(env, oracle, P, R, C, width, cut, frac, top, bot, seed, extended):
+    """Random bands, widths, shapes (aligned or not) and edges through the NCCL plan
+    with a self-exchanging one-rank communicator: bit-exact vs the oracle on the
+    image whose halo rows are the band's own boundary rows."""
+    _lib, dev, multi = env
+    r = width // 2
+    lo = int(cut * R) if top else 0
+    hi = min(R, lo + max(r, int(frac * R))) if bot else R
+    if top and lo < r or bot and hi + r > R or hi - lo < r or (not top and lo != 0) or (not bot and hi != R):
+        return
+    if R < width or C < width:
+        return
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(-2, 2, size=width).astype(np.float32)
+    x = rng.uniform(-100, 300, size=(P, R, C)).astype(np.float32)
+    band = multi.Band(0, 1, R, r, lo, hi)
+    src = torch.from_numpy(np.ascontiguousarray(x[:, lo:hi])).cuda()
+    dst = torch.full((P, hi - lo, C), -1.0, device="cuda")
+    st_ = multi.NcclBandStepper(src, dst, band, w, extended=extended, comm=multi.nccl_comm(None, 0),
+                                rank_above=0 if top else -1, rank_below=0 if bot else -1)
+    try:
+        st_.step()
+        torch.cuda.synchronize()
+        assert bits_equal(dst.cpu().numpy(), self_halo_expected(oracle, x, lo, hi, w, top, bot, extended=extended))
+    finally:
+        st_.close()
