@@ -330,6 +330,11 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
             }
             // padding columns + the 8-column halo of every strip
             double cost = (double)(strips * tw_ + 2 * HALO * strips) / j.C;
+            // the in-place two-pass (split / no scratch) also snapshots 8 columns around
+            // every strip boundary (written, then read back): wider strips pay
+            // (measured at cfg5: 1024-column strips -3%; cfg3 -3%). Not for the
+            // single pass + copy-back, whose plan it moved the wrong way (+3.5%).
+            if (j.mode == MODE_SPLITF) cost += 16.0 * (strips - 1) / j.C;
             int head = 0, bh = shrt;
             if (seg2) {
                 cost *= (double)(bh_short + 2 * rad) / bh_short;

@@ -25,7 +25,8 @@ x = dev.synthetic(shape, wl.seed, wl.kind)
 y = torch.empty_like(x)
 dense = np.outer(w, w).astype(np.float32)
 op = {"fused": lambda: dev.two_pass(x, w, y), "single": lambda: dev.single_pass(x, dense, y),
-      "hpass": lambda: dev.hpass(x, w, y), "vpass": lambda: dev.vpass(x, w, y)}[a.op]
+      "hpass": lambda: dev.hpass(x, w, y), "vpass": lambda: dev.vpass(x, w, y),
+      "inplace": lambda: dev.two_pass_inplace(x, w), "split": lambda: dev.two_pass_split(x, y, w)}[a.op]
 KEYS = ["SC_NS", "SC_OCC", "SC_NT", "SC_BAND_H", "SC_BAND_H2", "SC_TAIL_WAVES", "SC_EXACT_WAVES", "SC_L2_EVICT_FIRST", "SC_IPC"]
 def run(env):
     for k in KEYS: os.environ.pop(k, None)
