@@ -56,6 +56,7 @@ struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
     int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
     int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0, peer_timeout_ms = 0;
+    int u8_occ2 = 0;
 };
 
 static Knobs read_knobs() {
@@ -86,6 +87,7 @@ static Knobs read_knobs() {
         else if (name == "SPLIT_PASSES") k.split_passes = v;
         else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;
         else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;
+        else if (name == "U8_OCC2") k.u8_occ2 = v;  // small u8 payloads on the 2-CTA build
     }
     return k;
 }
@@ -714,7 +716,10 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
     const int rad = width / 2;
     bool symw = !read_knobs().no_sym;  // mirror-symmetric taps: shared products (bit-identical)
     for (int i = 0; i < width && symw; ++i) symw = std::memcmp(&taps[i], &taps[width - 1 - i], sizeof(float)) == 0;
-    const void* kern = kernel_u8(rad, symw);
+    // payloads below 32 Mpixel: the 3-CTA build (<= 128 consumer threads)
+    const bool large = (long long)R * C >= (1LL << 25);
+    const bool occ3 = !large && u8_occ3_fits(rad, symw) && !read_knobs().u8_occ2;
+    const void* kern = kernel_u8(rad, symw, occ3);
     if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(width));
     U8Params p;
     std::memset(&p, 0, sizeof(p));
@@ -727,7 +732,7 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
     p.hrow_lo = (flags & SC_EXTENDED) ? 0 : rad;
     p.hrow_hi = (flags & SC_EXTENDED) ? R : R - rad;
     p.flags = flags;
-    if ((long long)R * C >= (1LL << 25)) p.flags |= F_U8_LEAN;  // >= 32 Mpixel: the lean loops pay
+    if (large) p.flags |= F_U8_LEAN;  // >= 32 Mpixel: the lean loops pay
     p.one = 1.0f;
     for (int i = 0; i < width; ++i) p.w[i] = taps[i];
     // 4 columns per consumer thread; strips of TW = 4*nt columns, nt minimising padding
@@ -735,6 +740,7 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
     int nt = 128;
     long long best = -1;
     for (int c : cand) {
+        if (occ3 && c > 128) continue;  // the 3-CTA build is bounded to 160 threads
         const long long tw = 4LL * c, waste = ((C + tw - 1) / tw) * tw - C;
         if (best < 0 || waste < best) { best = waste; nt = c; }
     }

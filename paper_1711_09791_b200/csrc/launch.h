@@ -22,7 +22,9 @@ const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);
 const void* kernel_single_direct(int rad);
 
-const void* kernel_u8(int rad, bool symw = false);
+const void* kernel_u8(int rad, bool symw = false, bool occ3 = false);
+// whether the 3-CTA (128-register) u8 build holds this radius without spilling
+bool u8_occ3_fits(int rad, bool symw);
 cudaError_t launch_hwc_to_planes(const uint8_t* src, float* dst, long long srs, long long dps, long long drs, int R,
                                  int C, cudaStream_t s);
 cudaError_t launch_planes_to_hwc(const float* src, uint8_t* dst, long long sps, long long srs, long long drs, int R,
