@@ -223,7 +223,9 @@ int sc_fill_synthetic_f32(float *dst, int64_t count, uint64_t seed, uint64_t off
  * sc_two_pass_u8hwc: read_ppm -> two-pass -> write_ppm fused, i.e. the bytes the
  * reference writes after convolve_image(TWO_PASS) on read_ppm(src)
  * (S/ppm.py:72-73, S/executors.py:308-326, S/ppm.py:87-89: rint half-even,
- * clip 0..255). Needs cols % 16 == 0 and 16-B aligned src rows, 4-B aligned dst. */
+ * clip 0..255). Taps of width 1..9; any cols, row strides and byte offsets
+ * (16-B aligned src rows with cols % 16 == 0 and a 4-B aligned dst run the
+ * aligned build, anything else the general build: same bytes). */
 int sc_two_pass_u8hwc(const uint8_t *src, uint8_t *dst, int rows, int cols, int64_t src_row_stride,
                       int64_t dst_row_stride, const float *taps, int width, int flags, void *stream);
 /* u8 HWC -> 3 float32 planes (read_ppm_bytes, S/ppm.py:72-73). */

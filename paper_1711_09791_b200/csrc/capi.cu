@@ -57,6 +57,7 @@ struct Knobs {
     int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
     int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0, peer_timeout_ms = 0;
     int u8_occ2 = 0;
+    int u8_gen = 0;
 };
 
 static Knobs read_knobs() {
@@ -88,6 +89,7 @@ static Knobs read_knobs() {
         else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;
         else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;
         else if (name == "U8_OCC2") k.u8_occ2 = v;  // small u8 payloads on the 2-CTA build
+        else if (name == "U8_GEN") k.u8_gen = v;    // the general-geometry u8 build on aligned rows too
     }
     return k;
 }
@@ -714,12 +716,17 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
 int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long drs, int R, int C, const float* taps,
                    int width, int flags, cudaStream_t s) {
     const int rad = width / 2;
-    bool symw = !read_knobs().no_sym;  // mirror-symmetric taps: shared products (bit-identical)
+    const Knobs kn = read_knobs();
+    bool symw = !kn.no_sym;  // mirror-symmetric taps: shared products (bit-identical)
     for (int i = 0; i < width && symw; ++i) symw = std::memcmp(&taps[i], &taps[width - 1 - i], sizeof(float)) == 0;
     // payloads below 32 Mpixel: the 3-CTA build (<= 128 consumer threads)
     const bool large = (long long)R * C >= (1LL << 25);
-    const bool occ3 = !large && u8_occ3_fits(rad, symw) && !read_knobs().u8_occ2;
-    const void* kern = kernel_u8(rad, symw, occ3);
+    const bool occ3 = !large && u8_occ3_fits(rad, symw) && !kn.u8_occ2;
+    // rows the TMA can copy as they are (16-B aligned, whole 16-B multiples) and
+    // 4-B aligned destination rows; anything else runs the general build
+    const bool gen = (C % 16) || (srs % 16) || (drs % 4) || (reinterpret_cast<uintptr_t>(src) & 15) ||
+                     (reinterpret_cast<uintptr_t>(dst) & 3) || kn.u8_gen;
+    const void* kern = kernel_u8(rad, symw, occ3, gen);
     if (!kern) return fail(SC_UNSUPPORTED_WIDTH, "no kernel for width " + std::to_string(width));
     U8Params p;
     std::memset(&p, 0, sizeof(p));
@@ -746,13 +753,13 @@ int launch_rows_u8(const uint8_t* src, uint8_t* dst, long long srs, long long dr
     }
     p.tw = 4 * nt;
     p.nstrips = (C + p.tw - 1) / p.tw;
-    const Knobs kn = read_knobs();
+    p.rowb = 3 * (p.tw + 2 * U8_HALO) + (gen ? 32 : 0);  // GEN: up to 15 bytes of 16-B widening each side
     int ns = kn.ns ? kn.ns : 4;
     if (ns < 3) ns = 3;
     if (ns > 32) ns = 32;
     p.ns = ns;
     const int threads = 32 + nt;
-    const size_t smem = (size_t)((2 * ns * 8 + ns * 4 + 127) / 128) * 128 + (size_t)ns * 4 * 3 * (p.tw + 32);
+    const size_t smem = (size_t)((2 * ns * 8 + ns * 4 + 127) / 128) * 128 + (size_t)ns * U8_SROWS * p.rowb;
     int dev = 0;
     cudaGetDevice(&dev);
     const DevInfo di = dev_info(dev);

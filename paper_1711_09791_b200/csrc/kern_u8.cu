@@ -82,7 +82,59 @@ __device__ __forceinline__ void pack12(const F4 (&outv)[3], uint32_t (&w)[3]) {
 // stages whose rows all exist and emit skip the per-row range tests. Used for
 // large payloads only (F_U8_LEAN, set on the host): measured 16384^2 0.709 ->
 // 0.605 ms, 8192^2 0.200 -> 0.183, but 4096^2 +6% and 2048^2 +17%.
-template <int RAD, bool EDGE, bool SYMW, bool COLEDGE = true>
+// (address of the staged row's logical byte 0, column x0 - U8_HALO, of row y) mod 16
+__device__ __forceinline__ uint32_t u8_row_shift(const uint8_t* base, int y, long long stride, int x0) {
+    return ((uint32_t)reinterpret_cast<uintptr_t>(base) + (uint32_t)y * (uint32_t)stride + 3u * (uint32_t)x0 -
+            3u * (uint32_t)U8_HALO) & 15u;
+}
+
+// The output of a thread whose 4 columns touch the column ring or the image edge:
+// ring columns keep the input byte of row yo (the pixel ring equals the input),
+// staged RAD rows back in the ring. `words`: whole 4-byte stores are allowed
+// (destination aligned, all 4 columns inside the image).
+template <int RAD, bool GEN = false>
+__device__ __forceinline__ void u8_store_edge(const U8Params& p, const uint8_t* ring, const uint32_t (&w3)[3],
+                                              uint8_t* drow, int slot, int k, int NS, int SWB, int x0, int x4, int ct,
+                                              int yo, int C, bool ring_copy, bool words) {
+    uint32_t ob[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) ob[i] = (w3[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+    int rr = slot * U8_SROWS + k - RAD;
+    if (rr < 0) rr += NS * U8_SROWS;
+    const uint32_t shr = GEN ? u8_row_shift(p.src, yo, p.srs, x0) : 0u;
+    const uint8_t* yrow = ring + rr * SWB + shr + 12 * ct + 3 * U8_HALO;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int col = x4 + c;
+        if (col < RAD || col >= C - RAD) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) ob[3 * c + q] = ring_copy ? yrow[3 * c + q] : 0xFFFFFFFFu;
+        }
+    }
+    if (words && ring_copy && x4 + 4 <= C) {
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(drow);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) d32[i] = ob[4 * i] | (ob[4 * i + 1] << 8) | (ob[4 * i + 2] << 16) | (ob[4 * i + 3] << 24);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int col = x4 + c;
+            if (col >= C) break;
+            if (ring_copy || (col >= RAD && col < C - RAD))
+#pragma unroll
+                for (int q = 0; q < 3; ++q) drow[3 * c + q] = (uint8_t)ob[3 * c + q];
+        }
+    }
+}
+
+// GEN: any row geometry (cols % 16 != 0, rows or buffers not 16-B aligned). The
+// producer widens each row's copy to whole 16-byte blocks and places it so the
+// row's logical byte 0 (column x0 - U8_HALO) sits `sh` = its address mod 16 bytes
+// into the staged row; consumers read their 36-byte window through funnel shifts
+// and, on rows whose destination is not 4-byte aligned, store whole aligned words
+// made from their own bytes and the next lane's head bytes (shuffled), with single
+// bytes only at warp ends and next to column-edge threads.
+template <int RAD, bool EDGE, bool SYMW, bool COLEDGE = true, bool GEN = false>
 __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, uint64_t* full, uint64_t* empty,
                                         int SWB, int x0, int ylo, int yhi, int in_lo, int in_hi, int& slot,
                                         uint32_t& phase, int& gs) {
@@ -113,10 +165,21 @@ __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, 
                 const int yi = r0 + k;
                 if (!FAST && yi >= in_hi) break;
                 // 12 columns x 3 planes = 36 bytes at byte 12*ct + 36 of the staged row
-                const uint8_t* srow = ring + (slot * U8_SROWS + k) * SWB + 12 * ct + 3 * (U8_HALO - 4);
+                const uint32_t sh = GEN ? u8_row_shift(p.src, yi, p.srs, x0) : 0u;
+                const uint8_t* srow = ring + (slot * U8_SROWS + k) * SWB + sh + 12 * ct + 3 * (U8_HALO - 4);
                 uint32_t wd[9];
+                if constexpr (GEN) {
+                    const uint32_t* a = reinterpret_cast<const uint32_t*>(srow - (sh & 3u));
+                    const uint32_t s8 = 8u * (sh & 3u);
+                    uint32_t t[10];
     #pragma unroll
-                for (int i = 0; i < 9; ++i) wd[i] = reinterpret_cast<const uint32_t*>(srow)[i];
+                    for (int i = 0; i < 10; ++i) t[i] = a[i];
+    #pragma unroll
+                    for (int i = 0; i < 9; ++i) wd[i] = __funnelshift_r(t[i], t[i + 1], s8);
+                } else {
+    #pragma unroll
+                    for (int i = 0; i < 9; ++i) wd[i] = reinterpret_cast<const uint32_t*>(srow)[i];
+                }
                 const bool live = !EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
                 const int yo = yi - RAD;
                 const bool emit = FAST || (yo >= emit_lo && yo < emit_hi);
@@ -144,7 +207,34 @@ __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, 
                     }
                     outv[q] = col_fold<RAD, NACC, SYMW>(acc[q], v, p.w, p.one);
                 }
-                if (emit && (!COLEDGE || x4 < C)) {
+                const bool mine = !COLEDGE || x4 < C;
+                uint32_t dsh = 0;  // the output row's misalignment (GEN only), uniform across the CTA
+                if constexpr (GEN) dsh = ((uint32_t)reinterpret_cast<uintptr_t>(p.dst) + (uint32_t)yo * (uint32_t)p.drs) & 3u;
+                if (GEN && emit && dsh) {
+                    // words at drow - dsh + 4k; word 0 is the previous lane's, word 3 takes
+                    // the next lane's first 4 - dsh bytes when that lane stores words too
+                    uint32_t w3[3];
+                    pack12(outv, w3);
+                    uint8_t* drow = p.dst + (long long)yo * p.drs + 3LL * x4;
+                    const bool fs = fast && mine;
+                    const uint32_t nx = __shfl_down_sync(0xFFFFFFFFu, w3[0], 1);
+                    const bool nfs = __shfl_down_sync(0xFFFFFFFFu, (int)fs, 1) && lane != 31;
+                    const bool pfs = __shfl_up_sync(0xFFFFFFFFu, (int)fs, 1) && lane != 0;
+                    const uint32_t s8 = 8u * (4u - dsh);
+                    if (fs) {
+                        uint32_t* q = reinterpret_cast<uint32_t*>(drow - dsh);
+                        q[1] = __funnelshift_r(w3[0], w3[1], s8);
+                        q[2] = __funnelshift_r(w3[1], w3[2], s8);
+                        if (nfs)
+                            q[3] = __funnelshift_r(w3[2], nx, s8);
+                        else
+                            for (int b = 12 - (int)dsh; b < 12; ++b) drow[b] = (uint8_t)(w3[b >> 2] >> (8 * (b & 3)));
+                        if (!pfs)
+                            for (int b = 0; b < 4 - (int)dsh; ++b) drow[b] = (uint8_t)(w3[0] >> (8 * b));
+                    } else if (mine) {
+                        u8_store_edge<RAD, GEN>(p, ring, w3, drow, slot, k, NS, SWB, x0, x4, ct, yo, C, ring_copy, false);
+                    }
+                } else if (emit && mine) {
                     uint32_t w3[3];
                     pack12(outv, w3);
                     uint8_t* drow = p.dst + (long long)yo * p.drs + 3LL * x4;
@@ -153,42 +243,14 @@ __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, 
     #pragma unroll
                         for (int i = 0; i < 3; ++i) d32[i] = w3[i];
                     } else {
-                        // ring columns keep the input byte of row yo (pixel ring == input)
-                        uint32_t ob[12];
-    #pragma unroll
-                        for (int i = 0; i < 12; ++i) ob[i] = (w3[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-                        int rr = slot * U8_SROWS + k - RAD;
-                        if (rr < 0) rr += NS * U8_SROWS;
-                        const uint8_t* yrow = ring + rr * SWB + 12 * ct + 3 * U8_HALO;
-    #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const int col = x4 + c;
-                            if (col < RAD || col >= C - RAD) {
-    #pragma unroll
-                                for (int q = 0; q < 3; ++q) ob[3 * c + q] = ring_copy ? yrow[3 * c + q] : 0xFFFFFFFFu;
-                            }
-                        }
-                        if (ring_copy && x4 + 4 <= C) {
-                            uint32_t* d32 = reinterpret_cast<uint32_t*>(drow);
-    #pragma unroll
-                            for (int i = 0; i < 3; ++i)
-                                d32[i] = ob[4 * i] | (ob[4 * i + 1] << 8) | (ob[4 * i + 2] << 16) | (ob[4 * i + 3] << 24);
-                        } else {
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                const int col = x4 + c;
-                                if (col >= C) break;
-                                if (ring_copy || (col >= RAD && col < C - RAD))
-    #pragma unroll
-                                    for (int q = 0; q < 3; ++q) drow[3 * c + q] = (uint8_t)ob[3 * c + q];
-                            }
-                        }
+                        u8_store_edge<RAD, GEN>(p, ring, w3, drow, slot, k, NS, SWB, x0, x4, ct, yo, C, ring_copy,
+                                                true);
                     }
                 }
                 if (EDGE && ring_copy && yi >= ylo && yi < yhi && (yi < RAD || yi >= R - RAD) && x4 < C) {
                     // ring rows: the input bytes unchanged
                     uint8_t* drow = p.dst + (long long)yi * p.drs + 3LL * x4;
-                    const uint8_t* irow = ring + (slot * U8_SROWS + k) * SWB + 12 * ct + 3 * U8_HALO;
+                    const uint8_t* irow = ring + (slot * U8_SROWS + k) * SWB + sh + 12 * ct + 3 * U8_HALO;
                     const int nb = 3 * min(4, C - x4);
                     for (int b = 0; b < nb; ++b) drow[b] = irow[b];
                 }
@@ -220,7 +282,7 @@ __device__ __forceinline__ void u8_item(const U8Params& p, const uint8_t* ring, 
 // threads and 3 CTAs per SM (128 registers instead of 146, no spills): measured
 // 2048^2 -4.5%, 4096^2 -5%; on large payloads the 2-CTA build stays ahead (8192^2
 // +5%, 16384^2 +2.5% with OCC3), so the host picks by size.
-template <int RAD, bool SYMW, bool OCC3 = false>
+template <int RAD, bool SYMW, bool OCC3 = false, bool GEN = false>
 __global__ void __launch_bounds__(OCC3 ? 160 : SC_U8_MAXT, OCC3 ? 3 : SC_U8_MINB)
     sepconv_u8_kernel(const __grid_constant__ U8Params p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -229,7 +291,7 @@ __global__ void __launch_bounds__(OCC3 ? 160 : SC_U8_MAXT, OCC3 ? 3 : SC_U8_MINB
     uint64_t* empty = full + NS;
     int* sitem = reinterpret_cast<int*>(empty + NS);
     uint8_t* ring = smem_raw + ((2 * NS * 8 + NS * 4 + 127) / 128) * 128;
-    const int SWB = 3 * (p.tw + 2 * U8_HALO);  // bytes per staged row
+    const int SWB = p.rowb;  // bytes per staged row (3 * (tw + 2 * U8_HALO), + 32 for GEN)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ncw = (blockDim.x >> 5) - 1;
     const int units = p.nstrips;
@@ -283,10 +345,28 @@ __global__ void __launch_bounds__(OCC3 ? 160 : SC_U8_MAXT, OCC3 ? 3 : SC_U8_MINB
                 if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
                 const int nrows = min(U8_SROWS, in_hi - r0);
                 sitem[slot] = item;
-                mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
-                for (int k = 0; k < nrows; ++k)
-                    bulk_g2s(ring + (slot * U8_SROWS + k) * SWB + soff, p.src + (long long)(r0 + k) * p.srs + 3LL * cx0,
-                             bytes, &full[slot], pol);
+                if constexpr (GEN) {
+                    // whole 16-byte blocks around each row's bytes: every block holds a
+                    // payload byte, so the widened read stays inside mapped pages
+                    uint32_t tot = 0;
+                    for (int k = 0; k < nrows; ++k) {
+                        const uintptr_t g0 = reinterpret_cast<uintptr_t>(p.src + (long long)(r0 + k) * p.srs + 3LL * cx0);
+                        tot += (uint32_t)(((g0 + bytes + 15) & ~(uintptr_t)15) - (g0 & ~(uintptr_t)15));
+                    }
+                    mbar_arrive_expect_tx(&full[slot], tot);
+                    for (int k = 0; k < nrows; ++k) {
+                        const uintptr_t g0 = reinterpret_cast<uintptr_t>(p.src + (long long)(r0 + k) * p.srs + 3LL * cx0);
+                        const uintptr_t a0 = g0 & ~(uintptr_t)15, a1 = (g0 + bytes + 15) & ~(uintptr_t)15;
+                        const uint32_t sh = ((uint32_t)g0 - (uint32_t)soff) & 15u;
+                        bulk_g2s(ring + (slot * U8_SROWS + k) * SWB + ((sh + (uint32_t)soff) & ~15u),
+                                 reinterpret_cast<const uint8_t*>(a0), (uint32_t)(a1 - a0), &full[slot], pol);
+                    }
+                } else {
+                    mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nrows);
+                    for (int k = 0; k < nrows; ++k)
+                        bulk_g2s(ring + (slot * U8_SROWS + k) * SWB + soff,
+                                 p.src + (long long)(r0 + k) * p.srs + 3LL * cx0, bytes, &full[slot], pol);
+                }
                 if (++slot == NS) { slot = 0; phase ^= 1u; }
             }
         }
@@ -304,11 +384,13 @@ __global__ void __launch_bounds__(OCC3 ? 160 : SC_U8_MAXT, OCC3 ? 3 : SC_U8_MINB
         // interior items (every input row live, no ring rows) run the lean loop
         const bool edge = in_lo < p.hrow_lo || in_hi > p.hrow_hi || ylo < RAD || yhi > p.R - RAD;
         if (edge)
-            u8_item<RAD, true, SYMW>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
+            u8_item<RAD, true, SYMW, true, GEN>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
         else if (RAD >= 4 || !(p.flags & F_U8_LEAN) || x0 < RAD || x0 + p.tw > p.C - RAD)
-            u8_item<RAD, false, SYMW>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
+            u8_item<RAD, false, SYMW, true, GEN>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase,
+                                                 gs);
         else if constexpr (RAD < 4)  // r = 4 with the lean variant spills
-            u8_item<RAD, false, SYMW, false>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase, gs);
+            u8_item<RAD, false, SYMW, false, GEN>(p, ring, full, empty, SWB, x0, ylo, yhi, in_lo, in_hi, slot, phase,
+                                                  gs);
     }
 }
 
@@ -341,20 +423,28 @@ __global__ void planes_to_hwc_kernel(const float* __restrict__ src, uint8_t* __r
 bool u8_occ3_fits(int rad, bool symw) { return rad <= 1 || (rad == 2 && symw); }
 
 // symw: mirror-symmetric taps (w[j] == w[2r-j] bitwise): products shared by value
-const void* kernel_u8(int rad, bool symw, bool occ3) {
-#define SC_U8K(R, S) (occ3 ? (const void*)sepconv_u8_kernel<R, S, true> : (const void*)sepconv_u8_kernel<R, S, false>)
+template <bool GEN>
+static const void* kernel_u8_t(int rad, bool symw, bool occ3) {
+#define SC_U8K(R, S) \
+    (occ3 ? (const void*)sepconv_u8_kernel<R, S, true, GEN> : (const void*)sepconv_u8_kernel<R, S, false, GEN>)
+#define SC_U8K2(R, S) ((const void*)sepconv_u8_kernel<R, S, false, GEN>)
     switch (rad) {
         case 0: return SC_U8K(0, false);
         case 1: return symw ? SC_U8K(1, true) : SC_U8K(1, false);
         // r = 2 without shared products and r >= 3: the 3-CTA build would spill
         // (u8_occ3_fits); the 2-CTA build only
-        case 2: return symw ? SC_U8K(2, true) : (const void*)sepconv_u8_kernel<2, false>;
-        case 3: return symw ? (const void*)sepconv_u8_kernel<3, true> : (const void*)sepconv_u8_kernel<3, false>;
+        case 2: return symw ? SC_U8K(2, true) : SC_U8K2(2, false);
+        case 3: return symw ? SC_U8K2(3, true) : SC_U8K2(3, false);
         // r = 4 with shared products spills (the products of 5 distinct taps stay live)
-        case 4: return (const void*)sepconv_u8_kernel<4, false>;
+        case 4: return SC_U8K2(4, false);
         default: return nullptr;
     }
 #undef SC_U8K
+#undef SC_U8K2
+}
+
+const void* kernel_u8(int rad, bool symw, bool occ3, bool gen) {
+    return gen ? kernel_u8_t<true>(rad, symw, occ3) : kernel_u8_t<false>(rad, symw, occ3);
 }
 
 static int grid_cap(long long total, int threads) {
@@ -416,9 +506,6 @@ extern "C" int sc_two_pass_u8hwc(const uint8_t* src, uint8_t* dst, int rows, int
     if (width > MAX_W) return u8_fail(3, "kernel width > 9 not supported");
     if (rows < width || cols < width) return u8_fail(2, "image smaller than kernel width");
     if (src_row_stride < 3LL * cols || dst_row_stride < 3LL * cols) return u8_fail(1, "row stride shorter than a row");
-    if (cols % 16 || src_row_stride % 16 || dst_row_stride % 16 || (reinterpret_cast<uintptr_t>(src) & 15) ||
-        (reinterpret_cast<uintptr_t>(dst) & 3))
-        return u8_fail(1, "fused u8 path needs cols % 16 == 0, 16-B aligned rows (use unpack / two_pass / pack)");
     if (!dev_ptr(src) || !dev_ptr(dst)) return u8_fail(1, "buffer is not device memory");
     const long long ns = (long long)(rows - 1) * src_row_stride + 3LL * cols;
     const long long nd = (long long)(rows - 1) * dst_row_stride + 3LL * cols;

@@ -185,6 +185,7 @@ struct U8Params {
     int hrow_lo, hrow_hi;
     int flags;
     int tw, nstrips, band_h, nitems, ns;
+    int rowb;  // bytes per staged row in the ring
     float w[MAX_W];
     float one;
     int* work;

@@ -22,7 +22,8 @@ const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);
 const void* kernel_single_direct(int rad);
 
-const void* kernel_u8(int rad, bool symw = false, bool occ3 = false);
+// gen: any row geometry (cols % 16 != 0, rows or buffers not 16-B aligned)
+const void* kernel_u8(int rad, bool symw = false, bool occ3 = false, bool gen = false);
 // whether the 3-CTA (128-register) u8 build holds this radius without spilling
 bool u8_occ3_fits(int rad, bool symw);
 cudaError_t launch_hwc_to_planes(const uint8_t* src, float* dst, long long srs, long long dps, long long drs, int R,

@@ -561,8 +561,10 @@ def planes_to_hwc(src: torch.Tensor, out: torch.Tensor | None = None) -> torch.T
 def two_pass_u8hwc(src: torch.Tensor, taps, out: torch.Tensor | None = None, *,
                    extended: bool = False) -> torch.Tensor:
     """read_ppm -> two-pass -> write_ppm on a (R, C, 3) uint8 payload: one fused
-    kernel when cols % 16 == 0 (3 B/pixel each way); otherwise unpack, fused
-    float two-pass and pack, all on the GPU. Same output bytes either way."""
+    kernel (3 B/pixel each way) for taps of width 1..9 and any row geometry (odd
+    cols, padded or unaligned rows: the kernel's general build); wider taps run
+    unpack, fused float two-pass and pack, all on the GPU. Same output bytes
+    either way."""
     w = _taps(taps)
     R, C, srs = _hwc(src, "src")
     if out is None:
@@ -572,8 +574,7 @@ def two_pass_u8hwc(src: torch.Tensor, taps, out: torch.Tensor | None = None, *,
         raise InvalidArgumentError("source and destination dimensions differ")
     flags = _lib.SC_EXTENDED if extended else 0
     L = _lib.load()
-    if C % 16 == 0 and srs % 16 == 0 and drs % 16 == 0 and src.data_ptr() % 16 == 0 and out.data_ptr() % 4 == 0 \
-            and w.size <= 9:  # the fused u8 kernel covers widths 1..9; wider taps take the planes path
+    if w.size <= 9:  # the fused u8 kernel covers widths 1..9; wider taps take the planes path
         _lib.check(L.sc_two_pass_u8hwc(src.data_ptr(), out.data_ptr(), R, C, srs, drs, _fp(w), w.size, flags,
                                        _stream(src)))
         return out

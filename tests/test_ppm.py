@@ -134,3 +134,79 @@ def test_fused_u8_subnormal_taps(key):
     planes = np.stack([p.data for p in read_ppm_bytes(data).planes])
     got = dev.two_pass(torch.from_numpy(planes).cuda(), z[f"taps_{key}"]).cpu().numpy()
     assert np.array_equal(got.view(np.uint32), z[f"planes_out_{key}"].view(np.uint32))
+
+
+def _u8_view(torch, R, C, pad, off, seed):
+    """(R, C, 3) uint8 view `off` bytes into a buffer, rows `3C + pad` bytes apart."""
+    srs = 3 * C + pad
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    buf = torch.randint(0, 256, (off + R * srs + 64,), dtype=torch.uint8, device="cuda", generator=g)
+    return buf, buf.as_strided((R, C, 3), (srs, 3, 1), off)
+
+
+# (rows, cols, source row padding, source offset, destination row padding, destination offset)
+_GEOMETRIES = [(9, 9, 0, 0, 0, 0), (37, 17, 0, 1, 0, 0), (64, 33, 5, 3, 0, 1), (23, 127, 0, 7, 2, 2),
+               (130, 1001, 1, 13, 3, 3), (75, 1921, 0, 0, 0, 0), (48, 640, 7, 0, 0, 0), (48, 640, 0, 0, 1, 0),
+               (33, 2050, 0, 15, 0, 3), (520, 517, 2, 5, 1, 1)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("geom", _GEOMETRIES, ids=lambda g: "x".join(map(str, g)))
+def test_fused_u8_any_geometry(geom):
+    """The fused u8 kernel's general build (cols % 16 != 0, padded rows, rows and
+    buffers at any byte offset): the same bytes as unpack -> fused f32 -> pack, for
+    every tap width 1..9 (mirror-symmetric and not), in both ring modes, and no
+    byte outside the destination view touched."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_09791_b200 import device as dev
+
+    R, C, spad, soff, dpad, doff = geom
+    _, src = _u8_view(torch, R, C, spad, soff, R * 7 + C)
+    rng = np.random.default_rng(R + C)
+    taps = [np.array([1.0], np.float32), np.array([0.25, 0.5, 0.25], np.float32),
+            np.float32([1, 4, 6, 4, 1]) / np.float32(16), np.float32([-1, -2, 7, -2, -1]),
+            rng.standard_normal(7).astype(np.float32), np.float32([1, 2, 3, 4, 5, 4, 3, 2, 1]) / np.float32(25),
+            rng.uniform(-0.5, 1, 9).astype(np.float32)]
+    for w in taps:
+        if w.size > min(R, C):
+            continue
+        for extended in (False, True):
+            dbuf, dst = _u8_view(torch, R, C, dpad, doff, 99)
+            before = dbuf.clone()
+            dev.two_pass_u8hwc(src, w, dst, extended=extended)
+            ref = dev.planes_to_hwc(dev.two_pass(dev.hwc_to_planes(src), w, extended=extended))
+            assert torch.equal(dst, ref), (w.size, extended)
+            mask = torch.ones_like(dbuf, dtype=torch.bool)
+            mask.as_strided((R, C, 3), (3 * C + dpad, 3, 1), doff).fill_(False)
+            assert torch.equal(dbuf[mask], before[mask]), "bytes outside the view were written"
+
+
+@pytest.mark.gpu
+def test_fused_u8_general_build_on_aligned_rows_and_large_payloads():
+    """SC_U8_GEN=1 forces the general build on aligned rows (it must equal the
+    aligned build), and a >= 32 Mpixel payload with odd cols runs the general
+    build's lean loops."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import os
+
+    from paper_1711_09791_b200 import device as dev
+
+    w = np.float32([1, 4, 6, 4, 1]) / np.float32(16)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    src = torch.randint(0, 256, (1080, 1920, 3), dtype=torch.uint8, device="cuda", generator=g)
+    want = dev.two_pass_u8hwc(src, w)
+    os.environ["SC_U8_GEN"] = "1"
+    try:
+        got = dev.two_pass_u8hwc(src, w)
+    finally:
+        del os.environ["SC_U8_GEN"]
+    assert torch.equal(got, want)
+    _, big = _u8_view(torch, 4097, 8195, 1, 3, 21)  # 33.6 Mpixel
+    for taps in (w, np.float32([0.1, -0.3, 0.9, 0.2, 0.1])):
+        fused = dev.two_pass_u8hwc(big, taps)
+        ref = dev.planes_to_hwc(dev.two_pass(dev.hwc_to_planes(big), taps))
+        assert torch.equal(fused, ref)
