@@ -19,6 +19,7 @@ for _ in range(a.n):
     if a.op == "fused": dev.two_pass(x, w, y)
     elif a.op == "hpass": dev.hpass(x, w, y)
     elif a.op == "single": dev.single_pass(x, dense, y)
+    elif a.op == "single_general": dev.single_pass(x, np.random.default_rng(2).standard_normal((5, 5)).astype(np.float32), y)
     elif a.op == "inplace": dev.two_pass_inplace(x, w)
     elif a.op == "split": dev.two_pass_split(x, y, w)
 torch.cuda.synchronize()
