@@ -264,7 +264,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     }
     const DevInfo di = dev_info(dev);
     const int occ_cap = kn.occ;
-    const int lags = (rad + SROWS - 1) / SROWS > 0 ? (rad + SROWS - 1) / SROWS : 1;
+    const int lags = stage_lags(j.mode, rad);
     int ns_req = kn.ns ? kn.ns : 16 / SROWS;
     if (ns_req < lags + 2) ns_req = lags + 2;
     if (ns_req > 32) ns_req = 32;

@@ -395,6 +395,10 @@ __device__ __forceinline__ void st4(float* p, const F4& a) {
 #define SC_SROWS 4
 #endif
 constexpr int SROWS = SC_SROWS;
+// stages a consumer holds back after finishing one (see consume_item)
+__host__ __device__ constexpr int stage_lags(int mode, int rad) {
+    return mode == MODE_FUSED ? ((rad + SROWS - 1) / SROWS > 0 ? (rad + SROWS - 1) / SROWS : 1) : 0;
+}
 __host__ __device__ constexpr int groups_of(int mode) { return single_like(mode) ? SC_GROUPS_SINGLE : SC_GROUPS; }
 
 // Shared-memory row width (floats): the segment [x0-4, x0+TW+4), plus room for
@@ -1249,9 +1253,12 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 #ifdef SC_TRACE
         if (threadIdx.x == 32 && gs < 8) SC_TR(p, 56 + gs, clock64());
 #endif
-        // this stage is done; release the one LAGS stages back (rows up to RAD back
-        // are still read for the ring columns)
-        constexpr int LAGS = (RAD + SROWS - 1) / SROWS > 0 ? (RAD + SROWS - 1) / SROWS : 1;
+        // this stage is done; release the one LAGS stages back: the fused two-pass
+        // still reads rows up to RAD back for the ring columns, every other mode
+        // hands its stage straight back (one more stage of prefetch from the same
+        // ring; ncu on the single pass: 9% of the consumers' samples were waits
+        // for a full stage with a 3-stage ring)
+        constexpr int LAGS = stage_lags(MODE, RAD);
         if (gs >= LAGS) {
             int rel = slot - LAGS;
             if (rel < 0) rel += NS;
