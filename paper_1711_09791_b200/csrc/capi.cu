@@ -270,7 +270,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     if (ns_req > 32) ns_req = 32;
     auto smem_for = [&](int tw_, int ns_) {
         const int sw = aligned ? tw_ + 2 * HALO : tw_ + 2 * HALO + 16;  // row_width<ALIGNED>
-        const size_t staging = aligned ? 0 : (size_t)2 * SROWS * (tw_ + 8) * 4;  // unaligned output staging
+        const size_t staging = (aligned || SC_LANES) ? 0 : (size_t)2 * SROWS * (tw_ + 8) * 4;  // SC_LANES=0: output staging
         return (size_t)((2 * ns_ * 8 + ns_ * 4 + ns_ * SROWS * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * sw * 4 +
                staging;
     };

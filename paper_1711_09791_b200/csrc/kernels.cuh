@@ -394,6 +394,9 @@ __device__ __forceinline__ void st4(float* p, const F4& a) {
 #ifndef SC_SROWS
 #define SC_SROWS 4
 #endif
+#ifndef SC_LANES
+#define SC_LANES 1  // unaligned rows: the lane-strided consumer (0: adjacent columns + realignment)
+#endif
 constexpr int SROWS = SC_SROWS;
 // stages a consumer holds back after finishing one (see consume_item)
 __host__ __device__ constexpr int stage_lags(int mode, int rad) {
@@ -1270,6 +1273,248 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 }
 
 // ---------------------------------------------------------------------------
+// Consumer for rows of ANY alignment (ALIGNED false: cols % 4 != 0, views whose
+// rows do not start on 16-B boundaries, either side): lane-strided columns.
+//
+// Thread (warp q, lane l) owns columns 128q + l + 32i (i = 0..3) of each of its
+// groups instead of 4 adjacent ones. Every shared-memory read is then an LDS.32
+// whose 32 lanes hit 32 consecutive words -- conflict-free whatever the row's
+// shift -- so the window needs no realignment (the adjacent-column layout pays 26
+// selects per row for it), every packed operand pair (columns c, c+32) is formed
+// by the loads themselves (no odd-pair moves), and every store is an STG.32 whose
+// warp writes 128 contiguous bytes at any destination alignment (no staging rows,
+// no shuffles, no per-warp edge columns). Same products, same sums, same order
+// per column as everywhere else: bit-identical.
+// Measured on B200 (3 x 16384^2 views offset by one float, tools/misalign_probe.py;
+// odd sizes, tools/generic_perf.py): see DESIGN.md section 6.
+
+template <int RAD, bool SYMW>
+__device__ __forceinline__ float2 row_pass_pair(const float2 (&X)[2 * RAD + 1], const float* w, float2 one2) {
+    float2 acc = __fmul2_rn(X[0], make_float2(w[0], w[0]));
+#pragma unroll
+    for (int m = 1; m <= 2 * RAD; ++m) {
+        const int t = tap_ix<RAD, SYMW>(m);
+        acc = add2p(acc, __fmul2_rn(X[m], make_float2(w[t], w[t])), one2);
+    }
+    return acc;
+}
+
+template <int RAD, int NACC, bool SYMW>
+__device__ __forceinline__ float2 col_fold_pair(float2 (&acc)[NACC], float2 v, const float* w, float2 one2) {
+    if (RAD == 0) return __fmul2_rn(v, make_float2(w[0], w[0]));
+    constexpr int jl = tap_ix<RAD, SYMW>(2 * RAD);
+    const float2 out = mad2(acc[NACC - 1], v, make_float2(w[jl], w[jl]), one2);
+#pragma unroll
+    for (int j = NACC - 1; j >= 1; --j) {
+        const int jj = tap_ix<RAD, SYMW>(j);
+        acc[j] = mad2(acc[j - 1], v, make_float2(w[jj], w[jj]), one2);
+    }
+    acc[0] = __fmul2_rn(v, make_float2(w[0], w[0]));
+    return out;
+}
+
+// ROWSYM: K[i][j] == K[2r-i][j] bitwise (see dense_fold_sym): rows i and 2r-i share their products
+template <int RAD, int NACC, bool ROWSYM>
+__device__ __forceinline__ float2 dense_fold_pair(float2 (&acc)[NACC], const float2 (&X)[2 * RAD + 1], const float* k,
+                                                  float2 one2) {
+    constexpr int W = 2 * RAD + 1;
+    if (RAD == 0) return __fmul2_rn(X[0], make_float2(k[0], k[0]));
+    float2 pr[RAD + 1][W];  // products of kernel rows 0..RAD
+#pragma unroll
+    for (int i = 0; i <= RAD; ++i)
+#pragma unroll
+        for (int j = 0; j < W; ++j) pr[i][j] = __fmul2_rn(X[j], make_float2(k[i * W + j], k[i * W + j]));
+    auto prod = [&](int i, int j) {
+        if (i <= RAD) return pr[i][j];
+        if (ROWSYM) return pr[W - 1 - i][j];
+        return __fmul2_rn(X[j], make_float2(k[i * W + j], k[i * W + j]));
+    };
+    float2 t = acc[NACC - 1];
+#pragma unroll
+    for (int j = 0; j < W; ++j) t = add2p(t, prod(W - 1, j), one2);
+    const float2 out = t;
+#pragma unroll
+    for (int i = NACC - 1; i >= 1; --i) {
+        t = acc[i - 1];
+#pragma unroll
+        for (int j = 0; j < W; ++j) t = add2p(t, prod(i, j), one2);
+        acc[i] = t;
+    }
+    t = pr[0][0];
+#pragma unroll
+    for (int j = 1; j < W; ++j) t = add2p(t, pr[0][j], one2);
+    acc[0] = t;
+    return out;
+}
+
+template <int MODE, int RAD, bool ROW_EDGE, int SYM, bool SIG = false>
+__device__ __forceinline__ void consume_item_lanes(const Params& p, const Item& it, const float* ring, uint64_t* full,
+                                                   uint64_t* empty, const int* sshift, int& slot, uint32_t& phase,
+                                                   int& gs) {
+    static_assert(!snap_mode(MODE), "in-place modes run aligned rows only");
+    constexpr int W = 2 * RAD + 1;
+    constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
+    constexpr int GROUPS = groups_of(MODE);
+    constexpr bool SYMW = !single_like(MODE) && SYM != 0;
+    constexpr int LAGS = stage_lags(MODE, RAD);
+    const int SW = row_width<false>(p.tw);
+    const int NS = p.ns;
+    const int ct = threadIdx.x - 32;
+    const int lane = threadIdx.x & 31;
+    const int tw2 = p.tw / GROUPS;  // column offset between a thread's groups
+    const int R = p.R, C = p.C;
+    const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);
+    const bool zero_fill = (MODE == MODE_HPASS) && (p.flags & F_ZERO_FILL);
+    const float2 one2 = make_float2(p.one, p.one);
+
+    // column tests do not depend on the row: bit 4g + i of `inside` (column exists)
+    // and `valid` (column outside the column ring)
+    int rel[GROUPS];
+    unsigned inside = 0, valid = 0;
+#pragma unroll
+    for (int g = 0; g < GROUPS; ++g) {
+        rel[g] = g * tw2 + 4 * (ct & ~31) + lane;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int col = it.x0 + rel[g] + 32 * i;
+            if (col < C) inside |= 1u << (4 * g + i);
+            if (col >= RAD && col < C - RAD) valid |= 1u << (4 * g + i);
+        }
+    }
+    float* dplane = p.dst + (long long)it.plane * p.dst_plane_stride + it.x0;
+
+    int emit_lo, emit_hi;
+    if (MODE == MODE_HPASS) {
+        emit_lo = it.ylo;
+        emit_hi = it.yhi;
+    } else {
+        emit_lo = max(max(it.ylo, RAD), it.in_lo + RAD);
+        emit_hi = min(it.yhi, R - RAD);
+    }
+    float* dcur = dplane + (long long)(emit_lo - p.dst_row0) * p.dst_row_stride;
+
+    float2 acc[GROUPS][2][NACC];
+#pragma unroll
+    for (int g = 0; g < GROUPS; ++g)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int j = 0; j < NACC; ++j) acc[g][q][j] = make_float2(0.0f, 0.0f);
+
+    for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
+        if (r0 != it.in_lo) mbar_wait(&full[slot], phase);  // the item's first stage was waited by the caller
+        if (SIG && p.epoch && threadIdx.x == 32) {
+            if (r0 == it.in_lo && it.in_lo < p.src_row0) red_add_relaxed_sys(p.sig_self + 2, 1ULL);
+            if (r0 + SROWS >= it.in_hi && it.in_hi > p.src_row0 + p.src_rows) red_add_relaxed_sys(p.sig_self + 3, 1ULL);
+        }
+        // column x0 of ring row rr sits at ring[rr * SW + 8 + sshift[rr]] (producer)
+        int sh[SROWS];
+#pragma unroll
+        for (int k = 0; k < SROWS; ++k) sh[k] = sshift[slot * SROWS + k];
+        const float* sstage = ring + slot * SROWS * SW + 8;
+        auto stage_rows = [&](auto fast_stage) {
+            constexpr bool FAST = decltype(fast_stage)::value;
+#pragma unroll
+            for (int k = 0; k < SROWS; ++k) {
+                const int yi = r0 + k;
+                if (FAST || yi < it.in_hi) {
+                    const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
+                    const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
+                    const bool emit = FAST || (yo >= emit_lo && yo < emit_hi);
+                    const float* srow = sstage + k * SW + sh[k];
+                    const bool ring_row = ROW_EDGE && ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD);
+#pragma unroll
+                    for (int g = 0; g < GROUPS; ++g) {
+                        // a warp whose columns all lie right of the image has nothing to store
+                        if (it.x0 + rel[g] - lane >= C) continue;
+                        const float* s = srow + rel[g];
+                        float2 outv[2], own[2];
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            float2 X[W];
+                            if (MODE == MODE_VPASS) {
+                                own[q] = make_float2(s[64 * q], s[64 * q + 32]);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < W; ++j) X[j] = make_float2(s[64 * q + j - RAD], s[64 * q + 32 + j - RAD]);
+                                own[q] = X[RAD];
+                            }
+                            if (MODE == MODE_HPASS) {
+                                outv[q] = live ? row_pass_pair<RAD, SYMW>(X, p.w, one2) : make_float2(0.0f, 0.0f);
+                            } else if (single_like(MODE)) {
+                                outv[q] = dense_fold_pair<RAD, NACC, (SYM >= 1)>(acc[g][q], X, p.k, one2);
+                            } else {
+                                float2 v = own[q];  // VPASS: src already holds the row-pass result
+                                if (MODE == MODE_FUSED)  // dead rows: the faithful scratch row stays 0
+                                    v = live ? row_pass_pair<RAD, SYMW>(X, p.w, one2) : make_float2(0.0f, 0.0f);
+                                outv[q] = col_fold_pair<RAD, NACC, SYMW>(acc[g][q], v, p.w, one2);
+                            }
+                        }
+                        const unsigned in4 = (inside >> (4 * g)) & 0xFu, va4 = (valid >> (4 * g)) & 0xFu;
+                        const float o4[4] = {outv[0].x, outv[0].y, outv[1].x, outv[1].y};
+                        const float w4[4] = {own[0].x, own[0].y, own[1].x, own[1].y};
+                        if (MODE == MODE_HPASS) {
+                            // dead rows are written (as zeros) only under zero fill; on live
+                            // rows the column ring is zeroed under zero fill, else kept
+                            if (emit && (live || zero_fill)) {
+                                float* d = dcur + rel[g];
+                                if (live && va4 == 0xFu) {
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) d[32 * i] = o4[i];
+                                } else {
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) {
+                                        const bool val = live && ((va4 >> i) & 1u);
+                                        if (((in4 >> i) & 1u) && (val || zero_fill)) d[32 * i] = val ? o4[i] : 0.0f;
+                                    }
+                                }
+                            }
+                        } else if (emit) {
+                            float* d = dcur + rel[g];
+                            if (va4 == 0xFu) {
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) d[32 * i] = o4[i];
+                            } else {
+                                // ring columns of output row yo keep the input sample, staged RAD rows back
+                                int rr = slot * SROWS + k - RAD;
+                                if (rr < 0) rr += NS * SROWS;
+                                const float* rrow = ring + rr * SW + 8 + rel[g];
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    if ((va4 >> i) & 1u)
+                                        d[32 * i] = o4[i];
+                                    else if (ring_copy && ((in4 >> i) & 1u))
+                                        d[32 * i] = rrow[sshift[rr] + 32 * i];
+                                }
+                            }
+                        }
+                        if (ring_row) {  // a ring row of the image: the input row itself
+                            float* d = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride + rel[g];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                if ((in4 >> i) & 1u) d[32 * i] = w4[i];
+                        }
+                    }
+                    if (emit) dcur += p.dst_row_stride;
+                }
+            }
+        };
+        const int yo0 = (MODE == MODE_HPASS) ? r0 : r0 - RAD;
+        if (!ROW_EDGE && r0 + SROWS <= it.in_hi && yo0 >= emit_lo && yo0 + SROWS <= emit_hi)
+            stage_rows(std::true_type{});
+        else
+            stage_rows(std::false_type{});
+        if (gs >= LAGS) {
+            int rel_s = slot - LAGS;
+            if (rel_s < 0) rel_s += NS;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[rel_s]);
+        }
+        if (++slot == NS) { slot = 0; phase ^= 1u; }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // The kernel
 
 // SIG: the row-band readiness signalling (Params::sig_*) is compiled in; only the
@@ -1339,6 +1584,12 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 20 + ntr, clock64());
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
+        if constexpr (!ALIGNED && SC_LANES) {
+            if (item_rows_edge<MODE, RAD>(p, it))
+                consume_item_lanes<MODE, RAD, true, SYM, SIG>(p, it, ring, full, empty, sshift, slot, phase, gs);
+            else
+                consume_item_lanes<MODE, RAD, false, SYM, SIG>(p, it, ring, full, empty, sshift, slot, phase, gs);
+        } else
         if (item_rows_edge<MODE, RAD>(p, it))
             consume_item<MODE, RAD, ALIGNED, true, SYM, true, SIG>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
                                                                    gs);
