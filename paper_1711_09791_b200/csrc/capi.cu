@@ -54,7 +54,7 @@ int fail_cuda(cudaError_t e, const std::string& what) {
 // while the common case costs no getenv() per knob.
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
-    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_stage = 0;
+    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0;
     int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0, peer_timeout_ms = 0;
     int u8_occ2 = 0;
     int u8_gen = 0;
@@ -81,7 +81,6 @@ static Knobs read_knobs() {
         else if (name == "TAIL_WAVES") k.tail_waves = v;
         else if (name == "EXACT_WAVES") k.exact_waves = v;
         else if (name == "IPC") k.ipc = v;
-        else if (name == "NO_STAGE") k.no_stage = v;
         else if (name == "NO_SYM") k.no_sym = v;
         else if (name == "NO_COLSYM") k.no_colsym = v;
         else if (name == "NO_PDL") k.no_pdl = v;
@@ -270,9 +269,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     if (ns_req > 32) ns_req = 32;
     auto smem_for = [&](int tw_, int ns_) {
         const int sw = aligned ? tw_ + 2 * HALO : tw_ + 2 * HALO + 16;  // row_width<ALIGNED>
-        const size_t staging = (aligned || SC_LANES) ? 0 : (size_t)2 * SROWS * (tw_ + 8) * 4;  // SC_LANES=0: output staging
-        return (size_t)((2 * ns_ * 8 + ns_ * 4 + ns_ * SROWS * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * sw * 4 +
-               staging;
+        return (size_t)((2 * ns_ * 8 + ns_ * 4 + ns_ * SROWS * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * sw * 4;
     };
     // an SC_NS ring deeper than shared memory holds for the narrowest strip is clamped
     while (ns_req > lags + 2 && smem_for(COLS_PER_THREAD * 64, ns_req) > 227 * 1024) --ns_req;
@@ -577,10 +574,6 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.epoch = j.sig_self ? j.epoch : 0;
     p.sig_err = j.sig_err;
     p.sig_timeout_ns = (long long)(kn.peer_timeout_ms > 0 ? kn.peer_timeout_ms : 20000) * 1000000LL;
-    // unaligned kernels stage their output rows only when the DESTINATION rows are
-    // not all 16-B aligned (a misaligned source alone keeps direct stores)
-    const bool dst_aligned = (j.C % 4 == 0) && aligned16(j.dst) && (j.dps % 4 == 0) && (j.drs % 4 == 0);
-    if (!aligned && !dst_aligned && !kn.no_stage) p.flags |= F_STAGED_STORE;
     for (int i = 0; i < j.width; ++i) p.w[i] = j.taps ? j.taps[i] : 0.0f;
     if (j.dense)
         for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];

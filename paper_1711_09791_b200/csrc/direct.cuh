@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(32 * DWARPS, SC_DMINB) sepconv_direct_kernel(c
                         if (fast && live)
                             st4(dcur + x4, outv);
                         else
-                            store_edge<true>(dcur, x4, C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
+                            store_edge(dcur, x4, C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
                     }
                 } else {
                     if (MODE == MODE_SINGLE) {
@@ -186,12 +186,12 @@ __global__ void __launch_bounds__(32 * DWARPS, SC_DMINB) sepconv_direct_kernel(c
                             st4(dcur + x4, outv);
                         } else {
                             F4 ringv = (RAD > 0) ? hist[RAD > 0 ? RAD - 1 : 0] : own;
-                            store_edge<true>(dcur, x4, C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                            store_edge(dcur, x4, C, RAD, outv, ringv, ring_copy ? 1 : 0);
                         }
                     }
                     if (ring_copy && row_edge && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD)) {
                         float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
-                        store_edge<true>(drow, x4, C, 0, own, own, 1);
+                        store_edge(drow, x4, C, 0, own, own, 1);
                     }
                     if (MODE == MODE_FUSED && RAD > 0 && !fast) {
 #pragma unroll

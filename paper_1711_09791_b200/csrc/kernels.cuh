@@ -37,8 +37,11 @@
 //               window (3 x LDS.128), computes the row pass for its 4 columns
 //               and pushes them through a shift register of 2r partial column
 //               sums, emitting output row y-r as soon as input row y arrived.
-//               Results go straight to HBM with STG.128 (unaligned destination
-//               rows: staged in smem and written by bulk TMA stores).
+//               Results go straight to HBM with STG.128. Rows of any other
+//               alignment (cols % 4 != 0, misaligned views): thread (warp q,
+//               lane l) owns columns 128q + l + 32i instead -- conflict-free
+//               LDS.32 at any shift, STG.32 with 128 contiguous bytes per warp
+//               (consume_item_lanes).
 //
 // Bit-exactness: every product/sum is __fmul_rn/__fadd_rn (never contracted to
 // FMA) in the reference's fold order: left-to-right from the first product,
@@ -66,7 +69,6 @@ constexpr int F_EXTENDED = 0x1;
 constexpr int F_NO_RING = 0x2;
 constexpr int F_ZERO_FILL = 0x4;
 // tuning flags (set by the planner from SC_* environment variables)
-constexpr int F_STAGED_STORE = 0x200;  // unaligned kernels: dst rows not all 16-B aligned -> staged TMA stores
 constexpr int SIG_WORDS = 8;  // signal block: [0] ready, [2]/[3] done counts above/below, [4]/[5] per-launch targets
 constexpr int F_U8_LEAN = 0x400;  // u8 kernel: interior strips take the lean loops (large payloads)
 constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (default: evict_normal,
@@ -252,20 +254,6 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
         : "memory");
 }
 
-// Bulk shared -> global copy (TMA store, bulk-group completion) and its fences.
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void consumer_bar(int nthreads) {
-    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
 __device__ __forceinline__ uint64_t policy_evict_normal() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
@@ -393,9 +381,6 @@ __device__ __forceinline__ void st4(float* p, const F4& a) {
 #endif
 #ifndef SC_SROWS
 #define SC_SROWS 4
-#endif
-#ifndef SC_LANES
-#define SC_LANES 1  // unaligned rows: the lane-strided consumer (0: adjacent columns + realignment)
 #endif
 constexpr int SROWS = SC_SROWS;
 // stages a consumer holds back after finishing one (see consume_item)
@@ -837,7 +822,7 @@ __device__ __forceinline__ F4 dense_fold_sym(F4 (&acc)[NACC], const float (&win)
 //   ring_mode 0: keep -- only columns in [rad, C-rad) are written
 //   ring_mode 1: copy -- ring columns take `ringv` (the input samples)
 //   ring_mode 2: zero -- ring columns take 0
-template <bool ALIGNED>
+// (aligned rows: x4 + 4 <= C whenever x4 < C)
 __device__ __forceinline__ void store_edge(float* drow, int x4, int C, int rad, const F4& val, const F4& ringv,
                                         int ring_mode) {
     if (x4 >= C) return;
@@ -848,7 +833,7 @@ __device__ __forceinline__ void store_edge(float* drow, int x4, int C, int rad, 
         const bool valid = col >= rad && col < C - rad;
         o.v[c] = valid ? val.v[c] : (ring_mode == 1 ? ringv.v[c] : 0.0f);
     }
-    if (ALIGNED && ring_mode != 0) {  // x4 + 4 <= C when C % 4 == 0
+    if (ring_mode != 0) {
         st4(drow + x4, o);
         return;
     }
@@ -871,139 +856,21 @@ __device__ __forceinline__ void load_win(float (&win)[12], const float* s) {
     }
 }
 
-// Window of an unaligned row: columns x4-4..x4+7 start `shift` (0..3) floats
-// past a 16-B boundary. Four conflict-free LDS.128 from the boundary, then a
-// two-stage register select (shift & 1, shift & 2). Scalar LDS.32 at the
-// shifted address would hit the same bank from every 8th lane (lane stride
-// 4 words): 4-way conflicts, measured +34% on the whole kernel.
-__device__ __forceinline__ void load_win_shift(float (&win)[12], const float* aligned_base, int shift) {
-    float b[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const F4 v = ld4(aligned_base + 4 * q);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) b[4 * q + i] = v.v[i];
-    }
-    const bool s1 = shift & 1, s2 = shift & 2;
-    float t[14];
-#pragma unroll
-    for (int i = 0; i < 14; ++i) t[i] = s1 ? b[i + 1] : b[i];
-#pragma unroll
-    for (int i = 0; i < 12; ++i) win[i] = s2 ? t[i + 2] : t[i];
-}
-
-// Store 4 columns of an output row whose start is not 16-B aligned. The row's
-// 16-B aligned float4 groups begin e columns into each thread's 4 (e = 0..3,
-// uniform per row): lane l stores the aligned group [x4+e, x4+e+4), gathering
-// column x4+e+c from lane l + (e+c)/4 with one indexed shuffle each, as a
-// single STG.128; lane 0 and lane 31 store their split-off columns one by one.
-// Columns the policy must not touch are never written.
-// ring_mode as store_edge: 0 keep, 1 copy ringv, 2 zero.
-__device__ __forceinline__ void store_shift(float* drow, int x4, int C, int rad, const F4& val, const F4& ringv,
-                                           int ring_mode, int lane) {
-    float o[4];
-    unsigned m = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int col = x4 + c;
-        const bool valid = col >= rad && col < C - rad;
-        o[c] = valid ? val.v[c] : (ring_mode == 1 ? ringv.v[c] : 0.0f);
-        if (col < C && (valid || ring_mode != 0)) m |= 1u << c;
-    }
-    const int e = (4 - (int)((reinterpret_cast<uintptr_t>(drow) >> 2) & 3)) & 3;
-    if (e == 0) {
-        if (m == 0xFu) {
-            st4(drow + x4, F4{{o[0], o[1], o[2], o[3]}});
-        } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (m & (1u << c)) drow[x4 + c] = o[c];
-        }
-        return;
-    }
-    float g[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int k = c + e;              // 1..6
-        const int q = k & 3;              // element index in the source lane
-        const float pick = q == 0 ? o[0] : (q == 1 ? o[1] : (q == 2 ? o[2] : o[3]));
-        g[c] = __shfl_sync(0xffffffffu, pick, min(lane + (k >> 2), 31));
-    }
-    const unsigned nbm = __shfl_down_sync(0xffffffffu, m, 1);
-    if (lane == 0) {  // own columns before the first aligned group
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            if (c < e && (m & (1u << c))) drow[x4 + c] = o[c];
-    }
-    if (lane == 31) {  // the aligned group would reach into the next warp's columns
-#pragma unroll
-        for (int c = 1; c < 4; ++c)
-            if (c >= e && (m & (1u << c))) drow[x4 + c] = o[c];
-        return;
-    }
-    const unsigned gm = ((m >> e) | (nbm << (4 - e))) & 0xFu;
-    if (gm == 0xFu) {
-        st4(drow + x4 + e, F4{{g[0], g[1], g[2], g[3]}});
-    } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-            if (gm & (1u << c)) drow[x4 + e + c] = g[c];
-    }
-}
-
-// Unaligned rows: each output row of a strip is first assembled in a shared
-// staging row whose 16-B alignment matches the global row's (staging index of
-// column x = x - x0 + s, s = (row address / 4 + x0) mod 4), then written by ONE
-// bulk TMA store for its aligned middle plus <= 3 scalar stores at each end
-// (instead of realigning every warp's columns with shuffles and split-off
-// scalar stores at every warp edge). Columns the policy must not touch are
-// never staged and never stored.
-__device__ __forceinline__ int row_shift(const float* drow, int x0) {
-    return (int)(((reinterpret_cast<uintptr_t>(drow) >> 2) + (uintptr_t)x0) & 3u);
-}
-
-__device__ __forceinline__ void stage_cols(float* srow, int x4, int x0, int C, int rad, const F4& val,
-                                           const F4& ringv, int ring_mode) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int col = x4 + c;
-        const bool valid = col >= rad && col < C - rad;
-        if (col < C && (valid || ring_mode != 0))
-            srow[col - x0] = valid ? val.v[c] : (ring_mode == 1 ? ringv.v[c] : 0.0f);
-    }
-}
-
-// Columns [c_lo, c_hi) of a staged row -> global row (called by one warp).
-__device__ __forceinline__ void publish_row(float* drow, const float* srow, int x0, int c_lo, int c_hi, int lane) {
-    if (c_hi <= c_lo) return;
-    const uintptr_t f = reinterpret_cast<uintptr_t>(drow) >> 2;  // row start in floats
-    int a_lo = c_lo + (int)((4u - (unsigned)((f + (uintptr_t)c_lo) & 3u)) & 3u);
-    int a_hi = c_hi - (int)((f + (uintptr_t)c_hi) & 3u);
-    if (a_lo > c_hi) a_lo = c_hi;
-    if (a_hi < a_lo) a_hi = a_lo;
-    if (lane == 0 && a_hi > a_lo) bulk_s2g(drow + a_lo, srow + (a_lo - x0), 4u * (uint32_t)(a_hi - a_lo));
-    // the unaligned ends: [c_lo, a_lo) (<= 3 columns) and [a_hi, c_hi) (<= 7)
-    const int l = c_lo + lane;
-    if (l < a_lo) drow[l] = srow[l - x0];
-    const int r = a_hi + lane;
-    if (r < c_hi && lane < 8) drow[r] = srow[r - x0];
-}
-
 // ---------------------------------------------------------------------------
-// Consumer: one item (plane, strip, band). ROW_EDGE items contain ring rows or
-// rows with a dead row pass; all others run the lean loop.
+// Consumer of 16-B aligned rows: one item (plane, strip, band). ROW_EDGE items
+// contain ring rows or rows with a dead row pass; all others run the lean loop.
+// (Rows of any other alignment: consume_item_lanes below.)
 
 // COL_EDGE: the item's strip touches the image's column ring or its right edge
-// (first and last strips, unaligned rows); interior strips (COL_EDGE false) store
+// (first and last strips); interior strips (COL_EDGE false) store
 // every group with one STG.128 and need no per-row column tests (measured: -2% at
 // cfg5 under the bench's sustained power cap, where issue slots are scarce; not
 // used by the single pass, whose register allocation it upset: cfg2 +13%).
-template <int MODE, int RAD, bool ALIGNED, bool ROW_EDGE, int SYM, bool COL_EDGE = true, bool SIG = false>
+template <int MODE, int RAD, bool ROW_EDGE, int SYM, bool COL_EDGE = true, bool SIG = false>
 __device__ __forceinline__ void consume_item(const Params& p, const Item& it, const float* ring, uint64_t* full,
-                                             uint64_t* empty, const int* sshift, float* stage_out, int& slot,
-                                             uint32_t& phase, int& gs) {
+                                             uint64_t* empty, int& slot, uint32_t& phase, int& gs) {
     constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
-    const int SW = row_width<ALIGNED>(p.tw);
+    const int SW = row_width<true>(p.tw);
     const int NS = p.ns;
     const int ct = threadIdx.x - 32;
     const int lane = threadIdx.x & 31;
@@ -1016,16 +883,13 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
     const int R = p.R, C = p.C;
     const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);  // SPLITF: image ring untouched
     const bool zero_fill = (MODE == MODE_HPASS) && (p.flags & F_ZERO_FILL);
-    // unaligned kernels with 16-B aligned destination rows (only the source is
-    // misaligned) store directly; staging pays only when the stores are unaligned
-    const bool staged = !ALIGNED && (p.flags & F_STAGED_STORE);
 
     int x4[GROUPS];
     bool fast[GROUPS];
 #pragma unroll
     for (int g = 0; g < GROUPS; ++g) {
         x4[g] = it.x0 + 4 * ct + g * tw2;
-        fast[g] = ALIGNED && (!COL_EDGE || (x4[g] >= RAD && x4[g] + 4 <= C - RAD));
+        fast[g] = !COL_EDGE || (x4[g] >= RAD && x4[g] + 4 <= C - RAD);
     }
     float* dplane = p.dst + (long long)it.plane * p.dst_plane_stride;
 
@@ -1073,24 +937,14 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                     const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
                     const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
                     const bool emit = FAST || (yo >= emit_lo && yo < emit_hi);
-                    const int shift = ALIGNED ? 0 : sshift[slot * SROWS + k];
-                    // unaligned: this row's staging row, indexed so that srow[x - x0] has the
-                    // global column's 16-B alignment
-                    float* srow = nullptr;
-                    if (staged)
-                        srow = stage_out + ((gs & 1) * SROWS + k) * (p.tw + 8) + row_shift(dcur, it.x0);
     #pragma unroll
                     for (int g = 0; g < GROUPS; ++g) {
                         // a warp whose group lies wholly right of the image (the padding of a
-                        // partial last strip) has nothing to store: skip its arithmetic. The
-                        // test is warp-uniform (lane 0's columns), as store_shift shuffles.
+                        // partial last strip) has nothing to store: skip its arithmetic
+                        // (warp-uniform: lane 0's columns)
                         if (COL_EDGE && x4[g] - 4 * lane >= C) continue;
                         float win[12];
-                        if (ALIGNED) {
-                            load_win(win, sstage + k * SW + g * tw2);
-                        } else {
-                            load_win_shift(win, sstage + k * SW + g * tw2 + 4, shift);
-                        }
+                        load_win(win, sstage + k * SW + g * tw2);
                         F4 own;
     #pragma unroll
                         for (int i = 0; i < 4; ++i) own.v[i] = win[4 + i];
@@ -1136,7 +990,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                                         F4 zero;
     #pragma unroll
                                         for (int i = 0; i < 4; ++i) zero.v[i] = 0.0f;
-                                        store_edge<ALIGNED>(hrow, x4[g], C, RAD, v, zero, 2);
+                                        store_edge(hrow, x4[g], C, RAD, v, zero, 2);
                                     }
                                 }
                             }
@@ -1151,12 +1005,8 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                             if (emit && (live || zero_fill)) {
                                 if (fast[g] && live)
                                     st4(dcur + 4 * ct + g * tw2 + (it.x0), outv);
-                                else if (staged)
-                                    stage_cols(srow, x4[g], it.x0, C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
-                                else if (!ALIGNED)
-                                    store_shift(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0, lane);
                                 else
-                                    store_edge<ALIGNED>(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
+                                    store_edge(dcur, x4[g], C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
                             }
                         } else if (emit) {
                             if constexpr (MODE == MODE_SINGLECB) {
@@ -1168,7 +1018,7 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                                     F4 zero;
     #pragma unroll
                                     for (int i = 0; i < 4; ++i) zero.v[i] = 0.0f;
-                                    store_edge<ALIGNED>(irow, x4[g], C, RAD, outv, zero, 0);
+                                    store_edge(irow, x4[g], C, RAD, outv, zero, 0);
                                 }
                             }
                             if (fast[g]) {
@@ -1179,31 +1029,17 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
                                     int rr = slot * SROWS + k - RAD;  // ring row of input row yo
                                     if (rr < 0) rr += NS * SROWS;
                                     const float* rrow = ring + rr * SW + 4 * ct + g * tw2;
-                                    if (ALIGNED) {
-                                        ringv = ld4(rrow + 4);
-                                    } else {
-                                        const float* q = rrow + 8 + sshift[rr];
-    #pragma unroll
-                                        for (int i = 0; i < 4; ++i) ringv.v[i] = q[i];
-                                    }
+                                    ringv = ld4(rrow + 4);
                                 } else {
     #pragma unroll
                                     for (int i = 0; i < 4; ++i) ringv.v[i] = 0.0f;
                                 }
-                                if (ALIGNED)
-                                    store_edge<ALIGNED>(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0);
-                                else if (staged)
-                                    stage_cols(srow, x4[g], it.x0, C, RAD, outv, ringv, ring_copy ? 1 : 0);
-                                else
-                                    store_shift(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0, lane);
+                                store_edge(dcur, x4[g], C, RAD, outv, ringv, ring_copy ? 1 : 0);
                             }
                         }
                         if (ROW_EDGE && ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD)) {
                             float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
-                            if (ALIGNED)
-                                store_edge<ALIGNED>(drow, x4[g], C, 0, own, own, 1);
-                            else
-                                store_shift(drow, x4[g], C, 0, own, own, 1, lane);
+                            store_edge(drow, x4[g], C, 0, own, own, 1);
                         }
                     }
                     if (emit) dcur += p.dst_row_stride;
@@ -1215,44 +1051,6 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
             stage_rows(std::true_type{});
         else
             stage_rows(std::false_type{});
-        if (staged) {
-            // publish the stage's staged output rows: fence the generic-proxy smem
-            // writes for the TMA engine, make sure the bulk stores of the previous
-            // stage have read their (other) buffer, then one warp issues this stage's
-            bool any = false;
-#pragma unroll
-            for (int k = 0; k < SROWS; ++k) {
-                const int yi = r0 + k;
-                const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
-                any = any || (yi < it.in_hi && yo >= emit_lo && yo < emit_hi);
-            }
-            if (any) {
-                fence_proxy_async_smem();
-                if (ct == 0) bulk_wait_read0();
-                consumer_bar((int)blockDim.x - 32);
-                if (ct < 32) {
-#pragma unroll
-                    for (int k = 0; k < SROWS; ++k) {
-                        const int yi = r0 + k;
-                        const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
-                        if (yi >= it.in_hi || yo < emit_lo || yo >= emit_hi) continue;
-                        const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
-                        int c_lo = RAD, c_hi = C - RAD;  // VPASS, SINGLE: valid columns only
-                        if (MODE == MODE_FUSED && ring_copy) { c_lo = 0; c_hi = C; }
-                        if (MODE == MODE_HPASS) {
-                            if (!live && !zero_fill) continue;
-                            if (zero_fill) { c_lo = 0; c_hi = C; }
-                        }
-                        c_lo = max(c_lo, it.x0);
-                        c_hi = min(c_hi, it.x0 + p.tw);
-                        float* drow = dplane + (long long)(yo - p.dst_row0) * p.dst_row_stride;
-                        const float* srow = stage_out + ((gs & 1) * SROWS + k) * (p.tw + 8) + row_shift(drow, it.x0);
-                        publish_row(drow, srow, it.x0, c_lo, c_hi, lane);
-                    }
-                    if (ct == 0) bulk_commit();
-                }
-            }
-        }
 #ifdef SC_TRACE
         if (threadIdx.x == 32 && gs < 8) SC_TR(p, 56 + gs, clock64());
 #endif
@@ -1531,8 +1329,6 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     int* sitem = reinterpret_cast<int*>(empty + NS);
     int* sshift = sitem + NS;  // per ring row (NS * SROWS): float shift of an unaligned row
     float* ring = reinterpret_cast<float*>(smem_raw + ((2 * NS * 8 + NS * 4 + NS * SROWS * 4 + 127) / 128) * 128);
-    // unaligned kernels: 2 x SROWS staging rows of tw + 8 floats after the ring
-    float* stage_out = ring + NS * SROWS * row_width<ALIGNED>(p.tw);
     const int warp = threadIdx.x >> 5;
     const int ncw = (blockDim.x >> 5) - 1;
 
@@ -1584,27 +1380,22 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 20 + ntr, clock64());
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
-        if constexpr (!ALIGNED && SC_LANES) {
+        if constexpr (!ALIGNED) {
             if (item_rows_edge<MODE, RAD>(p, it))
                 consume_item_lanes<MODE, RAD, true, SYM, SIG>(p, it, ring, full, empty, sshift, slot, phase, gs);
             else
                 consume_item_lanes<MODE, RAD, false, SYM, SIG>(p, it, ring, full, empty, sshift, slot, phase, gs);
-        } else
-        if (item_rows_edge<MODE, RAD>(p, it))
-            consume_item<MODE, RAD, ALIGNED, true, SYM, true, SIG>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
-                                                                   gs);
-        else if (single_like(MODE) || !ALIGNED || it.x0 < RAD || it.x0 + p.tw > p.C - RAD)
-            consume_item<MODE, RAD, ALIGNED, false, SYM, true, SIG>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
-                                                                    gs);
+        } else if (item_rows_edge<MODE, RAD>(p, it))
+            consume_item<MODE, RAD, true, SYM, true, SIG>(p, it, ring, full, empty, slot, phase, gs);
+        else if (single_like(MODE) || it.x0 < RAD || it.x0 + p.tw > p.C - RAD)
+            consume_item<MODE, RAD, false, SYM, true, SIG>(p, it, ring, full, empty, slot, phase, gs);
         else
-            consume_item<MODE, RAD, ALIGNED, false, SYM, false, SIG>(p, it, ring, full, empty, sshift, stage_out, slot, phase,
-                                                                gs);
+            consume_item<MODE, RAD, false, SYM, false, SIG>(p, it, ring, full, empty, slot, phase, gs);
 #ifdef SC_TRACE
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 30 + ntr, clock64());
         ++ntr;
 #endif
     }
-    if (!ALIGNED && threadIdx.x == 32) bulk_wait_all();  // staged rows fully stored before smem goes away
 #ifdef SC_TRACE
     if (threadIdx.x == 32) {
         SC_TR(p, 40, clock64());

@@ -19,7 +19,4 @@ def view(b, off):
 for so, do in ((0, 0), (1, 0), (0, 1), (1, 1), (2, 2)):
     src, dst = view(base_s, so), view(base_d, do)
     ms = t(lambda: dev.two_pass(src, w, dst))
-    os.environ["SC_NO_STAGE"] = "1"
-    ms_ns = t(lambda: dev.two_pass(src, w, dst))
-    os.environ.pop("SC_NO_STAGE")
-    print(json.dumps({"src_off": so, "dst_off": do, "ms": round(ms, 4), "ms_no_stage": round(ms_ns, 4)}))
+    print(json.dumps({"src_off": so, "dst_off": do, "ms": round(ms, 4)}))
