@@ -54,7 +54,7 @@ int fail_cuda(cudaError_t e, const std::string& what) {
 // while the common case costs no getenv() per knob.
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
-    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0;
+    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_lanes_wide = 0;
     int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0, peer_timeout_ms = 0;
     int u8_occ2 = 0;
     int u8_gen = 0;
@@ -88,6 +88,7 @@ static Knobs read_knobs() {
         else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;
         else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;
         else if (name == "U8_OCC2") k.u8_occ2 = v;  // small u8 payloads on the 2-CTA build
+        else if (name == "NO_LANES_WIDE") k.no_lanes_wide = v;  // widths 11..21 on the plain kernels
         else if (name == "U8_GEN") k.u8_gen = v;    // the general-geometry u8 build on aligned rows too
     }
     return k;
@@ -253,7 +254,8 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
                      Plan& pl) {
     const int rad = j.width / 2;
     const bool seg2 = j.out_hi2 > j.out_lo2;
-    const int COLS_PER_THREAD = 4 * groups_of(j.mode);  // 4-column groups per consumer thread
+    const int COLS_PER_THREAD = 4 * groups_of(j.mode, rad);  // 4-column groups per consumer thread
+    const int HL = halo_of(rad);
     int nt = 0, threads = 0, ns = 0, tw = 0;
     size_t smem = 0;
     if (direct) {
@@ -268,7 +270,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     if (ns_req < lags + 2) ns_req = lags + 2;
     if (ns_req > 32) ns_req = 32;
     auto smem_for = [&](int tw_, int ns_) {
-        const int sw = aligned ? tw_ + 2 * HALO : tw_ + 2 * HALO + 16;  // row_width<ALIGNED>
+        const int sw = aligned ? tw_ + 2 * HL : tw_ + 2 * HL + 16;  // row_width<ALIGNED, HL>
         return (size_t)((2 * ns_ * 8 + ns_ * 4 + ns_ * SROWS * 4 + 127) / 128) * 128 + (size_t)ns_ * SROWS * sw * 4;
     };
     // an SC_NS ring deeper than shared memory holds for the narrowest strip is clamped
@@ -330,7 +332,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
                 shrt = 16;
             }
             // padding columns + the 8-column halo of every strip
-            double cost = (double)(strips * tw_ + 2 * HALO * strips) / j.C;
+            double cost = (double)(strips * tw_ + 2 * HL * strips) / j.C;
             // the in-place two-pass (split / no scratch) also snapshots 8 columns around
             // every strip boundary (written, then read back): wider strips pay
             // (measured at cfg5: 1024-column strips -3%; cfg3 -3%). Not for the
@@ -473,15 +475,20 @@ static int cached_plan(const RowsJob& j, const void* kern, bool aligned, bool di
 }
 
 int launch_rows(const RowsJob& j, cudaStream_t s) {
-    if (j.width > MAX_W) return launch_wide(j, s);
     const int rad = j.width / 2;
     const Knobs kn = read_knobs();
+    // widths 11..21: the lane-strided kernels (any alignment); wider ones, and the
+    // peer-band / in-place modes above width 9, the plain kernels of kern_wide.cu
+    const bool lanes_wide = j.width > MAX_W && j.width <= MAX_W_LANES && !kn.no_lanes_wide && !j.above && !j.below &&
+                            !j.sig_self &&
+                            (j.mode == MODE_FUSED || j.mode == MODE_HPASS || j.mode == MODE_VPASS || j.mode == MODE_SINGLE);
+    if (j.width > MAX_W && !lanes_wide) return launch_wide(j, s);
     const void* kern = nullptr;
     const bool peers_aligned = (!j.above || (aligned16(j.above) && j.above_ps % 4 == 0 && j.above_rs % 4 == 0)) &&
                                (!j.below || (aligned16(j.below) && j.below_ps % 4 == 0 && j.below_rs % 4 == 0));
     const bool aligned = (j.C % 4 == 0) && aligned16(j.src) && aligned16(j.dst) && (j.sps % 4 == 0) &&
                          (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) && peers_aligned &&
-                         kn.force_generic == 0;
+                         kn.force_generic == 0 && !lanes_wide;
     // single pass with a mirror-symmetric dense matrix (bitwise K[i][j] == K[2r-i][j],
     // e.g. outer(w, w) of symmetric taps): the kernel that reuses mirrored products
     // (measured: -17% at cfg5 size; the same reuse in the two-pass column fold
@@ -501,6 +508,9 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     // two-pass modes: mirror-symmetric taps (bitwise) share their products
     bool symw = !kn.no_sym && (j.mode == MODE_FUSED || j.mode == MODE_SPLITF) && j.taps;
     for (int i = 0; i < j.width && symw; ++i) symw = std::memcmp(&j.taps[i], &j.taps[j.width - 1 - i], sizeof(float)) == 0;
+    if (lanes_wide) {
+        kern = j.mode == MODE_SINGLE ? kernel_lanes_wide_single(rad) : kernel_lanes_wide(j.mode, rad, symw);
+    } else
     switch (j.mode) {
         case MODE_FUSED: kern = kernel_fused(rad, aligned, symw, j.sig_self != nullptr); break;
         case MODE_HPASS: kern = kernel_hpass(rad, aligned); break;
@@ -539,8 +549,9 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
         if (rc != SC_OK) return rc;
     }
 
-    Params p;
-    std::memset(&p, 0, sizeof(p));
+    ParamsW pw;  // the r <= 4 kernels take its Params part only
+    std::memset(&pw, 0, sizeof(pw));
+    Params& p = pw;
     p.src = j.src;
     p.dst = j.dst;
     p.src_plane_stride = j.sps;
@@ -574,9 +585,13 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     p.epoch = j.sig_self ? j.epoch : 0;
     p.sig_err = j.sig_err;
     p.sig_timeout_ns = (long long)(kn.peer_timeout_ms > 0 ? kn.peer_timeout_ms : 20000) * 1000000LL;
-    for (int i = 0; i < j.width; ++i) p.w[i] = j.taps ? j.taps[i] : 0.0f;
-    if (j.dense)
-        for (int i = 0; i < j.width * j.width; ++i) p.k[i] = j.dense[i];
+    {
+        float* w = lanes_wide ? pw.wide_w : p.w;
+        float* k = lanes_wide ? pw.wide_k : p.k;
+        for (int i = 0; i < j.width; ++i) w[i] = j.taps ? j.taps[i] : 0.0f;
+        if (j.dense)
+            for (int i = 0; i < j.width * j.width; ++i) k[i] = j.dense[i];
+    }
     p.tw = pl.tw;
     p.nstrips = pl.nstrips;
     p.ns = pl.ns;
@@ -656,7 +671,7 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     if (pl.grid > kTraceCtas) p.trace = nullptr;
 #endif
 
-    void* args[] = {&p};
+    void* args[] = {&pw};  // Params is ParamsW's base: same address
     // Programmatic dependent launch: this grid may be scheduled while the previous
     // kernel on the stream drains (its launch and smem/mbarrier setup overlap that
     // kernel's tail); the kernel itself waits (griddepcontrol.wait) for the

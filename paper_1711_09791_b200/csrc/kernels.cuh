@@ -77,7 +77,14 @@ constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (d
 constexpr int HALO = 4;       // smem columns kept either side of a strip (supports r <= 4)
 constexpr int MAX_RAD = 4;
 constexpr int MAX_W = 2 * MAX_RAD + 1;
-constexpr int MAX_W_WIDE = 255;  // widths 11..255 run the plain kernels of kern_wide.cu
+constexpr int MAX_W_WIDE = 255;  // widths 23..255 run the plain kernels of kern_wide.cu
+// widths 11..21 (r = 5..10): the lane-strided consumer (consume_item_lanes) with a
+// wider smem halo and the taps in ParamsW -- its window is streamed from shared
+// memory tap by tap, so only the column fold's 2r partial sums live in registers
+constexpr int MAX_RAD_LANES = 10;
+constexpr int MAX_W_LANES = 2 * MAX_RAD_LANES + 1;
+// smem columns kept either side of a strip: a multiple of 4 (16-B copies) >= r
+__host__ __device__ constexpr int halo_of(int rad) { return rad <= 4 ? 4 : ((rad + 3) / 4) * 4; }
 constexpr int MAX_THREADS = 32 + 256;  // producer warp + up to 8 consumer warps
 #ifndef SC_MAXT
 #define SC_MAXT MAX_THREADS
@@ -154,6 +161,13 @@ struct Params {
     unsigned int* sig_err;
     long long sig_timeout_ns;
     unsigned long long sig_n_above, sig_n_below;
+};
+
+// Parameters of the widths 11..21 kernels: Params plus their taps (kept out of
+// Params so the r <= 4 kernels' parameter block, and their launch cost, stay as they are).
+struct ParamsW : Params {
+    float wide_w[MAX_W_LANES];
+    float wide_k[MAX_W_LANES * MAX_W_LANES];
 };
 
 // SC_TRACE (a dev-only build variant): per-CTA timeline of TRACE_SLOTS words.
@@ -387,14 +401,16 @@ constexpr int SROWS = SC_SROWS;
 __host__ __device__ constexpr int stage_lags(int mode, int rad) {
     return mode == MODE_FUSED ? ((rad + SROWS - 1) / SROWS > 0 ? (rad + SROWS - 1) / SROWS : 1) : 0;
 }
-__host__ __device__ constexpr int groups_of(int mode) { return single_like(mode) ? SC_GROUPS_SINGLE : SC_GROUPS; }
+__host__ __device__ constexpr int groups_of(int mode, int rad = 0) {
+    return single_like(mode) && rad <= MAX_RAD ? SC_GROUPS_SINGLE : SC_GROUPS;
+}
 
 // Shared-memory row width (floats): the segment [x0-4, x0+TW+4), plus room for
 // the 16-B realignment of unaligned rows (up to 3 floats before and after, and
 // the 4-float pad the segment starts after).
-template <bool ALIGNED>
+template <bool ALIGNED, int HL = HALO>
 __device__ __forceinline__ int row_width(int tw) {
-    return ALIGNED ? tw + 2 * HALO : tw + 2 * HALO + 16;
+    return ALIGNED ? tw + 2 * HL : tw + 2 * HL + 16;
 }
 
 struct Item {
@@ -472,7 +488,8 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
     // published in sshift[] for the consumers. Either way one lane issues TMA.
     const int lane = threadIdx.x & 31;
     if (lane != 0) return;
-    const int SW = row_width<ALIGNED>(p.tw);
+    constexpr int HL = halo_of(RAD);
+    const int SW = row_width<ALIGNED, HL>(p.tw);
     const int NS = p.ns;
     uint64_t pol = 0;
     if (ALIGNED) pol = (p.flags & F_L2_EVICT_FIRST) ? policy_evict_first() : policy_evict_normal();
@@ -527,10 +544,10 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
             return;
         }
         const Item it = decode_item<MODE, RAD>(p, item);
-        const int cx0 = max(it.x0 - HALO, 0);
-        const int cx1 = min(it.x0 + p.tw + HALO, p.C);
+        const int cx0 = max(it.x0 - HL, 0);
+        const int cx1 = min(it.x0 + p.tw + HL, p.C);
         const int n = cx1 - cx0;
-        const int soff = cx0 - (it.x0 - HALO);
+        const int soff = cx0 - (it.x0 - HL);
         for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
             if (gs >= NS) mbar_wait(&empty[slot], phase ^ 1u);
             const int nrows = min(SROWS, it.in_hi - r0);
@@ -591,7 +608,7 @@ __device__ __forceinline__ void producer(const Params& p, float* ring, uint64_t*
             } else {
                 if (!waited) wait_neighbours();
                 // the segment [g, g+n) lands at the 16-B aligned smem index 4 + soff, preceded
-                // by its shift s = (g mod 16 B) / 4 floats: column c sits at c - x0 + 8 + s
+                // by its shift s = (g mod 16 B) / 4 floats: column c sits at c - x0 + HL + 4 + s
                 uint32_t total = 0;
                 for (int k = 0; k < nrows; ++k) {
                     const uintptr_t a = reinterpret_cast<uintptr_t>(src_row(p, it.plane, r0 + k) + cx0);
@@ -1117,45 +1134,70 @@ __device__ __forceinline__ float2 dense_fold_pair(float2 (&acc)[NACC], const flo
                                                   float2 one2) {
     constexpr int W = 2 * RAD + 1;
     if (RAD == 0) return __fmul2_rn(X[0], make_float2(k[0], k[0]));
-    float2 pr[RAD + 1][W];  // products of kernel rows 0..RAD
+    auto mul = [&](int i, int j) { return __fmul2_rn(X[j], make_float2(k[i * W + j], k[i * W + j])); };
+    float2 out;
+    if constexpr (ROWSYM) {
+        float2 pr[RAD + 1][W];  // products of kernel rows 0..RAD (rows 2r..r+1 mirror them)
 #pragma unroll
-    for (int i = 0; i <= RAD; ++i)
+        for (int i = 0; i <= RAD; ++i)
 #pragma unroll
-        for (int j = 0; j < W; ++j) pr[i][j] = __fmul2_rn(X[j], make_float2(k[i * W + j], k[i * W + j]));
-    auto prod = [&](int i, int j) {
-        if (i <= RAD) return pr[i][j];
-        if (ROWSYM) return pr[W - 1 - i][j];
-        return __fmul2_rn(X[j], make_float2(k[i * W + j], k[i * W + j]));
-    };
-    float2 t = acc[NACC - 1];
+            for (int j = 0; j < W; ++j) pr[i][j] = mul(i, j);
+        float2 t = acc[NACC - 1];
 #pragma unroll
-    for (int j = 0; j < W; ++j) t = add2p(t, prod(W - 1, j), one2);
-    const float2 out = t;
+        for (int j = 0; j < W; ++j) t = add2p(t, pr[0][j], one2);  // kernel row 2r == row 0
+        out = t;
 #pragma unroll
-    for (int i = NACC - 1; i >= 1; --i) {
-        t = acc[i - 1];
+        for (int i = NACC - 1; i >= 1; --i) {
+            t = acc[i - 1];
 #pragma unroll
-        for (int j = 0; j < W; ++j) t = add2p(t, prod(i, j), one2);
-        acc[i] = t;
+            for (int j = 0; j < W; ++j) t = add2p(t, pr[i <= RAD ? i : W - 1 - i][j], one2);
+            acc[i] = t;
+        }
+        t = pr[0][0];
+#pragma unroll
+        for (int j = 1; j < W; ++j) t = add2p(t, pr[0][j], one2);
+        acc[0] = t;
+    } else {
+        float2 t = acc[NACC - 1];
+#pragma unroll
+        for (int j = 0; j < W; ++j) t = add2p(t, mul(W - 1, j), one2);
+        out = t;
+#pragma unroll
+        for (int i = NACC - 1; i >= 1; --i) {
+            t = acc[i - 1];
+#pragma unroll
+            for (int j = 0; j < W; ++j) t = add2p(t, mul(i, j), one2);
+            acc[i] = t;
+        }
+        t = mul(0, 0);
+#pragma unroll
+        for (int j = 1; j < W; ++j) t = add2p(t, mul(0, j), one2);
+        acc[0] = t;
     }
-    t = pr[0][0];
-#pragma unroll
-    for (int j = 1; j < W; ++j) t = add2p(t, pr[0][j], one2);
-    acc[0] = t;
     return out;
 }
 
+// w / k: the taps / dense matrix in the kernel's parameter block (Params::w, ::k;
+// ParamsW::wide_w, ::wide_k for r > 4). LEAN (r > 4): the rows of a stage run in a
+// rolled loop and every item takes the ROW_EDGE path -- the unrolled bodies of a
+// 21 x 21 dense fold would not fit the instruction cache -- and mirror-symmetric
+// matrices share no products (their (r+1)(2r+1) product pairs would not fit the
+// register file).
 template <int MODE, int RAD, bool ROW_EDGE, int SYM, bool SIG = false>
-__device__ __forceinline__ void consume_item_lanes(const Params& p, const Item& it, const float* ring, uint64_t* full,
-                                                   uint64_t* empty, const int* sshift, int& slot, uint32_t& phase,
-                                                   int& gs) {
+__device__ __forceinline__ void consume_item_lanes(const Params& p, const float* w, const float* kd, const Item& it,
+                                                   const float* ring, uint64_t* full, uint64_t* empty,
+                                                   const int* sshift, int& slot, uint32_t& phase, int& gs) {
     static_assert(!snap_mode(MODE), "in-place modes run aligned rows only");
     constexpr int W = 2 * RAD + 1;
     constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
-    constexpr int GROUPS = groups_of(MODE);
+    constexpr int GROUPS = groups_of(MODE, RAD);
+    constexpr bool LEAN = RAD > MAX_RAD;
+    constexpr int ROW_UNROLL = LEAN ? 1 : SROWS;
     constexpr bool SYMW = !single_like(MODE) && SYM != 0;
+    constexpr bool ROWSYM = SYM >= 1 && !LEAN;
     constexpr int LAGS = stage_lags(MODE, RAD);
-    const int SW = row_width<false>(p.tw);
+    constexpr int HL = halo_of(RAD);
+    const int SW = row_width<false, HL>(p.tw);
     const int NS = p.ns;
     const int ct = threadIdx.x - 32;
     const int lane = threadIdx.x & 31;
@@ -1205,21 +1247,23 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const Item& 
             if (r0 == it.in_lo && it.in_lo < p.src_row0) red_add_relaxed_sys(p.sig_self + 2, 1ULL);
             if (r0 + SROWS >= it.in_hi && it.in_hi > p.src_row0 + p.src_rows) red_add_relaxed_sys(p.sig_self + 3, 1ULL);
         }
-        // column x0 of ring row rr sits at ring[rr * SW + 8 + sshift[rr]] (producer)
+        // column x0 of ring row rr sits at ring[rr * SW + HL + 4 + sshift[rr]] (producer)
         int sh[SROWS];
+        if (!LEAN) {
 #pragma unroll
-        for (int k = 0; k < SROWS; ++k) sh[k] = sshift[slot * SROWS + k];
-        const float* sstage = ring + slot * SROWS * SW + 8;
+            for (int k = 0; k < SROWS; ++k) sh[k] = sshift[slot * SROWS + k];
+        }
+        const float* sstage = ring + slot * SROWS * SW + HL + 4;
         auto stage_rows = [&](auto fast_stage) {
             constexpr bool FAST = decltype(fast_stage)::value;
-#pragma unroll
+#pragma unroll ROW_UNROLL
             for (int k = 0; k < SROWS; ++k) {
                 const int yi = r0 + k;
                 if (FAST || yi < it.in_hi) {
                     const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
                     const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
                     const bool emit = FAST || (yo >= emit_lo && yo < emit_hi);
-                    const float* srow = sstage + k * SW + sh[k];
+                    const float* srow = sstage + k * SW + (LEAN ? sshift[slot * SROWS + k] : sh[k]);
                     const bool ring_row = ROW_EDGE && ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD);
 #pragma unroll
                     for (int g = 0; g < GROUPS; ++g) {
@@ -1238,14 +1282,14 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const Item& 
                                 own[q] = X[RAD];
                             }
                             if (MODE == MODE_HPASS) {
-                                outv[q] = live ? row_pass_pair<RAD, SYMW>(X, p.w, one2) : make_float2(0.0f, 0.0f);
+                                outv[q] = live ? row_pass_pair<RAD, SYMW>(X, w, one2) : make_float2(0.0f, 0.0f);
                             } else if (single_like(MODE)) {
-                                outv[q] = dense_fold_pair<RAD, NACC, (SYM >= 1)>(acc[g][q], X, p.k, one2);
+                                outv[q] = dense_fold_pair<RAD, NACC, ROWSYM>(acc[g][q], X, kd, one2);
                             } else {
                                 float2 v = own[q];  // VPASS: src already holds the row-pass result
                                 if (MODE == MODE_FUSED)  // dead rows: the faithful scratch row stays 0
-                                    v = live ? row_pass_pair<RAD, SYMW>(X, p.w, one2) : make_float2(0.0f, 0.0f);
-                                outv[q] = col_fold_pair<RAD, NACC, SYMW>(acc[g][q], v, p.w, one2);
+                                    v = live ? row_pass_pair<RAD, SYMW>(X, w, one2) : make_float2(0.0f, 0.0f);
+                                outv[q] = col_fold_pair<RAD, NACC, SYMW>(acc[g][q], v, w, one2);
                             }
                         }
                         const unsigned in4 = (inside >> (4 * g)) & 0xFu, va4 = (valid >> (4 * g)) & 0xFu;
@@ -1276,7 +1320,7 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const Item& 
                                 // ring columns of output row yo keep the input sample, staged RAD rows back
                                 int rr = slot * SROWS + k - RAD;
                                 if (rr < 0) rr += NS * SROWS;
-                                const float* rrow = ring + rr * SW + 8 + rel[g];
+                                const float* rrow = ring + rr * SW + HL + 4 + rel[g];
 #pragma unroll
                                 for (int i = 0; i < 4; ++i) {
                                     if ((va4 >> i) & 1u)
@@ -1298,7 +1342,7 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const Item& 
             }
         };
         const int yo0 = (MODE == MODE_HPASS) ? r0 : r0 - RAD;
-        if (!ROW_EDGE && r0 + SROWS <= it.in_hi && yo0 >= emit_lo && yo0 + SROWS <= emit_hi)
+        if (!LEAN && !ROW_EDGE && r0 + SROWS <= it.in_hi && yo0 >= emit_lo && yo0 + SROWS <= emit_hi)
             stage_rows(std::true_type{});
         else
             stage_rows(std::false_type{});
@@ -1317,11 +1361,12 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const Item& 
 
 // SIG: the row-band readiness signalling (Params::sig_*) is compiled in; only the
 // peer-band launches use it, so every other kernel carries none of its code.
-template <int MODE, int RAD, bool ALIGNED, int SYM = 0, bool SIG = false>
 #ifndef SC_MINB
 #define SC_MINB 1
 #endif
-__global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __grid_constant__ Params p) {
+// w / kd: the taps and the dense matrix inside the kernel's parameter block
+template <int MODE, int RAD, bool ALIGNED, int SYM, bool SIG>
+__device__ __forceinline__ void rows_kernel_body(const Params& p, const float* w, const float* kd) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = p.ns;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -1329,6 +1374,8 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     int* sitem = reinterpret_cast<int*>(empty + NS);
     int* sshift = sitem + NS;  // per ring row (NS * SROWS): float shift of an unaligned row
     float* ring = reinterpret_cast<float*>(smem_raw + ((2 * NS * 8 + NS * 4 + NS * SROWS * 4 + 127) / 128) * 128);
+    (void)w;
+    (void)kd;
     const int warp = threadIdx.x >> 5;
     const int ncw = (blockDim.x >> 5) - 1;
 
@@ -1380,11 +1427,13 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 20 + ntr, clock64());
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
-        if constexpr (!ALIGNED) {
+        if constexpr (!ALIGNED && RAD > MAX_RAD) {  // r > 4: one (ROW_EDGE) body
+            consume_item_lanes<MODE, RAD, true, SYM, SIG>(p, w, kd, it, ring, full, empty, sshift, slot, phase, gs);
+        } else if constexpr (!ALIGNED) {
             if (item_rows_edge<MODE, RAD>(p, it))
-                consume_item_lanes<MODE, RAD, true, SYM, SIG>(p, it, ring, full, empty, sshift, slot, phase, gs);
+                consume_item_lanes<MODE, RAD, true, SYM, SIG>(p, w, kd, it, ring, full, empty, sshift, slot, phase, gs);
             else
-                consume_item_lanes<MODE, RAD, false, SYM, SIG>(p, it, ring, full, empty, sshift, slot, phase, gs);
+                consume_item_lanes<MODE, RAD, false, SYM, SIG>(p, w, kd, it, ring, full, empty, sshift, slot, phase, gs);
         } else if (item_rows_edge<MODE, RAD>(p, it))
             consume_item<MODE, RAD, true, SYM, true, SIG>(p, it, ring, full, empty, slot, phase, gs);
         else if (single_like(MODE) || it.x0 < RAD || it.x0 + p.tw > p.C - RAD)
@@ -1403,6 +1452,20 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
         SC_TR(p, 42, ntr);
     }
 #endif
+}
+
+template <int MODE, int RAD, bool ALIGNED, int SYM = 0, bool SIG = false>
+__global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __grid_constant__ Params p) {
+    static_assert(RAD <= MAX_RAD, "r > 4: sepconv_lanes_wide_kernel");
+    rows_kernel_body<MODE, RAD, ALIGNED, SYM, SIG>(p, p.w, p.k);
+}
+
+// Widths 11..21 (r = 5..10), rows of any alignment: the generic producer and the
+// lane-strided consumer with the taps of ParamsW.
+template <int MODE, int RAD, int SYM = 0>
+__global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_lanes_wide_kernel(const __grid_constant__ ParamsW p) {
+    static_assert(RAD > MAX_RAD && RAD <= MAX_RAD_LANES, "r = 5..10");
+    rows_kernel_body<MODE, RAD, false, SYM, false>(p, p.wide_w, p.wide_k);
 }
 
 }  // namespace sc

@@ -21,6 +21,9 @@ const void* kernel_fused_direct(int rad);
 const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);
 const void* kernel_single_direct(int rad);
+// widths 11..21 (r = 5..10), any row alignment (kern_lanes_wide*.cu); nullptr otherwise
+const void* kernel_lanes_wide(int mode, int rad, bool symw);
+const void* kernel_lanes_wide_single(int rad);
 
 // gen: any row geometry (cols % 16 != 0, rows or buffers not 16-B aligned)
 const void* kernel_u8(int rad, bool symw = false, bool occ3 = false, bool gen = false);
