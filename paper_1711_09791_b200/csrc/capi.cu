@@ -254,7 +254,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
                      Plan& pl) {
     const int rad = j.width / 2;
     const bool seg2 = j.out_hi2 > j.out_lo2;
-    const int COLS_PER_THREAD = 4 * groups_of(j.mode, rad);  // 4-column groups per consumer thread
+    const int COLS_PER_THREAD = cols_per_thread(j.mode, rad);  // 4-column groups (r > 4: column pairs) per consumer thread
     const int HL = halo_of(rad);
     int nt = 0, threads = 0, ns = 0, tw = 0;
     size_t smem = 0;
@@ -268,6 +268,9 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     const int lags = stage_lags(j.mode, rad);
     int ns_req = kn.ns ? kn.ns : 16 / SROWS;
     if (ns_req < lags + 2) ns_req = lags + 2;
+    // widths 11..21: the fused kernel holds ceil(r/4) stages back for the ring
+    // columns; keep two stages in flight beyond them (measured -2% at W = 11)
+    if (rad > MAX_RAD && !kn.ns && ns_req < lags + 3) ns_req = lags + 3;
     if (ns_req > 32) ns_req = 32;
     auto smem_for = [&](int tw_, int ns_) {
         const int sw = aligned ? tw_ + 2 * HL : tw_ + 2 * HL + 16;  // row_width<ALIGNED, HL>
@@ -295,8 +298,11 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     int lo1 = j.out_lo, hi1 = j.out_hi, lo2 = seg2 ? j.out_lo2 : 0, hi2 = seg2 ? j.out_hi2 : 0;
     if (hi1 <= lo1) { lo1 = lo2; hi1 = hi2; lo2 = hi2 = 0; }
     const int rows_total = (hi1 - lo1) + (hi2 > lo2 ? hi2 - lo2 : 0);
-    const int bh_tall = kn.band_h > 0 ? kn.band_h : 128;
-    const int bh_short = kn.band_h2 > 0 ? kn.band_h2 : 32;
+    // every band re-reads 2r halo rows: radii above 4 take bands twice as tall
+    // (measured at 3 x 8192^2: W = 11 -7%, W = 21 -4%)
+    const bool tall_bands = rad > MAX_RAD;
+    const int bh_tall = kn.band_h > 0 ? kn.band_h : (tall_bands ? 256 : 128);
+    const int bh_short = kn.band_h2 > 0 ? kn.band_h2 : (tall_bands ? 64 : 32);
     int occ = 1, h1 = bh_short, h2 = bh_short, nstrips = 0;
     long long G = 1;
     if (direct) {
@@ -327,7 +333,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
             // band heights scale with the job: fewer than ~8 waves of 128-row items
             // per CTA -> 64/16 (measured: cfg2 -11%, cfg3 -2.5% time; cfg5 keeps 128/32)
             int tall = bh_tall, shrt = bh_short;
-            if (!kn.band_h && !kn.band_h2 && units * (long long)rows < 8LL * g * 128) {
+            if (!kn.band_h && !kn.band_h2 && !tall_bands && units * (long long)rows < 8LL * g * 128) {
                 tall = 64;
                 shrt = 16;
             }

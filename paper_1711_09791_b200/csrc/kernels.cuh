@@ -404,6 +404,14 @@ __host__ __device__ constexpr int stage_lags(int mode, int rad) {
 __host__ __device__ constexpr int groups_of(int mode, int rad = 0) {
     return single_like(mode) && rad <= MAX_RAD ? SC_GROUPS_SINGLE : SC_GROUPS;
 }
+// lane-strided consumer: column pairs per thread and group. The dense fold of
+// widths 13..21 keeps 2r partial sums per column: one pair (2 columns) per thread
+// holds them without spilling (two pairs: 40..1470 bytes of spills at r = 6..10)
+__host__ __device__ constexpr int pairs_of(int mode, int rad) { return single_like(mode) && rad > 5 ? 1 : 2; }
+// output columns per consumer thread
+__host__ __device__ constexpr int cols_per_thread(int mode, int rad) {
+    return rad <= MAX_RAD ? 4 * groups_of(mode, rad) : 2 * pairs_of(mode, rad) * groups_of(mode, rad);
+}
 
 // Shared-memory row width (floats): the segment [x0-4, x0+TW+4), plus room for
 // the 16-B realignment of unaligned rows (up to 3 floats before and after, and
@@ -1178,11 +1186,11 @@ __device__ __forceinline__ float2 dense_fold_pair(float2 (&acc)[NACC], const flo
 }
 
 // w / k: the taps / dense matrix in the kernel's parameter block (Params::w, ::k;
-// ParamsW::wide_w, ::wide_k for r > 4). LEAN (r > 4): the rows of a stage run in a
-// rolled loop and every item takes the ROW_EDGE path -- the unrolled bodies of a
-// 21 x 21 dense fold would not fit the instruction cache -- and mirror-symmetric
-// matrices share no products (their (r+1)(2r+1) product pairs would not fit the
-// register file).
+// ParamsW::wide_w, ::wide_k for r > 4). LEAN (the single pass at r > 4): the rows
+// of a stage run in a rolled loop and every item takes the ROW_EDGE path -- the
+// unrolled bodies of a 21 x 21 dense fold would not fit the instruction cache --
+// and mirror-symmetric matrices share no products (their (r+1)(2r+1) product
+// pairs would not fit the register file).
 template <int MODE, int RAD, bool ROW_EDGE, int SYM, bool SIG = false>
 __device__ __forceinline__ void consume_item_lanes(const Params& p, const float* w, const float* kd, const Item& it,
                                                    const float* ring, uint64_t* full, uint64_t* empty,
@@ -1191,10 +1199,13 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const float*
     constexpr int W = 2 * RAD + 1;
     constexpr int NACC = (2 * RAD > 0) ? 2 * RAD : 1;
     constexpr int GROUPS = groups_of(MODE, RAD);
-    constexpr bool LEAN = RAD > MAX_RAD;
+    constexpr int PAIRS = pairs_of(MODE, RAD);  // column pairs (c, c+32) per thread and group
+    constexpr int CPT = 2 * PAIRS;
+    constexpr unsigned ALLC = (1u << CPT) - 1u;
+    constexpr bool LEAN = RAD > MAX_RAD && single_like(MODE);
     constexpr int ROW_UNROLL = LEAN ? 1 : SROWS;
     constexpr bool SYMW = !single_like(MODE) && SYM != 0;
-    constexpr bool ROWSYM = SYM >= 1 && !LEAN;
+    constexpr bool ROWSYM = SYM >= 1 && RAD <= MAX_RAD;
     constexpr int LAGS = stage_lags(MODE, RAD);
     constexpr int HL = halo_of(RAD);
     const int SW = row_width<false, HL>(p.tw);
@@ -1213,12 +1224,12 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const float*
     unsigned inside = 0, valid = 0;
 #pragma unroll
     for (int g = 0; g < GROUPS; ++g) {
-        rel[g] = g * tw2 + 4 * (ct & ~31) + lane;
+        rel[g] = g * tw2 + CPT * (ct & ~31) + lane;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < CPT; ++i) {
             const int col = it.x0 + rel[g] + 32 * i;
-            if (col < C) inside |= 1u << (4 * g + i);
-            if (col >= RAD && col < C - RAD) valid |= 1u << (4 * g + i);
+            if (col < C) inside |= 1u << (CPT * g + i);
+            if (col >= RAD && col < C - RAD) valid |= 1u << (CPT * g + i);
         }
     }
     float* dplane = p.dst + (long long)it.plane * p.dst_plane_stride + it.x0;
@@ -1233,11 +1244,11 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const float*
     }
     float* dcur = dplane + (long long)(emit_lo - p.dst_row0) * p.dst_row_stride;
 
-    float2 acc[GROUPS][2][NACC];
+    float2 acc[GROUPS][PAIRS][NACC];
 #pragma unroll
     for (int g = 0; g < GROUPS; ++g)
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < PAIRS; ++q)
 #pragma unroll
             for (int j = 0; j < NACC; ++j) acc[g][q][j] = make_float2(0.0f, 0.0f);
 
@@ -1270,9 +1281,9 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const float*
                         // a warp whose columns all lie right of the image has nothing to store
                         if (it.x0 + rel[g] - lane >= C) continue;
                         const float* s = srow + rel[g];
-                        float2 outv[2], own[2];
+                        float2 outv[PAIRS], own[PAIRS];
 #pragma unroll
-                        for (int q = 0; q < 2; ++q) {
+                        for (int q = 0; q < PAIRS; ++q) {
                             float2 X[W];
                             if (MODE == MODE_VPASS) {
                                 own[q] = make_float2(s[64 * q], s[64 * q + 32]);
@@ -1292,20 +1303,26 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const float*
                                 outv[q] = col_fold_pair<RAD, NACC, SYMW>(acc[g][q], v, w, one2);
                             }
                         }
-                        const unsigned in4 = (inside >> (4 * g)) & 0xFu, va4 = (valid >> (4 * g)) & 0xFu;
-                        const float o4[4] = {outv[0].x, outv[0].y, outv[1].x, outv[1].y};
-                        const float w4[4] = {own[0].x, own[0].y, own[1].x, own[1].y};
+                        const unsigned in4 = (inside >> (CPT * g)) & ALLC, va4 = (valid >> (CPT * g)) & ALLC;
+                        float o4[CPT], w4[CPT];
+#pragma unroll
+                        for (int q = 0; q < PAIRS; ++q) {
+                            o4[2 * q] = outv[q].x;
+                            o4[2 * q + 1] = outv[q].y;
+                            w4[2 * q] = own[q].x;
+                            w4[2 * q + 1] = own[q].y;
+                        }
                         if (MODE == MODE_HPASS) {
                             // dead rows are written (as zeros) only under zero fill; on live
                             // rows the column ring is zeroed under zero fill, else kept
                             if (emit && (live || zero_fill)) {
                                 float* d = dcur + rel[g];
-                                if (live && va4 == 0xFu) {
+                                if (live && va4 == ALLC) {
 #pragma unroll
-                                    for (int i = 0; i < 4; ++i) d[32 * i] = o4[i];
+                                    for (int i = 0; i < CPT; ++i) d[32 * i] = o4[i];
                                 } else {
 #pragma unroll
-                                    for (int i = 0; i < 4; ++i) {
+                                    for (int i = 0; i < CPT; ++i) {
                                         const bool val = live && ((va4 >> i) & 1u);
                                         if (((in4 >> i) & 1u) && (val || zero_fill)) d[32 * i] = val ? o4[i] : 0.0f;
                                     }
@@ -1313,16 +1330,16 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const float*
                             }
                         } else if (emit) {
                             float* d = dcur + rel[g];
-                            if (va4 == 0xFu) {
+                            if (va4 == ALLC) {
 #pragma unroll
-                                for (int i = 0; i < 4; ++i) d[32 * i] = o4[i];
+                                for (int i = 0; i < CPT; ++i) d[32 * i] = o4[i];
                             } else {
                                 // ring columns of output row yo keep the input sample, staged RAD rows back
                                 int rr = slot * SROWS + k - RAD;
                                 if (rr < 0) rr += NS * SROWS;
                                 const float* rrow = ring + rr * SW + HL + 4 + rel[g];
 #pragma unroll
-                                for (int i = 0; i < 4; ++i) {
+                                for (int i = 0; i < CPT; ++i) {
                                     if ((va4 >> i) & 1u)
                                         d[32 * i] = o4[i];
                                     else if (ring_copy && ((in4 >> i) & 1u))
@@ -1333,7 +1350,7 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const float*
                         if (ring_row) {  // a ring row of the image: the input row itself
                             float* d = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride + rel[g];
 #pragma unroll
-                            for (int i = 0; i < 4; ++i)
+                            for (int i = 0; i < CPT; ++i)
                                 if ((in4 >> i) & 1u) d[32 * i] = w4[i];
                         }
                     }
@@ -1427,7 +1444,7 @@ __device__ __forceinline__ void rows_kernel_body(const Params& p, const float* w
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 20 + ntr, clock64());
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
-        if constexpr (!ALIGNED && RAD > MAX_RAD) {  // r > 4: one (ROW_EDGE) body
+        if constexpr (!ALIGNED && RAD > MAX_RAD && single_like(MODE)) {  // one (ROW_EDGE) body
             consume_item_lanes<MODE, RAD, true, SYM, SIG>(p, w, kd, it, ring, full, empty, sshift, slot, phase, gs);
         } else if constexpr (!ALIGNED) {
             if (item_rows_edge<MODE, RAD>(p, it))
