@@ -54,7 +54,7 @@ int fail_cuda(cudaError_t e, const std::string& what) {
 // while the common case costs no getenv() per knob.
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
-    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_lanes_wide = 0;
+    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_lanes_wide = 0, no_lean_single = 0;
     int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0, peer_timeout_ms = 0;
     int u8_occ2 = 0;
     int u8_gen = 0;
@@ -88,6 +88,7 @@ static Knobs read_knobs() {
         else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;
         else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;
         else if (name == "U8_OCC2") k.u8_occ2 = v;  // small u8 payloads on the 2-CTA build
+        else if (name == "NO_LEAN_SINGLE") k.no_lean_single = v;  // general 7x7 / 9x9 single pass on the aligned kernel
         else if (name == "NO_LANES_WIDE") k.no_lanes_wide = v;  // widths 11..21 on the plain kernels
         else if (name == "U8_GEN") k.u8_gen = v;    // the general-geometry u8 build on aligned rows too
     }
@@ -492,9 +493,9 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     const void* kern = nullptr;
     const bool peers_aligned = (!j.above || (aligned16(j.above) && j.above_ps % 4 == 0 && j.above_rs % 4 == 0)) &&
                                (!j.below || (aligned16(j.below) && j.below_ps % 4 == 0 && j.below_rs % 4 == 0));
-    const bool aligned = (j.C % 4 == 0) && aligned16(j.src) && aligned16(j.dst) && (j.sps % 4 == 0) &&
-                         (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) && peers_aligned &&
-                         kn.force_generic == 0 && !lanes_wide;
+    bool aligned = (j.C % 4 == 0) && aligned16(j.src) && aligned16(j.dst) && (j.sps % 4 == 0) &&
+                   (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) && peers_aligned &&
+                   kn.force_generic == 0 && !lanes_wide;
     // single pass with a mirror-symmetric dense matrix (bitwise K[i][j] == K[2r-i][j],
     // e.g. outer(w, w) of symmetric taps): the kernel that reuses mirrored products
     // (measured: -17% at cfg5 size; the same reuse in the two-pass column fold
@@ -511,6 +512,10 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
             }
         sym = rows ? (cols && !kn.no_colsym ? 2 : 1) : 0;
     }
+    // 7 x 7 and 9 x 9 matrices without mirror symmetry: the lane-strided kernel with
+    // the rolled row loop (kernels.cuh, lean_of) beats the aligned kernel's
+    // unrolled bodies, which overflow the instruction cache (-30% / -40%)
+    if (j.mode == MODE_SINGLE && rad >= SC_LEAN_MIN_RAD && sym == 0 && !kn.no_lean_single) aligned = false;
     // two-pass modes: mirror-symmetric taps (bitwise) share their products
     bool symw = !kn.no_sym && (j.mode == MODE_FUSED || j.mode == MODE_SPLITF) && j.taps;
     for (int i = 0; i < j.width && symw; ++i) symw = std::memcmp(&j.taps[i], &j.taps[j.width - 1 - i], sizeof(float)) == 0;

@@ -408,6 +408,14 @@ __host__ __device__ constexpr int groups_of(int mode, int rad = 0) {
 // widths 13..21 keeps 2r partial sums per column: one pair (2 columns) per thread
 // holds them without spilling (two pairs: 40..1470 bytes of spills at r = 6..10)
 __host__ __device__ constexpr int pairs_of(int mode, int rad) { return single_like(mode) && rad > 5 ? 1 : 2; }
+// lane-strided consumer, dense fold of 7 x 7 and wider matrices: rolled row loop, one
+// body. The unrolled bodies (4 rows x FAST / edge variants) of a 9 x 9 fold are 83 KB
+// of FP instructions and run out of the instruction cache: measured at 3 x 8192^2,
+// general matrix, W = 7: 1.01 -> 0.71 ms, W = 9: 1.97 -> 1.18 ms (tools/_w79.py)
+#ifndef SC_LEAN_MIN_RAD
+#define SC_LEAN_MIN_RAD 3
+#endif
+__host__ __device__ constexpr bool lean_of(int mode, int rad) { return single_like(mode) && rad >= SC_LEAN_MIN_RAD; }
 // output columns per consumer thread
 __host__ __device__ constexpr int cols_per_thread(int mode, int rad) {
     return rad <= MAX_RAD ? 4 * groups_of(mode, rad) : 2 * pairs_of(mode, rad) * groups_of(mode, rad);
@@ -1202,7 +1210,7 @@ __device__ __forceinline__ void consume_item_lanes(const Params& p, const float*
     constexpr int PAIRS = pairs_of(MODE, RAD);  // column pairs (c, c+32) per thread and group
     constexpr int CPT = 2 * PAIRS;
     constexpr unsigned ALLC = (1u << CPT) - 1u;
-    constexpr bool LEAN = RAD > MAX_RAD && single_like(MODE);
+    constexpr bool LEAN = lean_of(MODE, RAD);
     constexpr int ROW_UNROLL = LEAN ? 1 : SROWS;
     constexpr bool SYMW = !single_like(MODE) && SYM != 0;
     constexpr bool ROWSYM = SYM >= 1 && RAD <= MAX_RAD;
@@ -1444,7 +1452,7 @@ __device__ __forceinline__ void rows_kernel_body(const Params& p, const float* w
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 20 + ntr, clock64());
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
-        if constexpr (!ALIGNED && RAD > MAX_RAD && single_like(MODE)) {  // one (ROW_EDGE) body
+        if constexpr (!ALIGNED && lean_of(MODE, RAD)) {  // one (ROW_EDGE) body
             consume_item_lanes<MODE, RAD, true, SYM, SIG>(p, w, kd, it, ring, full, empty, sshift, slot, phase, gs);
         } else if constexpr (!ALIGNED) {
             if (item_rows_edge<MODE, RAD>(p, it))
