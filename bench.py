@@ -544,8 +544,9 @@ def main():
         img = src.clone()
         scr = torch.empty_like(src)
 
-        def ev_ms(fn, n=10):
-            fn()
+        def ev_ms(fn, n=20):
+            for _ in range(3):  # plan, snapshot pool and clocks settled
+                fn()
             torch.cuda.synchronize()
             a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a_ev.record(stream)
