@@ -28,10 +28,12 @@ def bits(a, b):
 shapes = st.tuples(st.integers(1, 3), st.integers(5, 90), st.integers(5, 300))
 _N = int(os.environ.get("SC_HYPO_SCALE", "1"))  # stress runs: multiply the example counts
 widths = st.sampled_from([1, 3, 5, 7, 9])
+# plus the lane-strided kernels' widths (11..21) and the first plain-kernel width
+widths_any = st.sampled_from([1, 3, 5, 7, 9, 11, 13, 15, 17, 19, 21, 23])
 
 
 @settings(max_examples=200 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
-@given(shape=shapes, width=widths, seed=st.integers(0, 2**32 - 1), generic=st.booleans(),
+@given(shape=shapes, width=widths_any, seed=st.integers(0, 2**32 - 1), generic=st.booleans(),
        extended=st.booleans())
 def test_random_two_pass_and_passes(oracle, monkeypatch, shape, width, seed, generic, extended):
     _need_gpu()
@@ -62,7 +64,7 @@ def test_random_two_pass_and_passes(oracle, monkeypatch, shape, width, seed, gen
 
 
 @settings(max_examples=150 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
-@given(shape=shapes, width=widths, seed=st.integers(0, 2**32 - 1), generic=st.booleans(), copy=st.booleans(),
+@given(shape=shapes, width=widths_any, seed=st.integers(0, 2**32 - 1), generic=st.booleans(), copy=st.booleans(),
        sym=st.booleans())
 def test_random_single_pass(oracle, monkeypatch, shape, width, seed, generic, copy, sym):
     """sym: mirror-symmetric taps, so the dense matrix takes the product-reuse kernel."""
