@@ -22,7 +22,7 @@ LIB = os.path.join(PKG, "libsepconv_b200.so")
 OBJ = os.path.join(PKG, "csrc", "_obj")
 
 SOURCES = ["capi.cu", "stream.cu", "kern_aux.cu", "kern_fused.cu", "kern_hpass.cu", "kern_vpass.cu", "kern_single.cu", "kern_u8.cu",
-           "kern_wide.cu", "kern_lanes_wide.cu", "kern_lanes_wide_single.cu", "nccl_band.cu"]
+           "kern_wide.cu", "kern_lanes_wide.cu", "kern_lanes_wide2.cu", "kern_lanes_wide_single.cu", "nccl_band.cu"]
 HEADERS = ["kernels.cuh", "direct.cuh", "launch.h"]
 
 NVCC_FLAGS = [

@@ -89,7 +89,7 @@ static Knobs read_knobs() {
         else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;
         else if (name == "U8_OCC2") k.u8_occ2 = v;  // small u8 payloads on the 2-CTA build
         else if (name == "NO_LEAN_SINGLE") k.no_lean_single = v;  // general 7x7 / 9x9 single pass on the aligned kernel
-        else if (name == "NO_LANES_WIDE") k.no_lanes_wide = v;  // widths 11..21 on the plain kernels
+        else if (name == "NO_LANES_WIDE") k.no_lanes_wide = v;  // widths 11..31 on the plain kernels
         else if (name == "U8_GEN") k.u8_gen = v;    // the general-geometry u8 build on aligned rows too
     }
     return k;
@@ -269,7 +269,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
     const int lags = stage_lags(j.mode, rad);
     int ns_req = kn.ns ? kn.ns : 16 / SROWS;
     if (ns_req < lags + 2) ns_req = lags + 2;
-    // widths 11..21: the fused kernel holds ceil(r/4) stages back for the ring
+    // widths 11..31: the fused kernel holds ceil(r/4) stages back for the ring
     // columns; keep two stages in flight beyond them (measured -2% at W = 11)
     if (rad > MAX_RAD && !kn.ns && ns_req < lags + 3) ns_req = lags + 3;
     if (ns_req > 32) ns_req = 32;
@@ -484,7 +484,7 @@ static int cached_plan(const RowsJob& j, const void* kern, bool aligned, bool di
 int launch_rows(const RowsJob& j, cudaStream_t s) {
     const int rad = j.width / 2;
     const Knobs kn = read_knobs();
-    // widths 11..21: the lane-strided kernels (any alignment); wider ones, and the
+    // widths 11..31: the lane-strided kernels (any alignment); wider ones, and the
     // peer-band / in-place modes above width 9, the plain kernels of kern_wide.cu
     const bool lanes_wide = j.width > MAX_W && j.width <= MAX_W_LANES && !kn.no_lanes_wide && !j.above && !j.below &&
                             !j.sig_self &&
@@ -520,7 +520,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     bool symw = !kn.no_sym && (j.mode == MODE_FUSED || j.mode == MODE_SPLITF) && j.taps;
     for (int i = 0; i < j.width && symw; ++i) symw = std::memcmp(&j.taps[i], &j.taps[j.width - 1 - i], sizeof(float)) == 0;
     if (lanes_wide) {
-        kern = j.mode == MODE_SINGLE ? kernel_lanes_wide_single(rad) : kernel_lanes_wide(j.mode, rad, symw);
+        kern = j.mode == MODE_SINGLE ? kernel_lanes_wide_single(rad)
+                                     : (rad <= 10 ? kernel_lanes_wide(j.mode, rad, symw) : kernel_lanes_wide2(j.mode, rad, symw));
     } else
     switch (j.mode) {
         case MODE_FUSED: kern = kernel_fused(rad, aligned, symw, j.sig_self != nullptr); break;

@@ -1,5 +1,5 @@
-// Instantiates the widths 11..21 (r = 5..10) kernels of the two-pass modes (r = 11..15:
-// kern_lanes_wide2.cu): the
+// Instantiates the widths 23..31 (r = 11..15) kernels of the two-pass modes (r = 5..10:
+// kern_lanes_wide.cu): the
 // generic TMA producer + the lane-strided consumer (kernels.cuh,
 // consume_item_lanes), any row alignment. The single pass is in
 // kern_lanes_wide_single.cu (one TU per family keeps nvcc builds parallel).
@@ -9,7 +9,7 @@
 namespace sc {
 
 // symw: mirror-symmetric taps (w[j] == w[2r-j] bitwise): products shared by value
-const void* kernel_lanes_wide(int mode, int rad, bool symw) {
+const void* kernel_lanes_wide2(int mode, int rad, bool symw) {
 #define SC_K(R)                                                                                       \
     case R:                                                                                           \
         switch (mode) {                                                                               \
@@ -21,12 +21,11 @@ const void* kernel_lanes_wide(int mode, int rad, bool symw) {
             default: return nullptr;                                                                  \
         }
     switch (rad) {
-        SC_K(5)
-        SC_K(6)
-        SC_K(7)
-        SC_K(8)
-        SC_K(9)
-        SC_K(10)
+        SC_K(11)
+        SC_K(12)
+        SC_K(13)
+        SC_K(14)
+        SC_K(15)
         default:
             return nullptr;
     }

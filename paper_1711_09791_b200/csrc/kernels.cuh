@@ -77,11 +77,11 @@ constexpr int F_L2_EVICT_FIRST = 0x100;  // evict_first hint on the row loads (d
 constexpr int HALO = 4;       // smem columns kept either side of a strip (supports r <= 4)
 constexpr int MAX_RAD = 4;
 constexpr int MAX_W = 2 * MAX_RAD + 1;
-constexpr int MAX_W_WIDE = 255;  // widths 23..255 run the plain kernels of kern_wide.cu
-// widths 11..21 (r = 5..10): the lane-strided consumer (consume_item_lanes) with a
+constexpr int MAX_W_WIDE = 255;  // widths 33..255 run the plain kernels of kern_wide.cu
+// widths 11..31 (r = 5..15): the lane-strided consumer (consume_item_lanes) with a
 // wider smem halo and the taps in ParamsW -- its window is streamed from shared
 // memory tap by tap, so only the column fold's 2r partial sums live in registers
-constexpr int MAX_RAD_LANES = 10;
+constexpr int MAX_RAD_LANES = 15;
 constexpr int MAX_W_LANES = 2 * MAX_RAD_LANES + 1;
 // smem columns kept either side of a strip: a multiple of 4 (16-B copies) >= r
 __host__ __device__ constexpr int halo_of(int rad) { return rad <= 4 ? 4 : ((rad + 3) / 4) * 4; }
@@ -163,7 +163,7 @@ struct Params {
     unsigned long long sig_n_above, sig_n_below;
 };
 
-// Parameters of the widths 11..21 kernels: Params plus their taps (kept out of
+// Parameters of the widths 11..31 kernels: Params plus their taps (kept out of
 // Params so the r <= 4 kernels' parameter block, and their launch cost, stay as they are).
 struct ParamsW : Params {
     float wide_w[MAX_W_LANES];
@@ -404,10 +404,13 @@ __host__ __device__ constexpr int stage_lags(int mode, int rad) {
 __host__ __device__ constexpr int groups_of(int mode, int rad = 0) {
     return single_like(mode) && rad <= MAX_RAD ? SC_GROUPS_SINGLE : SC_GROUPS;
 }
-// lane-strided consumer: column pairs per thread and group. The dense fold of
-// widths 13..21 keeps 2r partial sums per column: one pair (2 columns) per thread
-// holds them without spilling (two pairs: 40..1470 bytes of spills at r = 6..10)
-__host__ __device__ constexpr int pairs_of(int mode, int rad) { return single_like(mode) && rad > 5 ? 1 : 2; }
+// lane-strided consumer: column pairs per thread and group. The column / dense fold
+// keeps 2r partial sums per column in registers: one pair (2 columns) per thread
+// holds them without spilling for the dense fold from r = 6 (two pairs: 40..1470
+// bytes of spills at r = 6..10) and for the two-pass modes from r = 11
+__host__ __device__ constexpr int pairs_of(int mode, int rad) {
+    return (single_like(mode) ? rad > 5 : rad > 10) ? 1 : 2;
+}
 // lane-strided consumer, dense fold of 7 x 7 and wider matrices: rolled row loop, one
 // body. The unrolled bodies (4 rows x FAST / edge variants) of a 9 x 9 fold are 83 KB
 // of FP instructions and run out of the instruction cache: measured at 3 x 8192^2,
@@ -1485,11 +1488,11 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
     rows_kernel_body<MODE, RAD, ALIGNED, SYM, SIG>(p, p.w, p.k);
 }
 
-// Widths 11..21 (r = 5..10), rows of any alignment: the generic producer and the
+// Widths 11..31 (r = 5..15), rows of any alignment: the generic producer and the
 // lane-strided consumer with the taps of ParamsW.
 template <int MODE, int RAD, int SYM = 0>
 __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_lanes_wide_kernel(const __grid_constant__ ParamsW p) {
-    static_assert(RAD > MAX_RAD && RAD <= MAX_RAD_LANES, "r = 5..10");
+    static_assert(RAD > MAX_RAD && RAD <= MAX_RAD_LANES, "r = 5..15");
     rows_kernel_body<MODE, RAD, false, SYM, false>(p, p.wide_w, p.wide_k);
 }
 

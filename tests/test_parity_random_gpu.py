@@ -28,8 +28,8 @@ def bits(a, b):
 shapes = st.tuples(st.integers(1, 3), st.integers(5, 90), st.integers(5, 300))
 _N = int(os.environ.get("SC_HYPO_SCALE", "1"))  # stress runs: multiply the example counts
 widths = st.sampled_from([1, 3, 5, 7, 9])
-# plus the lane-strided kernels' widths (11..21) and the first plain-kernel width
-widths_any = st.sampled_from([1, 3, 5, 7, 9, 11, 13, 15, 17, 19, 21, 23])
+# plus the lane-strided kernels' widths (11..31) and the first plain-kernel width
+widths_any = st.sampled_from([1, 3, 5, 7, 9, 11, 13, 15, 17, 19, 21, 23, 25, 27, 29, 31, 33])
 
 
 @settings(max_examples=200 * _N, deadline=None, suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])

@@ -16,12 +16,12 @@ def t(fn, n=10):
     e.record(); e.synchronize()
     return s.elapsed_time(e) / n
 FP = 126.7 * 148 * 1.965e9
-for W in (5, 9, 11, 13, 15, 21, 31, 63):
+for W in (5, 9, 11, 13, 15, 21, 25, 31, 33, 63):
     w = np.random.default_rng(W).standard_normal(W).astype(np.float32)
     ms = t(lambda: dev.two_pass(x, w, y))
     ops = 3 * R * C * 2 * (2 * W - 1)
     rec = {"W": W, "two_pass_ms": round(ms, 4), "hbm_floor_ms": round(24 * R * C / 6535.7e6, 4), "fp32_floor_ms": round(ops / FP * 1e3, 4)}
-    if W <= 15:
+    if W <= 15 or W == 31:
         k = np.outer(w, w).astype(np.float32)
         ms1 = t(lambda: dev.single_pass(x, k, y), n=3)
         rec["single_ms"] = round(ms1, 4)
