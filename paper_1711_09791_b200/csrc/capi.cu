@@ -324,6 +324,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
         const int rows = hi1 - lo1;
         for (int c : cand) {
             if (forced && c != forced) continue;
+            if (rad > MAX_RAD && 32 + c > WIDE_MAXT) continue;  // the wide kernels' launch bound
             const int tw_ = COLS_PER_THREAD * c;
             const int strips = (j.C + tw_ - 1) / tw_;
             const long long units = (long long)j.nplanes * strips;
@@ -488,7 +489,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     // peer-band / in-place modes above width 9, the plain kernels of kern_wide.cu
     const bool lanes_wide = j.width > MAX_W && j.width <= MAX_W_LANES && !kn.no_lanes_wide && !j.above && !j.below &&
                             !j.sig_self &&
-                            (j.mode == MODE_FUSED || j.mode == MODE_HPASS || j.mode == MODE_VPASS || j.mode == MODE_SINGLE);
+                            (j.mode == MODE_FUSED || j.mode == MODE_HPASS || j.mode == MODE_VPASS ||
+                             (j.mode == MODE_SINGLE && rad <= MAX_RAD_LANES_SINGLE));
     if (j.width > MAX_W && !lanes_wide) return launch_wide(j, s);
     const void* kern = nullptr;
     const bool peers_aligned = (!j.above || (aligned16(j.above) && j.above_ps % 4 == 0 && j.above_rs % 4 == 0)) &&

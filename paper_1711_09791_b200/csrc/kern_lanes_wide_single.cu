@@ -1,4 +1,5 @@
-// Instantiates the widths 11..31 (r = 5..15) single-pass kernels (dense
+// Instantiates the widths 11..21 (r = 5..10) single-pass kernels (wider dense folds
+// spill even at 255 registers: they stay on the plain kernel of kern_wide.cu) (dense
 // (2r+1)^2 fold, S/conv.py:86-114): generic TMA producer + lane-strided consumer
 // (kernels.cuh, consume_item_lanes), any row alignment.
 #include "kernels.cuh"
@@ -14,11 +15,6 @@ const void* kernel_lanes_wide_single(int rad) {
         case 8: return (const void*)sepconv_lanes_wide_kernel<MODE_SINGLE, 8, 0>;
         case 9: return (const void*)sepconv_lanes_wide_kernel<MODE_SINGLE, 9, 0>;
         case 10: return (const void*)sepconv_lanes_wide_kernel<MODE_SINGLE, 10, 0>;
-        case 11: return (const void*)sepconv_lanes_wide_kernel<MODE_SINGLE, 11, 0>;
-        case 12: return (const void*)sepconv_lanes_wide_kernel<MODE_SINGLE, 12, 0>;
-        case 13: return (const void*)sepconv_lanes_wide_kernel<MODE_SINGLE, 13, 0>;
-        case 14: return (const void*)sepconv_lanes_wide_kernel<MODE_SINGLE, 14, 0>;
-        case 15: return (const void*)sepconv_lanes_wide_kernel<MODE_SINGLE, 15, 0>;
         default: return nullptr;
     }
 }

@@ -82,7 +82,11 @@ constexpr int MAX_W_WIDE = 255;  // widths 33..255 run the plain kernels of kern
 // wider smem halo and the taps in ParamsW -- its window is streamed from shared
 // memory tap by tap, so only the column fold's 2r partial sums live in registers
 constexpr int MAX_RAD_LANES = 15;
+constexpr int MAX_RAD_LANES_SINGLE = 10;  // the dense fold: up to 21 x 21 (wider ones spill)
 constexpr int MAX_W_LANES = 2 * MAX_RAD_LANES + 1;
+// their CTAs: the producer warp + at most 4 consumer warps, so that ptxas may use up to
+// 255 registers (the dense fold at r = 11..15 spilled under the 288-thread bound)
+constexpr int WIDE_MAXT = 32 + 128;
 // smem columns kept either side of a strip: a multiple of 4 (16-B copies) >= r
 __host__ __device__ constexpr int halo_of(int rad) { return rad <= 4 ? 4 : ((rad + 3) / 4) * 4; }
 constexpr int MAX_THREADS = 32 + 256;  // producer warp + up to 8 consumer warps
@@ -1491,7 +1495,7 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
 // Widths 11..31 (r = 5..15), rows of any alignment: the generic producer and the
 // lane-strided consumer with the taps of ParamsW.
 template <int MODE, int RAD, int SYM = 0>
-__global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_lanes_wide_kernel(const __grid_constant__ ParamsW p) {
+__global__ void __launch_bounds__(WIDE_MAXT, 1) sepconv_lanes_wide_kernel(const __grid_constant__ ParamsW p) {
     static_assert(RAD > MAX_RAD && RAD <= MAX_RAD_LANES, "r = 5..15");
     rows_kernel_body<MODE, RAD, false, SYM, false>(p, p.wide_w, p.wide_k);
 }

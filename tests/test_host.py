@@ -268,6 +268,7 @@ def test_packed_math_keeps_two_roundings():
         # symmetric-tap u8 kernels reuse mirrored products: fewer FMUL2 than adds by
         # design, at most 2 adds per product
         sym = (re.search(r"sepconv_rows_kernelILi\d+ELi\d+ELb[01]ELi[12]E", fn) is not None
+               or re.search(r"sepconv_lanes_wide_kernelILi\d+ELi\d+ELi[12]E", fn) is not None  # widths 11..31
                or re.search(r"sepconv_u8_kernelILi\d+ELb1E", fn) is not None)  # u8 with symmetric taps
         # products of odd-start window pairs are two scalar FMULs (prod2)
         products = fmul2 + fmul // 2
