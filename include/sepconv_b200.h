@@ -108,7 +108,7 @@ int sc_two_pass_band_peer_f32(const float *src, float *dst, int nplanes, int glo
  * finished step e-1, so ping-pong buffers (step e writes what neighbours read in
  * step e-1) are safe too. sig_err (host-mapped u32, may be NULL) is set when a
  * wait outlives SC_PEER_TIMEOUT_MS (default 20000 ms); the kernel then goes on
- * rather than hang the GPU. Widths up to 9. */
+ * rather than hang the GPU. Widths up to 9 (the NCCL band plan: up to 31). */
 int sc_two_pass_band_peer_sig_f32(const float *src, float *dst, int nplanes, int global_rows, int cols,
                                   int64_t src_plane_stride, int64_t dst_plane_stride, int64_t src_row_stride,
                                   int64_t dst_row_stride, int src_row0, int src_rows, const float *above,

@@ -485,10 +485,10 @@ static int cached_plan(const RowsJob& j, const void* kern, bool aligned, bool di
 int launch_rows(const RowsJob& j, cudaStream_t s) {
     const int rad = j.width / 2;
     const Knobs kn = read_knobs();
-    // widths 11..31: the lane-strided kernels (any alignment); wider ones, and the
-    // peer-band / in-place modes above width 9, the plain kernels of kern_wide.cu
-    const bool lanes_wide = j.width > MAX_W && j.width <= MAX_W_LANES && !kn.no_lanes_wide && !j.above && !j.below &&
-                            !j.sig_self &&
+    // widths 11..31: the lane-strided kernels (any alignment, neighbouring bands'
+    // halo rows included); wider ones, and the signalled peer bands / in-place
+    // modes above width 9, the plain kernels of kern_wide.cu
+    const bool lanes_wide = j.width > MAX_W && j.width <= MAX_W_LANES && !kn.no_lanes_wide && !j.sig_self &&
                             (j.mode == MODE_FUSED || j.mode == MODE_HPASS || j.mode == MODE_VPASS ||
                              (j.mode == MODE_SINGLE && rad <= MAX_RAD_LANES_SINGLE));
     if (j.width > MAX_W && !lanes_wide) return launch_wide(j, s);
@@ -1181,7 +1181,7 @@ static int pass_common(int mode, const float* src, float* dst, int nplanes, int 
     j.taps = taps;
     j.dense = dense;
     if (single_like(mode)) {
-        static float zeros[MAX_W] = {0};
+        static float zeros[MAX_W_WIDE] = {0};
         j.taps = zeros;
     }
     if (mode == MODE_SINGLECB) {  // second destination: the source image itself (copy-back, in place)

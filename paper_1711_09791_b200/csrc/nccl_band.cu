@@ -96,7 +96,7 @@ struct BandPlan {
     float* dst = nullptr;
     int P = 0, R = 0, C = 0, r = 0, lo = 0, hi = 0, above = -1, below = -1;
     long long sps = 0, dps = 0, srs = 0, drs = 0;
-    float taps[MAX_W] = {};
+    float taps[MAX_W_LANES] = {};
     int width = 0, flags = 0;
     float *send_top = nullptr, *send_bot = nullptr, *recv_top = nullptr, *recv_bot = nullptr;
     cudaStream_t cs = nullptr;
@@ -284,8 +284,8 @@ int sc_band_plan_create(void* comm, const float* src, float* dst, int nplanes, i
     if (!plan_out || !src || !dst || !taps) return fail_arg("null argument");
     *plan_out = nullptr;
     if (width < 1 || width % 2 == 0) return fail_arg("kernel width must be odd and >= 1");
-    if (width > MAX_W) {
-        set_error("NCCL band plans support widths up to 9");
+    if (width > MAX_W_LANES) {
+        set_error("NCCL band plans support widths up to 31");
         return SC_UNSUPPORTED_WIDTH;
     }
     if (nplanes < 1 || cols < 1 || global_rows < 1) return fail_arg("dimensions must be positive");

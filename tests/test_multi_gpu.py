@@ -105,8 +105,8 @@ def test_nccl_plan_rejects_bad_geometry(env):
     with pytest.raises(InvalidArgumentError):  # a middle band without a neighbour above
         multi.NcclBandStepper(src, dst, multi.Band(0, 1, 100, 2, 30, 70), np.ones(5, np.float32), comm=comm,
                               rank_above=-1, rank_below=0)
-    with pytest.raises(UnsupportedWidthError):
-        multi.NcclBandStepper(src, dst, multi.Band(0, 1, 100, 5, 30, 70), np.ones(11, np.float32), comm=comm)
+    with pytest.raises(UnsupportedWidthError):  # widths up to 31 (the lane-strided kernels)
+        multi.NcclBandStepper(src, dst, multi.Band(0, 1, 100, 16, 30, 70), np.ones(33, np.float32), comm=comm)
 
 
 def _host_words(n):
@@ -242,7 +242,7 @@ from hypothesis import strategies as st  # noqa: E402
 
 @settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow,
                                                                  HealthCheck.function_scoped_fixture])
-@given(P=st.integers(1, 3), R=st.integers(20, 90), C=st.integers(9, 200), width=st.sampled_from([3, 5, 7, 9]),
+@given(P=st.integers(1, 3), R=st.integers(20, 90), C=st.integers(9, 200), width=st.sampled_from([3, 5, 7, 9, 11, 15]),
        cut=st.floats(0.1, 0.9), frac=st.floats(0.2, 0.8), top=st.booleans(), bot=st.booleans(),
        seed=st.integers(0, 2**20), extended=st.booleans())
 def test_random_nccl_plan_self_exchange(env, oracle, P, R, C, width, cut, frac, top, bot, seed, extended):
