@@ -412,8 +412,11 @@ __host__ __device__ constexpr int groups_of(int mode, int rad = 0) {
 // keeps 2r partial sums per column in registers: one pair (2 columns) per thread
 // holds them without spilling for the dense fold from r = 6 (two pairs: 40..1470
 // bytes of spills at r = 6..10) and for the two-pass modes from r = 11
+#ifndef SC_TWO_PAIRS_MAX_RAD
+#define SC_TWO_PAIRS_MAX_RAD 10
+#endif
 __host__ __device__ constexpr int pairs_of(int mode, int rad) {
-    return (single_like(mode) ? rad > 5 : rad > 10) ? 1 : 2;
+    return (single_like(mode) ? rad > 5 : rad > SC_TWO_PAIRS_MAX_RAD) ? 1 : 2;
 }
 // lane-strided consumer, dense fold of 7 x 7 and wider matrices: rolled row loop, one
 // body. The unrolled bodies (4 rows x FAST / edge variants) of a 9 x 9 fold are 83 KB

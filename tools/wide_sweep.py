@@ -18,7 +18,7 @@ def t(fn, n=10):
 grid = [{}]
 for ns in (5, 6, 8): grid.append({"SC_NS": str(ns)})
 for bh, bh2 in ((128, 32), (256, 64)): grid.append({"SC_BAND_H": str(bh), "SC_BAND_H2": str(bh2), "SC_NS": "6"})
-for nt in (64, 96, 256): grid.append({"SC_NT": str(nt), "SC_NS": "6", "SC_BAND_H": "128", "SC_BAND_H2": "32"})
+for nt in (64, 96): grid.append({"SC_NT": str(nt), "SC_NS": "6", "SC_BAND_H": "128", "SC_BAND_H2": "32"})
 for W in [int(v) for v in os.environ.get("WIDTHS", "11,15,21").split(",")]:
     w = np.random.default_rng(W).standard_normal(W).astype(np.float32)
     k = np.outer(w, w).astype(np.float32)
