@@ -54,7 +54,7 @@ int fail_cuda(cudaError_t e, const std::string& what) {
 // while the common case costs no getenv() per knob.
 struct Knobs {
     int force_generic = 0, direct = 0, l2_evict_first = 0, debug_plan = 0;
-    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_lanes_wide = 0, no_lean_single = 0;
+    int occ = 0, ns = 0, nt = 0, band_h = 0, band_h2 = 0, tail_waves = 0, exact_waves = 0, ipc = 0, no_lanes_wide = 0, no_lean_single = 0, no_wide_adj = 0;
     int no_sym = 0, no_colsym = 0, no_pdl = 0, split_passes = 0, snapshot_fail = 0, peer_timeout_ms = 0;
     int u8_occ2 = 0;
     int u8_gen = 0;
@@ -88,6 +88,7 @@ static Knobs read_knobs() {
         else if (name == "SNAPSHOT_FAIL") k.snapshot_fail = v;
         else if (name == "PEER_TIMEOUT_MS") k.peer_timeout_ms = v;
         else if (name == "U8_OCC2") k.u8_occ2 = v;  // small u8 payloads on the 2-CTA build
+        else if (name == "NO_WIDE_ADJ") k.no_wide_adj = v;  // widths 11..21 on aligned rows: the lane-strided consumer
         else if (name == "NO_LEAN_SINGLE") k.no_lean_single = v;  // general 7x7 / 9x9 single pass on the aligned kernel
         else if (name == "NO_LANES_WIDE") k.no_lanes_wide = v;  // widths 11..31 on the plain kernels
         else if (name == "U8_GEN") k.u8_gen = v;    // the general-geometry u8 build on aligned rows too
@@ -255,7 +256,7 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
                      Plan& pl) {
     const int rad = j.width / 2;
     const bool seg2 = j.out_hi2 > j.out_lo2;
-    const int COLS_PER_THREAD = cols_per_thread(j.mode, rad);  // 4-column groups (r > 4: column pairs) per consumer thread
+    const int COLS_PER_THREAD = cols_per_thread(j.mode, rad, aligned);  // 4-column groups (r > 4: column pairs) per consumer thread
     const int HL = halo_of(rad);
     int nt = 0, threads = 0, ns = 0, tw = 0;
     size_t smem = 0;
@@ -324,7 +325,6 @@ static int plan_rows(const RowsJob& j, const void* kern, bool aligned, bool dire
         const int rows = hi1 - lo1;
         for (int c : cand) {
             if (forced && c != forced) continue;
-            if (rad > MAX_RAD && 32 + c > WIDE_MAXT) continue;  // the wide kernels' launch bound
             const int tw_ = COLS_PER_THREAD * c;
             const int strips = (j.C + tw_ - 1) / tw_;
             const long long units = (long long)j.nplanes * strips;
@@ -497,7 +497,9 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
                                (!j.below || (aligned16(j.below) && j.below_ps % 4 == 0 && j.below_rs % 4 == 0));
     bool aligned = (j.C % 4 == 0) && aligned16(j.src) && aligned16(j.dst) && (j.sps % 4 == 0) &&
                    (j.dps % 4 == 0) && (j.srs % 4 == 0) && (j.drs % 4 == 0) && peers_aligned &&
-                   kn.force_generic == 0 && !lanes_wide;
+                   kn.force_generic == 0 &&
+                   // widths 11..31: aligned rows have their own consumer in the two-pass modes up to r = 10
+                   (!lanes_wide || (j.mode != MODE_SINGLE && rad <= MAX_RAD_ADJ && !kn.no_wide_adj));
     // single pass with a mirror-symmetric dense matrix (bitwise K[i][j] == K[2r-i][j],
     // e.g. outer(w, w) of symmetric taps): the kernel that reuses mirrored products
     // (measured: -17% at cfg5 size; the same reuse in the two-pass column fold
@@ -523,7 +525,8 @@ int launch_rows(const RowsJob& j, cudaStream_t s) {
     for (int i = 0; i < j.width && symw; ++i) symw = std::memcmp(&j.taps[i], &j.taps[j.width - 1 - i], sizeof(float)) == 0;
     if (lanes_wide) {
         kern = j.mode == MODE_SINGLE ? kernel_lanes_wide_single(rad)
-                                     : (rad <= 10 ? kernel_lanes_wide(j.mode, rad, symw) : kernel_lanes_wide2(j.mode, rad, symw));
+                                     : (rad <= 10 ? kernel_lanes_wide(j.mode, rad, symw, aligned)
+                                                  : kernel_lanes_wide2(j.mode, rad, symw));
     } else
     switch (j.mode) {
         case MODE_FUSED: kern = kernel_fused(rad, aligned, symw, j.sig_self != nullptr); break;

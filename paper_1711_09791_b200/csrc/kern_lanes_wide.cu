@@ -8,18 +8,24 @@
 
 namespace sc {
 
-// symw: mirror-symmetric taps (w[j] == w[2r-j] bitwise): products shared by value
-const void* kernel_lanes_wide(int mode, int rad, bool symw) {
-#define SC_K(R)                                                                                       \
-    case R:                                                                                           \
-        switch (mode) {                                                                               \
-            case MODE_FUSED:                                                                          \
-                return symw ? (const void*)sepconv_lanes_wide_kernel<MODE_FUSED, R, 1>                \
-                            : (const void*)sepconv_lanes_wide_kernel<MODE_FUSED, R, 0>;               \
-            case MODE_HPASS: return (const void*)sepconv_lanes_wide_kernel<MODE_HPASS, R, 0>;         \
-            case MODE_VPASS: return (const void*)sepconv_lanes_wide_kernel<MODE_VPASS, R, 0>;         \
-            default: return nullptr;                                                                  \
-        }
+// symw: mirror-symmetric taps (w[j] == w[2r-j] bitwise): products shared by value;
+// aligned: 16-B aligned rows -> the adjacent-column consumer (consume_item_adj)
+const void* kernel_lanes_wide(int mode, int rad, bool symw, bool aligned) {
+#define SC_KA(R, A)                                                                                   \
+    switch (mode) {                                                                                   \
+        case MODE_FUSED:                                                                              \
+            return symw ? (const void*)sepconv_lanes_wide_kernel<MODE_FUSED, R, 1, A>                 \
+                        : (const void*)sepconv_lanes_wide_kernel<MODE_FUSED, R, 0, A>;                \
+        case MODE_HPASS: return (const void*)sepconv_lanes_wide_kernel<MODE_HPASS, R, 0, A>;          \
+        case MODE_VPASS: return (const void*)sepconv_lanes_wide_kernel<MODE_VPASS, R, 0, A>;          \
+        default: return nullptr;                                                                      \
+    }
+#define SC_K(R)            \
+    case R:                \
+        if (aligned) {     \
+            SC_KA(R, true) \
+        }                  \
+        SC_KA(R, false)
     switch (rad) {
         SC_K(5)
         SC_K(6)
@@ -31,6 +37,7 @@ const void* kernel_lanes_wide(int mode, int rad, bool symw) {
             return nullptr;
     }
 #undef SC_K
+#undef SC_KA
 }
 
 }  // namespace sc

@@ -82,11 +82,9 @@ constexpr int MAX_W_WIDE = 255;  // widths 33..255 run the plain kernels of kern
 // wider smem halo and the taps in ParamsW -- its window is streamed from shared
 // memory tap by tap, so only the column fold's 2r partial sums live in registers
 constexpr int MAX_RAD_LANES = 15;
+constexpr int MAX_RAD_ADJ = 10;           // aligned rows, two-pass modes: the adjacent-column consumer up to 21 taps
 constexpr int MAX_RAD_LANES_SINGLE = 10;  // the dense fold: up to 21 x 21 (wider ones spill)
 constexpr int MAX_W_LANES = 2 * MAX_RAD_LANES + 1;
-// their CTAs: the producer warp + at most 4 consumer warps, so that ptxas may use up to
-// 255 registers (the dense fold at r = 11..15 spilled under the 288-thread bound)
-constexpr int WIDE_MAXT = 32 + 128;
 // smem columns kept either side of a strip: a multiple of 4 (16-B copies) >= r
 __host__ __device__ constexpr int halo_of(int rad) { return rad <= 4 ? 4 : ((rad + 3) / 4) * 4; }
 constexpr int MAX_THREADS = 32 + 256;  // producer warp + up to 8 consumer warps
@@ -426,9 +424,9 @@ __host__ __device__ constexpr int pairs_of(int mode, int rad) {
 #define SC_LEAN_MIN_RAD 3
 #endif
 __host__ __device__ constexpr bool lean_of(int mode, int rad) { return single_like(mode) && rad >= SC_LEAN_MIN_RAD; }
-// output columns per consumer thread
-__host__ __device__ constexpr int cols_per_thread(int mode, int rad) {
-    return rad <= MAX_RAD ? 4 * groups_of(mode, rad) : 2 * pairs_of(mode, rad) * groups_of(mode, rad);
+// output columns per consumer thread (aligned: the adjacent-column consumers)
+__host__ __device__ constexpr int cols_per_thread(int mode, int rad, bool aligned = false) {
+    return rad <= MAX_RAD || aligned ? 4 * groups_of(mode, rad) : 2 * pairs_of(mode, rad) * groups_of(mode, rad);
 }
 
 // Shared-memory row width (floats): the segment [x0-4, x0+TW+4), plus room for
@@ -1114,6 +1112,155 @@ __device__ __forceinline__ void consume_item(const Params& p, const Item& it, co
 }
 
 // ---------------------------------------------------------------------------
+// Consumer of 16-B aligned rows at widths 11..21 (r = 5..10), two-pass modes:
+// adjacent columns as consume_item, with a window of 4 + 2*halo_of(r) samples per
+// row (5-7 x LDS.128 for 4 outputs, where the lane-strided consumer reads 4*(2r+1)
+// words one by one: ncu had its shared-memory pipe 67% busy at W = 11, next to an
+// FMA pipe at 61%), products of odd-start window pairs as two scalar multiplies
+// (no pair-forming moves), the column fold through the same shift register.
+
+template <int RAD, bool SYMW, int HL>
+__device__ __forceinline__ F4 row_pass_win(const float (&win)[4 + 2 * HL], const float* w, float one) {
+    F4 h;
+    const float2 one2 = make_float2(one, one);
+    auto pairprod = [&](int idx, float kv) {
+        if (idx & 1) return make_float2(__fmul_rn(win[idx], kv), __fmul_rn(win[idx + 1], kv));
+        return __fmul2_rn(make_float2(win[idx], win[idx + 1]), make_float2(kv, kv));
+    };
+#pragma unroll
+    for (int c = 0; c < 4; c += 2) {
+        const int o = HL - RAD + c;
+        float2 acc = pairprod(o, w[0]);
+#pragma unroll
+        for (int m = 1; m <= 2 * RAD; ++m) acc = add2p(acc, pairprod(o + m, w[tap_ix<RAD, SYMW>(m)]), one2);
+        h.v[c] = acc.x;
+        h.v[c + 1] = acc.y;
+    }
+    return h;
+}
+
+template <int MODE, int RAD, bool ROW_EDGE, int SYM>
+__device__ __forceinline__ void consume_item_adj(const Params& p, const float* w, const Item& it, const float* ring,
+                                                 uint64_t* full, uint64_t* empty, int& slot, uint32_t& phase, int& gs) {
+    static_assert(MODE == MODE_FUSED || MODE == MODE_HPASS || MODE == MODE_VPASS, "two-pass modes only");
+    constexpr int NACC = 2 * RAD;
+    constexpr bool SYMW = SYM != 0;
+    constexpr int LAGS = stage_lags(MODE, RAD);
+    constexpr int HL = halo_of(RAD);
+    constexpr int WN = 4 + 2 * HL;
+    const int SW = row_width<true, HL>(p.tw);
+    const int NS = p.ns;
+    const int ct = threadIdx.x - 32;
+    const int lane = threadIdx.x & 31;
+    const int R = p.R, C = p.C;
+    const bool ring_copy = (MODE == MODE_FUSED) && !(p.flags & F_NO_RING);
+    const bool zero_fill = (MODE == MODE_HPASS) && (p.flags & F_ZERO_FILL);
+    const int x4 = it.x0 + 4 * ct;
+    const bool fast = x4 >= RAD && x4 + 4 <= C - RAD;  // all four columns valid
+    const bool warp_outside = x4 - 4 * lane >= C;       // the whole warp lies right of the image
+    float* dplane = p.dst + (long long)it.plane * p.dst_plane_stride;
+
+    int emit_lo, emit_hi;
+    if (MODE == MODE_HPASS) {
+        emit_lo = it.ylo;
+        emit_hi = it.yhi;
+    } else {
+        emit_lo = max(max(it.ylo, RAD), it.in_lo + RAD);
+        emit_hi = min(it.yhi, R - RAD);
+    }
+    float* dcur = dplane + (long long)(emit_lo - p.dst_row0) * p.dst_row_stride;
+
+    F4 acc[NACC];
+#pragma unroll
+    for (int j = 0; j < NACC; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[j].v[c] = 0.0f;
+
+    for (int r0 = it.in_lo; r0 < it.in_hi; r0 += SROWS, ++gs) {
+        if (r0 != it.in_lo) mbar_wait(&full[slot], phase);  // the item's first stage was waited by the caller
+        const float* sstage = ring + slot * SROWS * SW + 4 * ct;  // column x4 - HL of the stage's first row
+        auto stage_rows = [&](auto fast_stage) {
+            constexpr bool FAST = decltype(fast_stage)::value;
+#pragma unroll
+            for (int k = 0; k < SROWS; ++k) {
+                const int yi = r0 + k;
+                if (FAST || yi < it.in_hi) {
+                    const bool live = !ROW_EDGE || (yi >= p.hrow_lo && yi < p.hrow_hi);
+                    const int yo = (MODE == MODE_HPASS) ? yi : yi - RAD;
+                    const bool emit = FAST || (yo >= emit_lo && yo < emit_hi);
+                    if (!warp_outside) {
+                        const float* srow = sstage + k * SW;
+                        F4 own, outv;
+                        if (MODE == MODE_VPASS) {
+                            own = ld4(srow + HL);
+                            outv = col_fold<RAD, NACC, SYMW>(acc, own, w, p.one);
+                        } else {
+                            float win[WN];
+#pragma unroll
+                            for (int q = 0; q < WN / 4; ++q) {
+                                const F4 t = ld4(srow + 4 * q);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) win[4 * q + i] = t.v[i];
+                            }
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) own.v[i] = win[HL + i];
+                            F4 v;
+                            if (live) {
+                                v = row_pass_win<RAD, SYMW, HL>(win, w, p.one);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) v.v[i] = 0.0f;  // dead row: H0 = 0 / zero fill
+                            }
+                            outv = MODE == MODE_HPASS ? v : col_fold<RAD, NACC, SYMW>(acc, v, w, p.one);
+                        }
+                        if (MODE == MODE_HPASS) {
+                            if (emit && (live || zero_fill)) {
+                                if (fast && live)
+                                    st4(dcur + x4, outv);
+                                else
+                                    store_edge(dcur, x4, C, live ? RAD : 0, outv, own, zero_fill ? 2 : 0);
+                            }
+                        } else if (emit) {
+                            if (fast) {
+                                st4(dcur + x4, outv);
+                            } else {
+                                F4 ringv;
+                                if (ring_copy) {
+                                    int rr = slot * SROWS + k - RAD;  // ring row of input row yo
+                                    if (rr < 0) rr += NS * SROWS;
+                                    ringv = ld4(ring + rr * SW + 4 * ct + HL);
+                                } else {
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) ringv.v[i] = 0.0f;
+                                }
+                                store_edge(dcur, x4, C, RAD, outv, ringv, ring_copy ? 1 : 0);
+                            }
+                        }
+                        if (ROW_EDGE && ring_copy && yi >= it.ylo && yi < it.yhi && (yi < RAD || yi >= R - RAD)) {
+                            float* drow = dplane + (long long)(yi - p.dst_row0) * p.dst_row_stride;
+                            store_edge(drow, x4, C, 0, own, own, 1);
+                        }
+                    }
+                    if (emit) dcur += p.dst_row_stride;
+                }
+            }
+        };
+        const int yo0 = (MODE == MODE_HPASS) ? r0 : r0 - RAD;
+        if (!ROW_EDGE && r0 + SROWS <= it.in_hi && yo0 >= emit_lo && yo0 + SROWS <= emit_hi)
+            stage_rows(std::true_type{});
+        else
+            stage_rows(std::false_type{});
+        if (gs >= LAGS) {
+            int rel_s = slot - LAGS;
+            if (rel_s < 0) rel_s += NS;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[rel_s]);
+        }
+        if (++slot == NS) { slot = 0; phase ^= 1u; }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Consumer for rows of ANY alignment (ALIGNED false: cols % 4 != 0, views whose
 // rows do not start on 16-B boundaries, either side): lane-strided columns.
 //
@@ -1462,7 +1609,12 @@ __device__ __forceinline__ void rows_kernel_body(const Params& p, const float* w
         if (threadIdx.x == 32 && ntr < 8) SC_TR(p, 20 + ntr, clock64());
 #endif
         const Item it = decode_item<MODE, RAD>(p, item);
-        if constexpr (!ALIGNED && lean_of(MODE, RAD)) {  // one (ROW_EDGE) body
+        if constexpr (ALIGNED && RAD > MAX_RAD) {  // widths 11..21 on aligned rows
+            if (item_rows_edge<MODE, RAD>(p, it))
+                consume_item_adj<MODE, RAD, true, SYM>(p, w, it, ring, full, empty, slot, phase, gs);
+            else
+                consume_item_adj<MODE, RAD, false, SYM>(p, w, it, ring, full, empty, slot, phase, gs);
+        } else if constexpr (!ALIGNED && lean_of(MODE, RAD)) {  // one (ROW_EDGE) body
             consume_item_lanes<MODE, RAD, true, SYM, SIG>(p, w, kd, it, ring, full, empty, sshift, slot, phase, gs);
         } else if constexpr (!ALIGNED) {
             if (item_rows_edge<MODE, RAD>(p, it))
@@ -1497,10 +1649,12 @@ __global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_rows_kernel(const __
 
 // Widths 11..31 (r = 5..15), rows of any alignment: the generic producer and the
 // lane-strided consumer with the taps of ParamsW.
-template <int MODE, int RAD, int SYM = 0>
-__global__ void __launch_bounds__(WIDE_MAXT, 1) sepconv_lanes_wide_kernel(const __grid_constant__ ParamsW p) {
+// ALIGNED (two-pass modes, r <= 10): 16-B aligned rows, the adjacent-column consumer.
+template <int MODE, int RAD, int SYM = 0, bool ALIGNED = false>
+__global__ void __launch_bounds__(SC_MAXT, SC_MINB) sepconv_lanes_wide_kernel(const __grid_constant__ ParamsW p) {
     static_assert(RAD > MAX_RAD && RAD <= MAX_RAD_LANES, "r = 5..15");
-    rows_kernel_body<MODE, RAD, false, SYM, false>(p, p.wide_w, p.wide_k);
+    static_assert(!ALIGNED || (RAD <= MAX_RAD_ADJ && !single_like(MODE)), "aligned variant: two-pass modes, r <= 10");
+    rows_kernel_body<MODE, RAD, ALIGNED, SYM, false>(p, p.wide_w, p.wide_k);
 }
 
 }  // namespace sc

@@ -22,7 +22,7 @@ const void* kernel_hpass_direct(int rad);
 const void* kernel_vpass_direct(int rad);
 const void* kernel_single_direct(int rad);
 // widths 11..31 (r = 5..10 / 11..15), any row alignment (kern_lanes_wide*.cu); nullptr otherwise
-const void* kernel_lanes_wide(int mode, int rad, bool symw);
+const void* kernel_lanes_wide(int mode, int rad, bool symw, bool aligned);
 const void* kernel_lanes_wide2(int mode, int rad, bool symw);
 const void* kernel_lanes_wide_single(int rad);
 
