@@ -262,6 +262,16 @@ int sc_host_unregister(void *ptr);
 int sc_two_pass_host_split_f32(float *const *image_planes, float *const *scratch_planes, int nplanes, int rows,
                                int cols, const float *taps, int width, int flags, int device);
 
+/* Single pass over HOST planes: convolve_image's single-pass variants on numpy
+ * planes (S/executors.py:327-356; bodies S/conv.py:86-114, :146-175).
+ * workspace[valid] := the dense fold of the image (dense = width x width,
+ * row-major: the reference's outer_product(kernel).matrix); with SC_COPY_BACK the
+ * same samples also go back into image[valid] (S/conv.py:424-449), in place.
+ * Everything else in both buffers keeps its values. The workspace must not
+ * overlap the image. Streams like sc_two_pass_host_f32. */
+int sc_single_pass_host_f32(float *const *image_planes, float *const *workspace_planes, int nplanes, int rows,
+                            int cols, const float *dense, int width, int flags, int device);
+
 /* Rows [out_lo, out_hi) only (one rank's row band of a host-resident image,
  * global-row rules): reads host rows [out_lo-r, out_hi+r) clipped to the image,
  * writes host rows [out_lo, out_hi); plane pointers address row 0 and no other

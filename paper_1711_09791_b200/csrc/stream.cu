@@ -282,10 +282,15 @@ struct HostJob {
     int width, flags, device;
     const float* const* halo_top;  // optional: r rows holding global rows [out_lo - r, out_lo)
     const float* const* halo_bot;  // optional: r rows holding global rows [out_hi, out_hi + r)
+    // single pass (sc_single_pass_host_f32): the dense width x width matrix; dst =
+    // the workspace planes (valid region only); dst2 = the image planes when the
+    // valid region is also copied back (S/executors.py:330-331), else null
+    const float* dense = nullptr;
+    float* const* dst2 = nullptr;
 };
 
 static int validate(const HostJob& j) {
-    if (!j.src || !j.dst || !j.taps || j.nplanes < 1 || j.rows < 1 || j.cols < 1) {
+    if (!j.src || !j.dst || (!j.taps && !j.dense) || j.nplanes < 1 || j.rows < 1 || j.cols < 1) {
         set_error("null pointer or non-positive dimension");
         return SC_INVALID_ARGUMENT;
     }
@@ -302,10 +307,23 @@ static int validate(const HostJob& j) {
         return SC_INVALID_DIMENSION;
     }
     for (int p = 0; p < j.nplanes; ++p)
-        if (!j.src[p] || !j.dst[p] || (j.scr && !j.scr[p])) {
+        if (!j.src[p] || !j.dst[p] || (j.scr && !j.scr[p]) || (j.dst2 && !j.dst2[p])) {
             set_error("null plane pointer");
             return SC_INVALID_ARGUMENT;
         }
+    if (j.dense) {
+        // the workspace must not alias the image (S/conv.py:68-75 _check_pair)
+        const size_t bytes = (size_t)j.rows * j.cols * sizeof(float);
+        for (int a = 0; a < j.nplanes; ++a)
+            for (int b = 0; b < j.nplanes; ++b) {
+                const char* x = reinterpret_cast<const char*>(j.dst[a]);
+                const char* z = reinterpret_cast<const char*>(j.src[b]);
+                if (x < z + bytes && z < x + bytes) {
+                    set_error("workspace planes must not overlap the image");
+                    return SC_INVALID_ARGUMENT;
+                }
+            }
+    }
     if (j.scr) {
         // the workspace must not alias the image (S/conv.py:68-75 _check_pair)
         const size_t bytes = (size_t)j.rows * j.cols * sizeof(float);
@@ -369,7 +387,7 @@ static int host_band(const HostJob& J) {
     const bool split = J.scr != nullptr;
 
     // memory kinds: stage pageable planes through pinned slots
-    std::vector<char> stage_src(J.nplanes), stage_dst(J.nplanes), stage_scr(J.nplanes);
+    std::vector<char> stage_src(J.nplanes), stage_dst(J.nplanes), stage_scr(J.nplanes), stage_dst2(J.nplanes);
     bool any_in = false, any_out = false;
     for (int p = 0; p < J.nplanes; ++p) {
         // (the multi-device halo copies are small host vectors: their rows go by a
@@ -377,8 +395,9 @@ static int host_band(const HostJob& J) {
         stage_src[p] = pageable(J.src[p]);
         stage_dst[p] = pageable(J.dst[p]);
         stage_scr[p] = split && pageable(J.scr[p]);
+        stage_dst2[p] = J.dst2 && pageable(J.dst2[p]);
         any_in |= stage_src[p] != 0;
-        any_out |= stage_dst[p] || stage_scr[p];
+        any_out |= stage_dst[p] || stage_scr[p] || stage_dst2[p];
     }
     const size_t in_f = (size_t)(chunk + 2 * r) * cols, out_f = (size_t)chunk * cols;
     if ((e = grow_dev(c->in_buf, c->in_cap, in_f)) != cudaSuccess ||
@@ -408,7 +427,8 @@ static int host_band(const HostJob& J) {
         }
     const size_t n = chunks.size();
     const size_t row_bytes = (size_t)cols * sizeof(float);
-    const bool no_ring = (J.flags & SC_NO_RING) != 0;
+    // the single pass writes the valid region only: nothing else leaves the device
+    const bool no_ring = (J.flags & SC_NO_RING) != 0 || J.dense != nullptr;
     CopyPool& pool = copy_pool();
     std::vector<std::shared_ptr<CopyGroup>> in_grp(n), out_grp(n);
 
@@ -471,22 +491,24 @@ static int host_band(const HostJob& J) {
     // host copy of chunk k out of its pinned slots into the caller's rows
     auto copy_out = [&](size_t k) -> cudaError_t {
         const Chunk& q = chunks[k];
-        if (!stage_dst[q.plane] && !stage_scr[q.plane]) return cudaSuccess;
+        if (!stage_dst[q.plane] && !stage_scr[q.plane] && !stage_dst2[q.plane]) return cudaSuccess;
         const int s = (int)(k % NSLOT);
         cudaError_t e2 = cudaEventSynchronize(c->ev_d2h[s]);
         if (e2 != cudaSuccess) return e2;
         std::vector<Seg> segs;
-        if (stage_dst[q.plane]) {
+        auto from_pinned = [&](float* plane) {
             if (no_ring) {
                 const int vlo = q.lo > r ? q.lo : r;
                 const int vhi = q.hi < rows - r ? q.hi : rows - r;
                 for (int y = vlo; y < vhi; ++y)
-                    segs.push_back({J.dst[q.plane] + (size_t)y * cols + r, c->pin_out[s] + (size_t)(y - q.lo) * cols + r,
+                    segs.push_back({plane + (size_t)y * cols + r, c->pin_out[s] + (size_t)(y - q.lo) * cols + r,
                                     (size_t)(cols - 2 * r) * sizeof(float)});
             } else {
-                segs.push_back({J.dst[q.plane] + (size_t)q.lo * cols, c->pin_out[s], (size_t)(q.hi - q.lo) * row_bytes});
+                segs.push_back({plane + (size_t)q.lo * cols, c->pin_out[s], (size_t)(q.hi - q.lo) * row_bytes});
             }
-        }
+        };
+        if (stage_dst[q.plane]) from_pinned(J.dst[q.plane]);
+        if (stage_dst2[q.plane]) from_pinned(J.dst2[q.plane]);
         if (stage_scr[q.plane])
             segs.push_back({J.scr[q.plane] + (size_t)q.lo * cols, c->pin_scr[s], (size_t)(q.hi - q.lo) * row_bytes});
         out_grp[k] = pool.submit(std::move(segs));
@@ -538,7 +560,16 @@ static int host_band(const HostJob& J) {
         j.flags = J.flags & (SC_EXTENDED | SC_NO_RING);
         j.width = J.width;
         j.taps = J.taps;
-        rc = launch_rows(j, c->cmp);
+        if (J.dense) {
+            static const float zeros[MAX_W_WIDE] = {0};
+            j.mode = MODE_SINGLE;
+            j.dense = J.dense;
+            j.taps = zeros;
+            j.flags = 0;
+            j.out_lo = q.lo > r ? q.lo : r;  // the valid rows of this chunk
+            j.out_hi = q.hi < rows - r ? q.hi : rows - r;
+        }
+        rc = (J.dense && j.out_hi <= j.out_lo) ? SC_OK : launch_rows(j, c->cmp);
         if (rc == SC_OK && split) {
             // H0 of the chunk's own rows: the zeroed workspace with the row pass on
             // the live rows (zero on dead rows and on the column ring)
@@ -566,22 +597,27 @@ static int host_band(const HostJob& J) {
             out_grp[k - NSLOT].reset();
         }
         e = cudaSuccess;
-        if (stage_dst[q.plane]) {
-            e = cudaMemcpyAsync(c->pin_out[s], c->out_buf[s], (size_t)(q.hi - q.lo) * row_bytes,
-                                cudaMemcpyDeviceToHost, c->d2h);
-        } else if (no_ring) {
-            // only valid rows/cols leave the device: the host ring keeps its values
+        // only valid rows/cols leave the device under no_ring: the host ring keeps its values
+        auto valid_region_d2h = [&](float* plane) -> cudaError_t {
             const int vlo = q.lo > r ? q.lo : r;
             const int vhi = q.hi < rows - r ? q.hi : rows - r;
-            if (vhi > vlo)
-                e = cudaMemcpy2DAsync(J.dst[q.plane] + (size_t)vlo * cols + r, row_bytes,
-                                      c->out_buf[s] + (size_t)(vlo - q.lo) * cols + r, row_bytes,
-                                      (size_t)(cols - 2 * r) * sizeof(float), (size_t)(vhi - vlo),
-                                      cudaMemcpyDeviceToHost, c->d2h);
-        } else {
-            e = cudaMemcpyAsync(J.dst[q.plane] + (size_t)q.lo * cols, c->out_buf[s], (size_t)(q.hi - q.lo) * row_bytes,
+            if (vhi <= vlo) return cudaSuccess;
+            return cudaMemcpy2DAsync(plane + (size_t)vlo * cols + r, row_bytes,
+                                     c->out_buf[s] + (size_t)(vlo - q.lo) * cols + r, row_bytes,
+                                     (size_t)(cols - 2 * r) * sizeof(float), (size_t)(vhi - vlo),
+                                     cudaMemcpyDeviceToHost, c->d2h);
+        };
+        if (stage_dst[q.plane] || stage_dst2[q.plane])
+            e = cudaMemcpyAsync(c->pin_out[s], c->out_buf[s], (size_t)(q.hi - q.lo) * row_bytes,
                                 cudaMemcpyDeviceToHost, c->d2h);
+        if (e == cudaSuccess && !stage_dst[q.plane]) {
+            if (no_ring)
+                e = valid_region_d2h(J.dst[q.plane]);
+            else
+                e = cudaMemcpyAsync(J.dst[q.plane] + (size_t)q.lo * cols, c->out_buf[s],
+                                    (size_t)(q.hi - q.lo) * row_bytes, cudaMemcpyDeviceToHost, c->d2h);
         }
+        if (e == cudaSuccess && J.dst2 && !stage_dst2[q.plane]) e = valid_region_d2h(J.dst2[q.plane]);
         if (e == cudaSuccess && split)
             e = cudaMemcpyAsync(stage_scr[q.plane] ? c->pin_scr[s] : J.scr[q.plane] + (size_t)q.lo * cols,
                                 c->scr_buf[s], (size_t)(q.hi - q.lo) * row_bytes, cudaMemcpyDeviceToHost, c->d2h);
@@ -637,6 +673,25 @@ extern "C" int sc_host_unregister(void* ptr) {
 extern "C" int sc_two_pass_host_f32(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows,
                                     int cols, const float* taps, int width, int flags, int device) {
     HostJob j{src_planes, dst_planes, nullptr, nplanes, rows, cols, 0, rows, taps, width, flags, device, nullptr, nullptr};
+    return host_band(j);
+}
+
+// Single pass over HOST planes (convolve_image's single-pass variants on numpy
+// planes, S/executors.py:327-356): workspace[valid] = dense fold of the image;
+// with SC_COPY_BACK the same samples also go back into image[valid] (in place:
+// a chunk's write-back is ordered after the next chunk's input left its rows).
+// Everything else in both buffers keeps its values.
+extern "C" int sc_single_pass_host_f32(float* const* image_planes, float* const* workspace_planes, int nplanes,
+                                       int rows, int cols, const float* dense, int width, int flags, int device) {
+    set_error("");
+    if (!workspace_planes || !dense) {
+        set_error("null workspace planes or matrix");
+        return SC_INVALID_ARGUMENT;
+    }
+    HostJob j{image_planes, workspace_planes, nullptr, nplanes, rows, cols, 0, rows, nullptr, width, 0, device,
+              nullptr, nullptr};
+    j.dense = dense;
+    j.dst2 = (flags & SC_COPY_BACK) ? image_planes : nullptr;
     return host_band(j);
 }
 

@@ -481,6 +481,28 @@ def two_pass_host_split(image_planes, scratch_planes, taps, *, extended: bool = 
                                             shape[1], _fp(w), w.size, flags, int(device)))
 
 
+def single_pass_host(image_planes, workspace_planes, dense, *, copy_back: bool = False, device: int = 0,
+                     register: bool = True) -> None:
+    """convolve_image's single-pass variants on HOST planes (S/executors.py:327-356):
+    workspace_planes[valid] := the dense fold of image_planes; with copy_back the
+    same samples also go back into image_planes[valid] in place. Everything else
+    in both buffers keeps its values. Streamed through the GPU like
+    two_pass_host (chunked H2D / kernel / D2H); blocks until done."""
+    m = _dense(dense)
+    image_planes, workspace_planes = list(image_planes), list(workspace_planes)
+    if register:
+        for a in image_planes + workspace_planes:
+            host_registry.pin(a)
+    ptrs_img, shape = _host_ptrs(image_planes)
+    ptrs_ws, _ = _host_ptrs(workspace_planes, shape)
+    if not ptrs_img or len(ptrs_img) != len(ptrs_ws):
+        raise InvalidArgumentError("need matching, non-empty image and workspace plane lists")
+    L = _lib.load()
+    _lib.check(L.sc_single_pass_host_f32(_ptr_array(ptrs_img), _ptr_array(ptrs_ws), len(ptrs_img), shape[0],
+                                         shape[1], _fp(m), m.shape[0], _lib.SC_COPY_BACK if copy_back else 0,
+                                         int(device)))
+
+
 def two_pass_host_band(src_rows, dst_rows, taps, *, global_rows: int, row0: int, out_lo: int, out_hi: int,
                        extended: bool = False, ring: bool = True, device: int = 0) -> None:
     """One rank's row band of a host-resident image, end to end (streamed H2D ->

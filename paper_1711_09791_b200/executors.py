@@ -205,16 +205,10 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
             dev.two_pass_host_split(img_planes, ws_planes, taps, device=device_index, register=plan.register_host,
                                     devices=plan.devices)
         else:
-            with torch.cuda.device(device_index):
-                src = torch.stack([torch.from_numpy(a) for a in img_planes]).cuda()
-                wsd = torch.stack([torch.from_numpy(a) for a in ws_planes]).cuda()
-                dev.single_pass(src, outer_product(kernel).matrix, wsd, copy_back=copy_back)
-                src_h, wsd_h = src.cpu().numpy(), wsd.cpu().numpy()
-            rl, rh, cl, ch = region.row_lo, region.row_hi, region.col_lo, region.col_hi
-            for p in range(nplanes):
-                ws_planes[p][rl:rh, cl:ch] = wsd_h[p, rl:rh, cl:ch]
-                if copy_back:
-                    img_planes[p][rl:rh, cl:ch] = src_h[p, rl:rh, cl:ch]
+            # streamed like the two-pass: workspace[valid] (and image[valid] with
+            # copy-back) written in place, nothing else touched
+            dev.single_pass_host(img_planes, ws_planes, outer_product(kernel).matrix, copy_back=copy_back,
+                                 device=device_index, register=plan.register_host)
 
     stats.wall_time_ns = time.perf_counter_ns() - t0
     stats.parallel_region_launches = _lib.launch_count() - before

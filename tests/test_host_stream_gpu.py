@@ -74,6 +74,58 @@ def test_host_split_end_state(dev, oracle, small_chunks, kind, width, extended):
     assert bits_equal(as_np(scr), oracle.two_pass_scratch(x, w, extended=extended))
 
 
+@pytest.mark.parametrize("kind", ["pageable", "pinned", "mixed"])
+@pytest.mark.parametrize("width,copy_back", [(5, False), (5, True), (3, True), (9, True), (11, False), (21, True)])
+def test_host_single_pass_streamed(dev, oracle, small_chunks, kind, width, copy_back):
+    """sc_single_pass_host_f32: convolve_image's single-pass variants on host planes,
+    streamed in 16-row chunks. workspace[valid] = the dense fold; with copy-back
+    image[valid] too, in place; every other sample of both buffers keeps its bits."""
+    rng = np.random.default_rng(width)
+    R, C = 157, 203
+    r = width // 2
+    dense = rng.uniform(-1, 1, size=(width, width)).astype(np.float32)
+    x = oracle.synthetic(3 * R * C, 60 + width, kind=2).reshape(3, R, C)
+    img = planes_of(x, kind)
+    ws = planes_of(np.full_like(x, -3.0), kind)
+    dev.single_pass_host(img, ws, dense, copy_back=copy_back)
+    want = oracle.single_pass(x, dense)
+    exp_ws = np.full_like(x, -3.0)
+    exp_ws[:, r:R - r, r:C - r] = want[:, r:R - r, r:C - r]
+    assert bits_equal(as_np(ws), exp_ws)
+    exp_img = x.copy()
+    if copy_back:
+        exp_img[:, r:R - r, r:C - r] = want[:, r:R - r, r:C - r]
+    assert bits_equal(as_np(img), exp_img)
+
+
+def test_host_single_pass_default_chunks_and_checks(dev, oracle):
+    """Default chunking on a plane large enough for several chunks, through
+    convolve_image on numpy planes (the drop-in call); aliased workspaces are refused."""
+    from paper_1711_09791_b200 import Algorithm, ConvVariant, Cuda, Image, Plane, SeparableKernel, convolve_image
+    from paper_1711_09791_b200.errors import InvalidArgumentError
+
+    R, C = 1500, 2048
+    x = oracle.synthetic(2 * R * C, 5, kind=1).reshape(2, R, C)
+    w = np.array([1, 4, 6, 4, 1], np.float32) / 16
+    k = SeparableKernel(w)
+    dense = oracle.outer_product(w)
+    want = oracle.single_pass(x, dense)
+    for copy_back in (False, True):
+        image = Image([Plane(p.copy()) for p in x])
+        ws = Image([Plane(np.zeros_like(p)) for p in x])
+        convolve_image(image, k, ConvVariant(Algorithm.SINGLE_PASS_UNROLLED5, copy_back), Cuda(), workspace=ws)
+        exp = np.zeros_like(x)
+        exp[:, 2:-2, 2:-2] = want[:, 2:-2, 2:-2]
+        assert bits_equal(np.stack([p.data for p in ws.planes]), exp)
+        exp_img = x.copy()
+        if copy_back:
+            exp_img[:, 2:-2, 2:-2] = want[:, 2:-2, 2:-2]
+        assert bits_equal(np.stack([p.data for p in image.planes]), exp_img)
+    buf = x[0].copy()
+    with pytest.raises(InvalidArgumentError):
+        dev.single_pass_host([buf], [buf], dense)
+
+
 @pytest.mark.parametrize("kind", ["pageable", "pinned"])
 @pytest.mark.parametrize("width", [35, 65])
 def test_host_in_place_radius_above_chunk_floor(dev, oracle, small_chunks, kind, width):
