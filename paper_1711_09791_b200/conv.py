@@ -102,13 +102,17 @@ class _Staged:
     """Device views of a group of planes; host planes are uploaded and, on exit,
     the named regions are written back (only those the reference writes)."""
 
-    def __init__(self, planes):
+    def __init__(self, planes, write_only=()):
+        """write_only: indices of planes whose device copy is only written (and
+        partly written back): allocated on the device, not uploaded."""
         torch = _torch()
         self.planes = planes
         self.host = not _is_dev(planes[0])
         if self.host:
             dev = torch.device("cuda", torch.cuda.current_device())
-            self.t = [torch.from_numpy(p.data).to(dev, non_blocking=False).unsqueeze(0) for p in planes]
+            self.t = [(torch.empty(p.data.shape, dtype=torch.float32, device=dev) if i in write_only
+                       else torch.from_numpy(p.data).to(dev, non_blocking=False)).unsqueeze(0)
+                      for i, p in enumerate(planes)]
         else:
             self.t = [p.data.unsqueeze(0) for p in planes]
 
@@ -131,6 +135,16 @@ class _Staged:
             _torch().cuda.current_stream().synchronize()
 
 
+def _streamable(*planes: Plane) -> bool:
+    """Host planes the streamed entry points take as they are (the reference's Plane
+    keeps a C-contiguous 2-D float32 numpy array, S/image.py:37-39)."""
+    for p in planes:
+        a = p.data
+        if not isinstance(a, np.ndarray) or a.dtype != np.float32 or a.ndim != 2 or not a.flags.c_contiguous:
+            return False
+    return True
+
+
 def _count(counter: OpCounter | None, mults: int, adds: int) -> None:
     if counter is not None:
         counter.multiplications += mults
@@ -147,10 +161,14 @@ def conv_single_pass_generic(src: Plane, kernel: DenseKernel, dst: Plane, *, vec
 
     _check_pair(src, dst, kernel.width)
     region = valid_region(src.rows, src.cols, kernel.radius)
-    st = _Staged([src, dst])
-    device.single_pass(st.t[0], kernel.matrix, st.t[1])
-    st.write_back(1, (region.row_lo, region.row_hi), (region.col_lo, region.col_hi))
-    st.finish()
+    if _streamable(src, dst):
+        # host planes: chunked H2D / kernel / D2H of the valid region (sc_single_pass_host_f32)
+        device.single_pass_host([src.data], [dst.data], kernel.matrix)
+    else:
+        st = _Staged([src, dst])
+        device.single_pass(st.t[0], kernel.matrix, st.t[1])
+        st.write_back(1, (region.row_lo, region.row_hi), (region.col_lo, region.col_hi))
+        st.finish()
     n = (region.row_hi - region.row_lo) * (region.col_hi - region.col_lo)
     _count(counter, kernel.width**2 * n, (kernel.width**2 - 1) * n)
 
@@ -168,7 +186,7 @@ def _one_pass(which: str, src: Plane, kernel: SeparableKernel, dst: Plane, count
 
     _check_pair(src, dst, kernel.width)
     region = valid_region(src.rows, src.cols, kernel.radius)
-    st = _Staged([src, dst])
+    st = _Staged([src, dst], write_only=(1,))
     fn = device.hpass if which == "h" else device.vpass
     fn(st.t[0], kernel.weights, st.t[1], region.row_lo, region.row_hi)
     st.write_back(1, (region.row_lo, region.row_hi), (region.col_lo, region.col_hi))
@@ -201,11 +219,15 @@ def conv_two_pass(plane: Plane, kernel: SeparableKernel, scratch: Plane, *, vect
 
     _check_pair(plane, scratch, kernel.width)
     r = kernel.radius
-    st = _Staged([plane, scratch])
-    device.two_pass_split(st.t[0], st.t[1], kernel.weights, extended=extended)
-    st.write_back(0, (r, plane.rows - r), (r, plane.cols - r))
-    st.write_back(1)
-    st.finish()
+    if _streamable(plane, scratch):
+        # host planes: streamed, both buffers' end state (sc_two_pass_host_split_f32)
+        device.two_pass_host_split([plane.data], [scratch.data], kernel.weights, extended=extended)
+    else:
+        st = _Staged([plane, scratch])
+        device.two_pass_split(st.t[0], st.t[1], kernel.weights, extended=extended)
+        st.write_back(0, (r, plane.rows - r), (r, plane.cols - r))
+        st.write_back(1)
+        st.finish()
     span = plane.cols - 2 * r
     h_rows = plane.rows if extended else plane.rows - 2 * r
     v_rows = plane.rows - 2 * r
@@ -227,7 +249,7 @@ def copy_back(src: Plane, dst: Plane, region: ValidRegion) -> None:
         raise InvalidArgumentError(f"region {region} out of bounds for {src.rows}x{src.cols}")
     if _is_dev(src) != _is_dev(dst):
         raise InvalidArgumentError("planes must both be host arrays or both live on the same CUDA device")
-    st = _Staged([src, dst])
+    st = _Staged([src, dst], write_only=(1,))
     device.copy_region(st.t[0], st.t[1], region.row_lo, region.row_hi, region.col_lo, region.col_hi)
     st.write_back(1, (region.row_lo, region.row_hi), (region.col_lo, region.col_hi))
     st.finish()
