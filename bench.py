@@ -564,6 +564,67 @@ def main():
                                 "path": "sc_two_pass_split_f32: image and scratch (H0), one pass + halo snapshot"}}
         del img, scr
 
+    # ---- config 2 also names the single pass (copy-back on / off): the FP32-bound
+    # kernel next to the reference algorithm's FP32 floor (49 ops per sample at 126.7
+    # lane-ops per cycle per SM x 148 SMs x the maximum SM clock; tools/fp2_rate.cu),
+    # device-resident under the same L2-flush protocol, and end to end through
+    # convolve_image on numpy planes (streamed, sc_single_pass_host_f32)
+    single = None
+    if args.config == "cfg2" and world == 1 and band is not None:
+        dense = np.ascontiguousarray(np.multiply.outer(w, w), dtype=np.float32)
+        ws_t = torch.zeros_like(src)
+        img_t = src.clone()
+        W = len(w)
+        valid = P * (R - 2 * r) * (C - 2 * r)
+        fp_floor_ms = valid * (2 * W * W - 1) / (126.7 * 148 * 1.965e9) * 1e3
+
+        def flushed(fn, n=50):
+            for _ in range(3):
+                fn()
+            ps = []
+            for _ in range(n):
+                if flush is not None:
+                    flush.fill_(1)
+                a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_ev.record(stream)
+                fn()
+                b_ev.record(stream)
+                ps.append((a_ev, b_ev))
+            torch.cuda.synchronize()
+            return statistics.median(a.elapsed_time(b) for a, b in ps)
+
+        nc_ms = flushed(lambda: dev.single_pass(src, dense, ws_t))
+        cb_ms = flushed(lambda: dev.single_pass(img_t, dense, ws_t, copy_back=True))
+        single = {"fp32_floor_ms": round(fp_floor_ms, 4),
+                  "no_copy": {"ms": round(nc_ms, 4), "value": round(total_px / (nc_ms / 1e3) / 1e9, 3),
+                              "frac_of_fp32_floor": round(fp_floor_ms / nc_ms, 3)},
+                  "copy_back": {"ms": round(cb_ms, 4), "value": round(total_px / (cb_ms / 1e3) / 1e9, 3),
+                                "path": "one pass: workspace and image in place"}}
+        if args.e2e_steps > 0:
+            import time as _time
+
+            from paper_1711_09791_b200 import Algorithm, ConvVariant, Cuda, Image, Plane, SeparableKernel
+            from paper_1711_09791_b200 import convolve_image as _convolve
+
+            host = src.cpu().numpy()
+            image = Image([Plane(np.ascontiguousarray(pl)) for pl in host])
+            wsi = Image([Plane(np.zeros_like(pl)) for pl in host])
+            kern = SeparableKernel(w)
+            for cb in (False, True):
+                var = ConvVariant(Algorithm.SINGLE_PASS_GENERIC, cb)
+                _convolve(image, kern, var, Cuda(), workspace=wsi)  # first call: page-locking
+                ts = []
+                for _ in range(max(args.e2e_steps, 3)):
+                    t0 = _time.perf_counter()
+                    _convolve(image, kern, var, Cuda(), workspace=wsi)
+                    ts.append(_time.perf_counter() - t0)
+                ems = min(ts) * 1e3
+                single["e2e_copy_back" if cb else "e2e_no_copy"] = {
+                    "ms": round(ems, 3), "value": round(total_px / (ems / 1e3) / 1e9, 3),
+                    "path": "convolve_image(image, kernel, SINGLE_PASS_GENERIC, Cuda(), workspace=ws) on numpy planes"}
+            del host, image, wsi
+        del ws_t, img_t
+
     # ---- N>1 row bands: the same steps with the OTHER halo transport (secondary)
     # (only when the peer transport is the timed one: the NCCL plan then always
     # exists, while a peer stepper built where peer access failed could leave the
@@ -807,6 +868,7 @@ def main():
             **({"halo_alt": halo_alt} if halo_alt is not None else {}),
             **({"band_check": band_check} if band_check is not None else {}),
             **({"dropin_device": dropin} if dropin is not None else {}),
+            **({"single_pass": single} if single is not None else {}),
             "effective_GBps": round(eff, 1), "pct_of_8TBps": round(100 * eff / NOMINAL_HBM_GBPS, 2),
             "pct_of_measured_copy": round(100 * eff / peak, 2),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,
