@@ -272,6 +272,13 @@ int sc_two_pass_host_split_f32(float *const *image_planes, float *const *scratch
 int sc_single_pass_host_f32(float *const *image_planes, float *const *workspace_planes, int nplanes, int rows,
                             int cols, const float *dense, int width, int flags, int device);
 
+/* horizontal_pass / vertical_pass on HOST planes (S/conv.py:362-389): dst[valid] :=
+ * the row pass (vertical = 0) or the column pass (vertical != 0) of src over rows
+ * [r, R-r) and columns [r, C-r); dst elsewhere keeps its values; dst must not
+ * overlap src. Streams like sc_two_pass_host_f32. */
+int sc_pass_host_f32(const float *const *src_planes, float *const *dst_planes, int nplanes, int rows, int cols,
+                     const float *taps, int width, int vertical, int device);
+
 /* Rows [out_lo, out_hi) only (one rank's row band of a host-resident image,
  * global-row rules): reads host rows [out_lo-r, out_hi+r) clipped to the image,
  * writes host rows [out_lo, out_hi); plane pointers address row 0 and no other

@@ -186,11 +186,14 @@ def _one_pass(which: str, src: Plane, kernel: SeparableKernel, dst: Plane, count
 
     _check_pair(src, dst, kernel.width)
     region = valid_region(src.rows, src.cols, kernel.radius)
-    st = _Staged([src, dst], write_only=(1,))
-    fn = device.hpass if which == "h" else device.vpass
-    fn(st.t[0], kernel.weights, st.t[1], region.row_lo, region.row_hi)
-    st.write_back(1, (region.row_lo, region.row_hi), (region.col_lo, region.col_hi))
-    st.finish()
+    if _streamable(src, dst):
+        device.pass_host([src.data], [dst.data], kernel.weights, vertical=(which == "v"))
+    else:
+        st = _Staged([src, dst], write_only=(1,))
+        fn = device.hpass if which == "h" else device.vpass
+        fn(st.t[0], kernel.weights, st.t[1], region.row_lo, region.row_hi)
+        st.write_back(1, (region.row_lo, region.row_hi), (region.col_lo, region.col_hi))
+        st.finish()
     n = (region.row_hi - region.row_lo) * (region.col_hi - region.col_lo)
     _count(counter, kernel.width * n, (kernel.width - 1) * n)
 

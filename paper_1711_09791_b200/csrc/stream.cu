@@ -287,6 +287,8 @@ struct HostJob {
     // valid region is also copied back (S/executors.py:330-331), else null
     const float* dense = nullptr;
     float* const* dst2 = nullptr;
+    // row pass (1) or column pass (2) alone (sc_pass_host_f32): dst[valid] only
+    int one_pass = 0;
 };
 
 static int validate(const HostJob& j) {
@@ -311,7 +313,7 @@ static int validate(const HostJob& j) {
             set_error("null plane pointer");
             return SC_INVALID_ARGUMENT;
         }
-    if (j.dense) {
+    if (j.dense || j.one_pass) {
         // the workspace must not alias the image (S/conv.py:68-75 _check_pair)
         const size_t bytes = (size_t)j.rows * j.cols * sizeof(float);
         for (int a = 0; a < j.nplanes; ++a)
@@ -428,7 +430,7 @@ static int host_band(const HostJob& J) {
     const size_t n = chunks.size();
     const size_t row_bytes = (size_t)cols * sizeof(float);
     // the single pass writes the valid region only: nothing else leaves the device
-    const bool no_ring = (J.flags & SC_NO_RING) != 0 || J.dense != nullptr;
+    const bool no_ring = (J.flags & SC_NO_RING) != 0 || J.dense != nullptr || J.one_pass != 0;
     CopyPool& pool = copy_pool();
     std::vector<std::shared_ptr<CopyGroup>> in_grp(n), out_grp(n);
 
@@ -569,7 +571,15 @@ static int host_band(const HostJob& J) {
             j.out_lo = q.lo > r ? q.lo : r;  // the valid rows of this chunk
             j.out_hi = q.hi < rows - r ? q.hi : rows - r;
         }
-        rc = (J.dense && j.out_hi <= j.out_lo) ? SC_OK : launch_rows(j, c->cmp);
+        if (J.one_pass) {
+            j.mode = J.one_pass == 1 ? MODE_HPASS : MODE_VPASS;
+            j.flags = 0;
+            j.hrow_lo = r;
+            j.hrow_hi = rows - r;
+            j.out_lo = q.lo > r ? q.lo : r;  // the valid rows of this chunk
+            j.out_hi = q.hi < rows - r ? q.hi : rows - r;
+        }
+        rc = ((J.dense || J.one_pass) && j.out_hi <= j.out_lo) ? SC_OK : launch_rows(j, c->cmp);
         if (rc == SC_OK && split) {
             // H0 of the chunk's own rows: the zeroed workspace with the row pass on
             // the live rows (zero on dead rows and on the column ring)
@@ -692,6 +702,17 @@ extern "C" int sc_single_pass_host_f32(float* const* image_planes, float* const*
               nullptr, nullptr};
     j.dense = dense;
     j.dst2 = (flags & SC_COPY_BACK) ? image_planes : nullptr;
+    return host_band(j);
+}
+
+// horizontal_pass / vertical_pass on HOST planes (S/conv.py:362-389): dst[valid]
+// := the row pass (vertical = 0) or the column pass (vertical != 0) of src over the
+// valid rows [r, R-r) and columns [r, C-r); dst elsewhere keeps its values.
+extern "C" int sc_pass_host_f32(const float* const* src_planes, float* const* dst_planes, int nplanes, int rows,
+                                int cols, const float* taps, int width, int vertical, int device) {
+    set_error("");
+    HostJob j{src_planes, dst_planes, nullptr, nplanes, rows, cols, 0, rows, taps, width, 0, device, nullptr, nullptr};
+    j.one_pass = vertical ? 2 : 1;
     return host_band(j);
 }
 

@@ -503,6 +503,24 @@ def single_pass_host(image_planes, workspace_planes, dense, *, copy_back: bool =
                                          int(device)))
 
 
+def pass_host(src_planes, dst_planes, taps, *, vertical: bool, device: int = 0, register: bool = True) -> None:
+    """horizontal_pass / vertical_pass on HOST planes (S/conv.py:362-389): dst[valid] :=
+    the row (or column) pass of src; dst elsewhere keeps its values. Streamed
+    through the GPU like two_pass_host; blocks until done."""
+    w = _taps(taps)
+    src_planes, dst_planes = list(src_planes), list(dst_planes)
+    if register:
+        for a in src_planes + dst_planes:
+            host_registry.pin(a)
+    ptrs_src, shape = _host_ptrs(src_planes)
+    ptrs_dst, _ = _host_ptrs(dst_planes, shape)
+    if not ptrs_src or len(ptrs_src) != len(ptrs_dst):
+        raise InvalidArgumentError("need matching, non-empty source and destination plane lists")
+    L = _lib.load()
+    _lib.check(L.sc_pass_host_f32(_ptr_array(ptrs_src), _ptr_array(ptrs_dst), len(ptrs_src), shape[0], shape[1],
+                                  _fp(w), w.size, 1 if vertical else 0, int(device)))
+
+
 def two_pass_host_band(src_rows, dst_rows, taps, *, global_rows: int, row0: int, out_lo: int, out_hi: int,
                        extended: bool = False, ring: bool = True, device: int = 0) -> None:
     """One rank's row band of a host-resident image, end to end (streamed H2D ->

@@ -98,6 +98,27 @@ def test_host_single_pass_streamed(dev, oracle, small_chunks, kind, width, copy_
     assert bits_equal(as_np(img), exp_img)
 
 
+@pytest.mark.parametrize("kind", ["pageable", "pinned"])
+@pytest.mark.parametrize("width", [1, 5, 9, 13])
+@pytest.mark.parametrize("vertical", [False, True])
+def test_host_row_and_column_pass_streamed(dev, oracle, small_chunks, kind, width, vertical):
+    """sc_pass_host_f32: horizontal_pass / vertical_pass on host planes, streamed in
+    16-row chunks: dst[valid] = the pass, every other sample of dst keeps its bits."""
+    R, C = 131, 150
+    r = width // 2
+    w = taps_of(width)
+    x = oracle.synthetic(2 * R * C, 70 + width, kind=2).reshape(2, R, C)
+    src = planes_of(x, kind)
+    dst = planes_of(np.full_like(x, -6.0), kind)
+    dev.pass_host(src, dst, w, vertical=vertical)
+    exp = np.full_like(x, -6.0)
+    ofn = oracle.vertical_rows if vertical else oracle.horizontal_rows
+    for p in range(2):
+        ofn(x[p], exp[p], w, r, R - r)
+    assert bits_equal(as_np(dst), exp)
+    assert bits_equal(as_np(src), x)
+
+
 def test_host_single_pass_default_chunks_and_checks(dev, oracle):
     """Default chunking on a plane large enough for several chunks, through
     convolve_image on numpy planes (the drop-in call); aliased workspaces are refused."""
