@@ -624,6 +624,36 @@ def main():
                     "path": "convolve_image(image, kernel, SINGLE_PASS_GENERIC, Cuda(), workspace=ws) on numpy planes"}
             del host, image, wsi
         del ws_t, img_t
+        # the reference package's own single pass on the host cores (config 2
+        # also times SINGLE_PASS_UNROLLED5 without copy-back), same image
+        sl = import_reference() if not args.no_cpu_baseline else None
+        if sl is not None:
+            from oracle import oracle as orc
+
+            cores = os.cpu_count() or 1
+            hostx = orc.synthetic(P * R * C, wl.seed, wl.kind).reshape(P, R, C)
+            rimg = sl.Image([sl.Plane(hostx[pl]) for pl in range(P)])
+            rws = sl.Image.zeros(R, C, P)
+            rk = sl.SeparableKernel(w)
+            rvar = sl.ConvVariant(sl.Algorithm.SINGLE_PASS_UNROLLED5, False)
+            rpool = sl.WorkerPool(cores)
+            try:
+                rplan = sl.StaticChunked(workers=cores)
+                sl.convolve_image(rimg, rk, rvar, rplan, workspace=rws, pool=rpool)
+                rts = []
+                for _ in range(3):
+                    t0 = time.perf_counter()
+                    sl.convolve_image(rimg, rk, rvar, rplan, workspace=rws, pool=rpool)
+                    rts.append(time.perf_counter() - t0)
+            finally:
+                rpool.close()
+            rms = min(rts) * 1e3
+            single["cpu_reference"] = {
+                "ms": round(rms, 2), "value": round(total_px / (rms / 1e3) / 1e9, 4), "cores": cores,
+                "cpu_model": cpu_model(),
+                "path": f"sepconv_lab {sl.__version__} convolve_image(SINGLE_PASS_UNROLLED5, no copy-back, "
+                        f"StaticChunked({cores})), vectorised"}
+            del hostx, rimg, rws
 
     # ---- N>1 row bands: the same steps with the OTHER halo transport (secondary)
     # (only when the peer transport is the timed one: the NCCL plan then always
