@@ -272,6 +272,13 @@ int sc_two_pass_host_split_f32(float *const *image_planes, float *const *scratch
 int sc_single_pass_host_f32(float *const *image_planes, float *const *workspace_planes, int nplanes, int rows,
                             int cols, const float *dense, int width, int flags, int device);
 
+/* sc_single_pass_host_f32 over several GPUs from one process: row bands by the
+ * reference's balanced split (S/executors.py:121-139), one host thread and one
+ * PCIe link per device, the rows around band boundaries copied aside first. */
+int sc_single_pass_host_multi_f32(float *const *image_planes, float *const *workspace_planes, int nplanes,
+                                  int rows, int cols, const float *dense, int width, int flags,
+                                  const int *devices, int ndev);
+
 /* horizontal_pass / vertical_pass on HOST planes (S/conv.py:362-389): dst[valid] :=
  * the row pass (vertical = 0) or the column pass (vertical != 0) of src over rows
  * [r, R-r) and columns [r, C-r); dst elsewhere keeps its values; dst must not

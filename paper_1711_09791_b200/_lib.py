@@ -65,6 +65,7 @@ EXPORTS = (
     "sc_two_pass_host_f32",
     "sc_two_pass_host_split_f32",
     "sc_single_pass_host_f32",
+    "sc_single_pass_host_multi_f32",
     "sc_pass_host_f32",
     "sc_host_register",
     "sc_host_unregister",
@@ -129,6 +130,7 @@ _SIGNATURES = {
     "sc_two_pass_host_split_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_single_pass_host_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_pass_host_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
+    "sc_single_pass_host_multi_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _i32], _i32),
     "sc_two_pass_host_band_f32": ([_vp, _vp, _i32, _i32, _i32, _i32, _i32, _fp, _i32, _i32, _i32], _i32),
     "sc_two_pass_host_multi_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _i32], _i32),
     "sc_two_pass_host_multi_split_f32": ([_vp, _vp, _i32, _i32, _i32, _fp, _i32, _i32, _vp, _i32], _i32),

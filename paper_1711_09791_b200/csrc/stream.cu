@@ -752,13 +752,13 @@ extern "C" int sc_two_pass_host_band_f32(const float* const* src_planes, float* 
 // overwritten. A device listed twice runs its bands one after the other.
 static int host_multi(const float* const* src_planes, float* const* dst_planes, float* const* scr_planes,
                       int nplanes, int rows, int cols, const float* taps, int width, int flags, const int* devices,
-                      int ndev) {
+                      int ndev, const float* dense = nullptr, float* const* dst2 = nullptr) {
     set_error("");
     if (!devices || ndev < 1) {
         set_error("need at least one device");
         return SC_INVALID_ARGUMENT;
     }
-    if (!src_planes || !dst_planes || !taps || nplanes < 1 || rows < 1 || cols < 1) {
+    if (!src_planes || !dst_planes || (!taps && !dense) || nplanes < 1 || rows < 1 || cols < 1) {
         set_error("null pointer or non-positive dimension");
         return SC_INVALID_ARGUMENT;
     }
@@ -769,6 +769,8 @@ static int host_multi(const float* const* src_planes, float* const* dst_planes, 
     if (nb == 1) {
         HostJob j{src_planes, dst_planes, scr_planes, nplanes, rows, cols, 0, rows, taps, width, flags, devices[0],
                   nullptr, nullptr};
+        j.dense = dense;
+        j.dst2 = dst2;
         return host_band(j);
     }
     std::vector<int> lo(nb + 1);
@@ -796,6 +798,8 @@ static int host_multi(const float* const* src_planes, float* const* dst_planes, 
         HostJob j{src_planes, dst_planes, scr_planes, nplanes, rows, cols, lo[g], lo[g + 1], taps, width, flags,
                   devices[g % ndev], g > 0 && r > 0 ? top.data() : nullptr,
                   g + 1 < nb && r > 0 ? bot.data() : nullptr};
+        j.dense = dense;
+        j.dst2 = dst2;
         rcs[g] = host_band(j);
         errs[g] = sc_last_error();
     };
@@ -810,6 +814,20 @@ static int host_multi(const float* const* src_planes, float* const* dst_planes, 
         }
     set_error("");
     return SC_OK;
+}
+
+// sc_single_pass_host_f32 over several GPUs from one process (row bands, as
+// sc_two_pass_host_multi_f32: the rows around every band boundary are copied aside
+// first, so copy-back in place never reads rows a neighbouring band has rewritten).
+extern "C" int sc_single_pass_host_multi_f32(float* const* image_planes, float* const* workspace_planes, int nplanes,
+                                             int rows, int cols, const float* dense, int width, int flags,
+                                             const int* devices, int ndev) {
+    if (!workspace_planes || !dense) {
+        set_error("null workspace planes or matrix");
+        return SC_INVALID_ARGUMENT;
+    }
+    return host_multi(image_planes, workspace_planes, nullptr, nplanes, rows, cols, nullptr, width, 0, devices, ndev,
+                      dense, (flags & SC_COPY_BACK) ? image_planes : nullptr);
 }
 
 // One process, several GPUs (the reference's single-process plan model): the

@@ -482,7 +482,7 @@ def two_pass_host_split(image_planes, scratch_planes, taps, *, extended: bool = 
 
 
 def single_pass_host(image_planes, workspace_planes, dense, *, copy_back: bool = False, device: int = 0,
-                     register: bool = True) -> None:
+                     register: bool = True, devices=None) -> None:
     """convolve_image's single-pass variants on HOST planes (S/executors.py:327-356):
     workspace_planes[valid] := the dense fold of image_planes; with copy_back the
     same samples also go back into image_planes[valid] in place. Everything else
@@ -498,6 +498,16 @@ def single_pass_host(image_planes, workspace_planes, dense, *, copy_back: bool =
     if not ptrs_img or len(ptrs_img) != len(ptrs_ws):
         raise InvalidArgumentError("need matching, non-empty image and workspace plane lists")
     L = _lib.load()
+    flags = _lib.SC_COPY_BACK if copy_back else 0
+    if devices is not None and len(list(devices)) > 1:  # row bands through several GPUs from this process
+        devs = [int(d) for d in devices]
+        arr_dev = (ctypes.c_int * len(devs))(*devs)
+        _lib.check(L.sc_single_pass_host_multi_f32(_ptr_array(ptrs_img), _ptr_array(ptrs_ws), len(ptrs_img), shape[0],
+                                                   shape[1], _fp(m), m.shape[0], flags,
+                                                   ctypes.cast(arr_dev, ctypes.c_void_p), len(devs)))
+        return
+    if devices is not None and len(list(devices)) == 1:
+        device = int(list(devices)[0])
     _lib.check(L.sc_single_pass_host_f32(_ptr_array(ptrs_img), _ptr_array(ptrs_ws), len(ptrs_img), shape[0],
                                          shape[1], _fp(m), m.shape[0], _lib.SC_COPY_BACK if copy_back else 0,
                                          int(device)))

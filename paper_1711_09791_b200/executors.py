@@ -208,7 +208,7 @@ def convolve_image(image: Image, kernel: SeparableKernel, variant: ConvVariant, 
             # streamed like the two-pass: workspace[valid] (and image[valid] with
             # copy-back) written in place, nothing else touched
             dev.single_pass_host(img_planes, ws_planes, outer_product(kernel).matrix, copy_back=copy_back,
-                                 device=device_index, register=plan.register_host)
+                                 device=device_index, register=plan.register_host, devices=plan.devices)
 
     stats.wall_time_ns = time.perf_counter_ns() - t0
     stats.parallel_region_launches = _lib.launch_count() - before

@@ -119,6 +119,29 @@ def test_host_row_and_column_pass_streamed(dev, oracle, small_chunks, kind, widt
     assert bits_equal(as_np(src), x)
 
 
+@pytest.mark.parametrize("ndev", [2, 3])
+@pytest.mark.parametrize("copy_back", [False, True])
+def test_host_single_pass_multi_device(dev, oracle, small_chunks, ndev, copy_back):
+    """sc_single_pass_host_multi_f32: row bands through several devices from one
+    process (here the same device listed several times), copy-back in place."""
+    rng = np.random.default_rng(ndev)
+    R, C, width = 149, 120, 5
+    r = width // 2
+    dense = rng.uniform(-1, 1, size=(width, width)).astype(np.float32)
+    x = oracle.synthetic(3 * R * C, 90, kind=2).reshape(3, R, C)
+    img = planes_of(x, "pageable")
+    ws = planes_of(np.full_like(x, -3.0), "pinned")
+    dev.single_pass_host(img, ws, dense, copy_back=copy_back, devices=[0] * ndev)
+    want = oracle.single_pass(x, dense)
+    exp_ws = np.full_like(x, -3.0)
+    exp_ws[:, r:R - r, r:C - r] = want[:, r:R - r, r:C - r]
+    assert bits_equal(as_np(ws), exp_ws)
+    exp_img = x.copy()
+    if copy_back:
+        exp_img[:, r:R - r, r:C - r] = want[:, r:R - r, r:C - r]
+    assert bits_equal(as_np(img), exp_img)
+
+
 def test_host_single_pass_default_chunks_and_checks(dev, oracle):
     """Default chunking on a plane large enough for several chunks, through
     convolve_image on numpy planes (the drop-in call); aliased workspaces are refused."""
