@@ -849,6 +849,9 @@ def main():
         # (timed on its own) and stays registered while it lives, so later calls DMA
         # straight from it
         first_ms = timed(Cuda(device=local), 1)
+        # (buffers below 64 MB are staged on first use and page-locked when they come
+        # back: the second call pays it, also untimed)
+        second_ms = timed(Cuda(device=local), 1)
         reg_ms = timed(Cuda(device=local), args.e2e_steps)
         # (b) never registered: every call stages through the pinned ring
         from paper_1711_09791_b200.device import host_registry
@@ -859,9 +862,9 @@ def main():
         st_ms = timed(staged, args.e2e_steps)
         e2e_pageable = {"value": round(total_px / (reg_ms / 1e3) / 1e9, 4), "unit": "Gpix/s",
                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(reg_ms, 3),
-                        "first_call_ms": round(first_ms, 3),
+                        "first_call_ms": round(first_ms, 3), "second_call_ms": round(second_ms, 3),
                         "path": call + " on pageable numpy planes; the buffer is page-locked on the first call "
-                                       "(first_call_ms) and kept registered while it lives",
+                                       "(64 MB and more; smaller ones on the second) and kept registered while it lives",
                         "staged": {"value": round(total_px / (st_ms / 1e3) / 1e9, 4), "ms_per_step": round(st_ms, 3),
                                    "path": "Cuda(register_host=False): every call through the library's pinned "
                                            "staging ring (host copy threads, non-temporal stores)"}}

@@ -379,6 +379,44 @@ def test_host_registry_lifetime_and_bits(dev, oracle):
     assert reg.total == 0
 
 
+def test_host_registry_small_buffers_on_second_use(dev, oracle):
+    """Buffers below the 64 MB floor are staged on first use and page-locked when the
+    same live buffer comes back (a reps loop); both paths give the same bits; a freed
+    buffer is forgotten."""
+    import gc
+
+    from paper_1711_09791_b200.device import HostRegistry, host_registry
+
+    reg = HostRegistry()
+    a = np.zeros((3, 700, 1024), np.float32)  # 8.6 MB
+    reg.new_call()
+    assert not reg.pin(a[0]) and not reg.pin(a[1]) and not reg.registered(a)  # first call: every plane staged
+    reg.new_call()
+    assert reg.pin(a[1]) and reg.registered(a)              # second call: registered (the root buffer)
+    assert reg.pin(a[2]) and len(reg._regs) == 1
+    del a
+    gc.collect()
+    assert reg.total == 0 and not reg._regs and not reg._seen
+    b = np.zeros((256, 1024), np.float32)  # 1 MB: seen once, then freed
+    assert not reg.pin(b)
+    del b
+    gc.collect()
+    assert not reg._seen
+    assert not reg.pin(np.zeros((100, 100), np.float32)) and not reg._seen  # below 1 MB: never tracked
+    # end to end: three calls on the same small image, bit-exact on the staged and the registered path
+    w = np.array([1, 4, 6, 4, 1], np.float32) / np.float32(16)
+    x = oracle.synthetic(3 * 600 * 1024, 4, kind=1).reshape(3, 600, 1024)
+    want = oracle.two_pass(x, w)
+    buf = x.copy()
+    host_registry.clear()
+    for call in range(3):
+        buf[...] = x
+        dev.two_pass_host([buf[p] for p in range(3)], [buf[p] for p in range(3)], w)
+        assert bits_equal(buf, want)
+        assert host_registry.registered(buf) == (call >= 1)
+    host_registry.clear()
+
+
 def test_host_registry_budget_evicts_lru(dev):
     from paper_1711_09791_b200.device import HostRegistry
 
